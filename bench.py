@@ -1,0 +1,410 @@
+#!/usr/bin/env python
+"""Benchmark of the J-DOB hot path on B200 (driver contract: one JSON line from rank 0).
+
+Step (N GPUs, weak scaling): every rank solves its own slice of the workload
+(default C2: 2^20 instances of 10 VGG-16 users per GPU, BASELINE.json configs[1])
+through the C ABI: jdob_solve_batch (K0 aggregates + K1 J-DOB solve incl. LC +
+K4 statistics) and jdob_eval re-verifying every plan (K3); the statistics are
+then all-reduced over NCCL (the path's only exchange step).  Inputs are resident
+in HBM before the timed region and are larger than L2.
+
+Extra legs in the same line: "bruteforce" (C4 exhaustive search, 2.75e10
+candidates, index space sharded over the ranks, NCCL MIN-allreduce of (E, idx)),
+"e2e" (jdob_solve_batch_host from pinned host buffers, copies inside the timed
+region), "cpu_baseline" (the C oracle on a bounded sample on the host cores),
+"roofline" (FP64-pipe work of K1 from the literal Alg. 2 counters / its live
+CUDA-event duration, against the FP64 peak of DESIGN.md §Roofline).
+
+--impl reference times the CPU oracle (the reference arm of this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import jdobgen as G  # noqa: E402
+
+# FP64-pipe instructions of one correctly rounded double division in the sm_100a SASS of
+# the solve kernel (MUFU.RCP64H + DFMA/DMUL refinement + checks).
+W_DIV = 9
+PEAK_FP64_SM_PER_CLK = 64      # FP64 lanes per SM per clock (B200), DESIGN.md §Roofline
+N_SMS = 148
+
+WORKLOADS = {
+    "c2": ("c2_vgg16_m10_identical_beta0-35", 1 << 20),
+    "c3": ("c3_resnet18_m4-20_mixed_deadlines", 100_000),
+    "c5": ("c5_montecarlo_m1-32_3models_5regimes_3grids", 1_000_000),
+}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="mine", choices=["mine", "reference"])
+    p.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    p.add_argument("--n-inst", type=int, default=None, help="instances per GPU")
+    p.add_argument("--no-bf", action="store_true")
+    p.add_argument("--bf-reps", type=int, default=2)
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=10.0)
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------------------------
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            if len(r) >= 9:
+                for nm, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def fp64_work(batch, counts, mode_nts=None):
+    """FP64-pipe lane-instructions of K1's algorithmic work.
+
+    Per instance, from the literal Alg. 2 counters (n_visit, n_eval, n_member):
+      LC                     M (1 div + 6)
+      per n~ < N (setup)     M (3 div + 6) + M(M-1)/2 compares + M suffix-min
+      per visited (n~, j)    2 div (1/f_e, guard) + 3
+      per evaluated (n~, j)  (M - B_o) adds + 5 (edge term, compare)
+      per member evaluation  1 div + 8 (budget 2, clamp 2, energy 3, sum 1)
+    """
+    M = np.diff(batch.user_off).astype(np.float64)
+    N = np.array([batch.models[m].N for m in batch.model_id], np.float64)
+    visit, ev, mem = (counts[:, 0].astype(np.float64), counts[:, 1].astype(np.float64),
+                      counts[:, 2].astype(np.float64))
+    div = M + N * 3 * M + 2 * visit + mem
+    other = 6 * M + N * (6 * M + M * (M - 1) / 2 + M) + 3 * visit + (ev * M - mem) + 5 * ev + 8 * mem
+    return float(np.sum(div * W_DIV + other)), float(np.sum(div)), float(np.sum(other))
+
+
+def cpu_baseline(batch, seconds, label):
+    """The oracle, as it stands, on a bounded sample of the same workload, all host cores."""
+    import oracle as O
+    cores = os.cpu_count() or 1
+    probe = batch.subset(0, min(batch.n_inst, 2000))
+    t0 = time.perf_counter()
+    O.solve_batch(probe, threads=cores)
+    rate = probe.n_inst / max(time.perf_counter() - t0, 1e-6)
+    n = int(min(batch.n_inst, max(probe.n_inst, rate * seconds)))
+    sub = batch.subset(0, n)
+    t0 = time.perf_counter()
+    O.solve_batch(sub, threads=cores)
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "instances/s", "cores": cores, "kind": "oracle",
+            "sample": f"first {n} instances of {label} ({dt:.1f} s, C oracle -O2, {cores} threads)"}
+
+
+def bf_leg(J, torch, world, rank, reps, dist):
+    """C4 exhaustive search, contiguous vector-aligned index ranges per rank."""
+    b = G.config_batch("c4")
+    db = J.DeviceBatch(b)
+    k = G.grid_size(float(b.fe_min[0]), float(b.fe_max[0]), float(b.rho[0]))
+    N, M = b.models[0].N, b.M(0)
+    size = J.bf_space_size(0, N, M, k)
+    V = size // k
+    lo = (V * rank // world) * k
+    hi = (V * (rank + 1) // world) * k
+    J.bruteforce(db, 0, lo, min(hi, lo + 64 * 1024 * k))     # warm-up (small)
+    torch.cuda.synchronize()
+    times = []
+    res = None
+    for _ in range(reps):
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        E, I, S = J.bruteforce(db, 0, lo, hi)
+        if dist:
+            Eg = E.clone()
+            dist.all_reduce(Eg, op=dist.ReduceOp.MIN)
+            Ic = torch.where(E == Eg, I, torch.full_like(I, 2 ** 62))
+            dist.all_reduce(Ic, op=dist.ReduceOp.MIN)
+            E, I = Eg, Ic
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e)
+        if dist:
+            t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        times.append(ms)
+        res = (float(E.item()), int(I.item()), int(S.item()))
+    ms = float(np.median(times))
+    return {"metric": "brute-force candidates/s", "value": size / (ms / 1e3), "unit": "candidates/s",
+            "workload": "c4_resnet18_m8_12pp_k64_general", "candidates": size, "ms": ms, "reps": reps,
+            "scaling": "strong", "E_min": res[0], "idx_min": res[1], "status": res[2],
+            "gpu_launches_per_rep": 5}
+
+
+def run_mine(args):
+    import torch
+    world, rank, local = dist_env()
+    dist = None
+    if world > 1:
+        import torch.distributed as D
+        D.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = D
+    torch.cuda.set_device(local)
+    import paper_2504_14611_b200 as J
+    label, n_default = WORKLOADS[args.workload]
+    n = args.n_inst or n_default
+    batch = G.config_batch(args.workload, n_inst=n, inst_begin=rank * n)
+    n_buckets = int(batch.meta.get("n_buckets", 32))
+    db = J.DeviceBatch(batch)
+    torch.cuda.synchronize()
+
+    # untimed: algorithmic work counters (literal Alg. 2 counts, checked against the oracle in tests)
+    res_c = J.solve_batch(db, counts=True, f_user=False)
+    counts = res_c["counts"].cpu().numpy()
+    work, n_div, n_other = fp64_work(batch, counts)
+    # parity spot check against the oracle on 64 sampled instances (rank 0)
+    parity = None
+    if rank == 0:
+        import oracle as O
+        idx = np.linspace(0, n - 1, 64).astype(np.int64)
+        orc = O.solve_batch(batch.take(idx))
+        ok = all(np.array_equal(res_c[f].cpu().numpy()[idx].view(np.int64 if res_c[f].dtype == torch.float64
+                                                                       else np.int32),
+                                orc[f].view(np.int64 if orc[f].dtype == np.float64 else np.int32))
+                 for f in ("E", "t_free_next", "f_e", "n_tilde", "j", "status", "mask"))
+        parity = f"{'64/64' if ok else 'MISMATCH'} sampled instances bit-exact vs oracle"
+    del res_c
+
+    res = J.solve_batch(db, stats=True, n_buckets=n_buckets, f_user=False)
+    ev = J.eval_plans(db, plans=res, f_user=False)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        J.solve_batch(db, stats=True, n_buckets=n_buckets, f_user=False, out=res)
+        J.eval_plans(db, plans=res, f_user=False, out=ev)
+        if dist:
+            st = res["stats"]
+            red = st.clone()
+            dist.all_reduce(red, op=dist.ReduceOp.SUM)
+            mx = st[:, 3].contiguous()
+            mn = st[:, 4].contiguous()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            dist.all_reduce(mn, op=dist.ReduceOp.MIN)
+            red[:, 3] = mx
+            red[:, 4] = mn
+            res["stats_global"] = red
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    K = args.steps
+    ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    t_s, t_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_s.record(stream)
+    for i in range(K):
+        ev_s[i].record(stream)
+        J.solve_batch(db, stats=True, n_buckets=n_buckets, f_user=False, out=res)
+        ev_e[i].record(stream)
+        J.eval_plans(db, plans=res, f_user=False, out=ev)
+        if dist:
+            st = res["stats"]
+            red = st.clone()
+            dist.all_reduce(red, op=dist.ReduceOp.SUM)
+            mx = st[:, 3].contiguous()
+            mn = st[:, 4].contiguous()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            dist.all_reduce(mn, op=dist.ReduceOp.MIN)
+    t_e.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    total_ms = t_s.elapsed_time(t_e)
+    solve_ms = float(np.mean([a.elapsed_time(b) for a, b in zip(ev_s, ev_e)]))
+    viol = int((ev["violations"] != 0).sum().item())
+    if dist:
+        t = torch.tensor([total_ms, solve_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, solve_ms = float(t[0]), float(t[1])
+        w = torch.tensor([work], device="cuda", dtype=torch.float64)
+        dist.all_reduce(w, op=dist.ReduceOp.MAX)   # per-GPU work of the slowest rank's kind
+    value = world * n * K / (total_ms / 1e3)
+
+    # end-to-end through the public host-buffer API (copies inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        hb = J.HostBuffers(batch, stats=True, n_buckets=n_buckets)
+        J.solve_batch_host(hb)
+        reps = max(1, min(K, 3))
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        for _ in range(reps):
+            h2d, d2h = J.solve_batch_host(hb)
+        e.record(stream)
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e)
+        if dist:
+            t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        e2e = {"value": world * n * reps / (ms / 1e3), "unit": "instances/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "api": "jdob_solve_batch_host (pinned host buffers)", "reps": reps}
+        del hb
+
+    bf = None
+    if not args.no_bf:
+        bf = bf_leg(J, torch, world, rank, args.bf_reps, dist)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(batch, args.cpu_seconds, label)
+
+    if rank == 0:
+        peak_clk = (clk or {}).get("sm_max_mhz") or 1965.0
+        peak = N_SMS * PEAK_FP64_SM_PER_CLK * peak_clk * 1e6 / 1e9   # G FP64-pipe lane-instr/s
+        achieved = work / (solve_ms / 1e3) / 1e9
+        line = {
+            "metric": "J-DOB instances solved/s",
+            "value": value,
+            "unit": "instances/s",
+            "n_gpus": world,
+            "steps": K,
+            "warmup": args.warmup,
+            "ms_per_step": total_ms / K,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (jdobgen seeded generator, paper-shaped profiles; DESIGN.md §Input recipe)",
+            "config": {"workload": label, "n_inst_per_gpu": n, "global_instances": world * n,
+                       "users_per_gpu": int(batch.n_users), "input_bytes_per_gpu": int(batch.nbytes()),
+                       "l2": "inputs larger than L2 (126 MB)" if batch.nbytes() > 126e6 else "inputs fit in L2",
+                       "step": "jdob_solve_batch (K0+K1+K4 stats) + jdob_eval of every plan (K3) + NCCL stats allreduce",
+                       "parallelism": f"dp{world}"},
+            "roofline": {"bound": "alu", "kernel": "k_solve (K1)", "achieved": achieved, "peak": peak,
+                         "unit": "G FP64-pipe lane-instr/s", "frac": achieved / peak, "traffic": None,
+                         "work_per_launch": work, "div_per_launch": n_div, "w_div": W_DIV,
+                         "launch_ms": solve_ms,
+                         "peak_note": "148 SMs x 64 FP64 lanes/clk x max SM clock (DESIGN.md §Roofline)"},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": 6 * K,
+            "clocks": clk,
+            "bruteforce": bf,
+            "plan_violations": viol,
+            "parity": parity,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    """Reference arm of this tier: the CPU oracle, as it stands, on the host cores."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle as O
+    label, n_default = WORKLOADS[args.workload]
+    n = args.n_inst or n_default
+    cores = os.cpu_count() or 1
+    # each step: a bounded sample of the workload (different instances per step)
+    probe = G.config_batch(args.workload, n_inst=1000, inst_begin=0)
+    t0 = time.perf_counter()
+    O.solve_batch(probe, threads=cores)
+    rate = probe.n_inst / max(time.perf_counter() - t0, 1e-6)
+    per_step = int(max(1000, min(n, rate * 60.0 / max(args.steps + args.warmup, 1))))
+    batch = G.config_batch(args.workload, n_inst=per_step * (args.steps + args.warmup), inst_begin=0)
+    for w in range(args.warmup):
+        O.solve_batch(batch.subset(w * per_step, (w + 1) * per_step), threads=cores)
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        i0 = (args.warmup + s) * per_step
+        O.solve_batch(batch.subset(i0, i0 + per_step), threads=cores)
+    dt = time.perf_counter() - t0
+    value = per_step * args.steps / dt
+    line = {"metric": "J-DOB instances solved/s", "value": value, "unit": "instances/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": label, "n_inst_per_step": per_step, "parallelism": f"host x{cores} threads"},
+            "cpu_baseline": {"value": value, "unit": "instances/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{per_step} instances of {label} per step"},
+            "e2e": {"value": value, "unit": "instances/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_mine(a)

@@ -1,0 +1,247 @@
+/*
+ * jdob.h -- C ABI of the B200-native J-DOB hot path (libjdob.so).
+ *
+ * Method: Xu, Zhou, Niu, "Joint Optimization of Offloading, Batching and DVFS for
+ * Multiuser Co-Inference" (arXiv 2504.14611).  "P:n" cites /root/reference/PAPER.md
+ * line n; R1..R16 are the readings listed in DESIGN.md §Readings; the arithmetic
+ * contract (operation order, no FMA contraction, IEEE division) is DESIGN.md
+ * §Arithmetic contract.  Every entry point is asynchronous on the caller's stream
+ * unless stated otherwise.
+ *
+ * Conventions for every entry point
+ *  - Plain C types only.  Pointers documented "device" must point to device memory
+ *    valid on the current device; "host" pointers to host memory.
+ *  - The caller owns every buffer.  The library allocates nothing that outlives a
+ *    call (jdob_solve_batch_host allocates and frees its own stream-ordered
+ *    device buffers inside the call).
+ *  - Return value: JDOB_OK, or a call-level error (JDOB_EINVAL bad shape/pointer/
+ *    limit detectable on the host, JDOB_ECUDA a CUDA launch/runtime failure).  The
+ *    message of the last error of the calling thread is jdob_last_error().
+ *  - Value errors inside the data are reported per instance in `status`
+ *    (JDOB_ST_*), never by aborting: the instance's outputs are then the local-
+ *    computing (LC) answer (n~* = N, j* = 0, mask 0), or NaN energies when the
+ *    instance or its model is malformed.
+ *  - No exceptions cross the ABI; the library never calls exit/abort.
+ *  - Frequencies in Hz, times in s, data sizes in bits, workloads in MAC/FLOP,
+ *    powers in W, energies in J (§II).
+ */
+#ifndef JDOB_H
+#define JDOB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define JDOB_API __attribute__((visibility("default")))
+#else
+#define JDOB_API
+#endif
+
+#define JDOB_MAX_M 32          /* users per instance (M' of Alg. 1)                 */
+#define JDOB_MAX_N 63          /* sub-tasks per DNN (N)                        */
+#define JDOB_MAX_K 65536       /* edge-frequency grid points per instance (k) */
+#define JDOB_STATS_FIELDS 80   /* doubles per statistics bucket (a12)               */
+#define JDOB_MAX_BUCKETS 64
+
+/* call-level return codes */
+enum { JDOB_OK = 0, JDOB_EINVAL = 1, JDOB_ETOOBIG = 2, JDOB_ECUDA = 3 };
+
+/* per-instance status codes (same numbering as the oracle) */
+enum {
+    JDOB_ST_OK = 0,
+    JDOB_ST_LOCAL_INFEASIBLE = 1, /* zeta sum(gA)/f_max > T for some user        */
+    JDOB_ST_REQUIRE = 2,          /* min_m T_m < t_free: Alg. 1 Require violated  */
+    JDOB_ST_BADPARAM = 3,         /* M out of [1, min(32, B_max)], non-finite or out-of-box
+                                     user/edge parameters, k > JDOB_MAX_K                 */
+    JDOB_ST_BADMODEL = 4,         /* model tables invalid (A_0 != 0, A_n <= 0, d not
+                                     positive non-decreasing in b, c < 0, ...)           */
+    JDOB_ST_TOOBIG = 5            /* brute-force index space >= 2^62                      */
+};
+
+/* solver modes (§IV benchmarks) */
+enum {
+    JDOB_MODE_FULL = 0,         /* Alg. 1 + Alg. 2                                         */
+    JDOB_MODE_LC = 1,           /* local computing only (benchmark (i))                    */
+    JDOB_MODE_NO_EDGE_DVFS = 2, /* f_e fixed at f_e,max (k = 1)                            */
+    JDOB_MODE_BINARY = 3        /* n~ restricted to {0, N}                                 */
+};
+
+/*
+ * One DNN profile (§II-B, Eq. (5)).  Host struct whose
+ * array members are DEVICE pointers.
+ *   A, O, g, q : [N+1] doubles; index 0 is the virtual input layer (A[0] = 0,
+ *                O[0] = input size).  A_n workload, O_n output bits, g_n/q_n
+ *                latency/energy block factors of Eqs. (1)-(2).
+ *   d, c       : row-major [(N+1) x (B_max+1)] doubles, element n*(B_max+1)+b =
+ *                d_n(b), c_n(b) of Eq. (5); rows n = 0 and columns b = 0 unused.
+ */
+typedef struct {
+    int32_t N, B_max; /* 1 <= N <= 63, 1 <= B_max <= 32 */
+    const double *A, *O, *g, *q;
+    const double *d, *c;
+} jdob_model;
+
+/*
+ * A batch of independent co-inference instances, users in CSR layout (struct of
+ * arrays; DESIGN.md §Data layout).  All array members are DEVICE pointers.
+ *   model_id [n_inst]      : index into the models[] array of the call.
+ *   user_off [n_inst+1]    : users of instance i are user_off[i] .. user_off[i+1]-1;
+ *                            M_i = user_off[i+1] - user_off[i] must be in [1, 32].
+ *   zeta, kappa, f_min, f_max, R, p_u, T [user_off[n_inst]] : per-user zeta_m
+ *                            (cycles/workload), kappa_m (switched capacitance),
+ *                            f_m,min/max (Hz), R_m (bit/s), p_m^u (W), T_m^(d) (s)
+ *                            (P:116-138).
+ *   t_free, fe_min, fe_max, rho [n_inst] : GPU-available time t_free, edge
+ *                            frequency box and sweep step rho of Alg. 2 (P:155,
+ *                            P:326-348).
+ *   bucket [n_inst]        : optional statistics bucket in [0, n_buckets); NULL =
+ *                            bucket M_i - 1.
+ */
+typedef struct {
+    int64_t n_inst;
+    int32_t n_models;
+    const int32_t *model_id;
+    const int64_t *user_off;
+    const double *zeta, *kappa, *f_min, *f_max, *R, *p_u, *T;
+    const double *t_free, *fe_min, *fe_max, *rho;
+    const int32_t *bucket;
+} jdob_batch;
+
+/*
+ * Outputs of jdob_solve_batch, DEVICE pointers, caller-allocated.
+ *   E [n_inst]           : E_* of Alg. 1, the (P1) objective of the plan.
+ *   E_lc [n_inst]        : local-computing energy (benchmark (i)).
+ *   t_free_next [n_inst] : t_free,* (D22); t_free when all-local.
+ *   f_e [n_inst]         : chosen edge frequency; 0.0 when all-local.
+ *   n_tilde [n_inst]     : identical partition point n~*; N when all-local (R4, R8).
+ *   j [n_inst]           : grid index of f_e (f_e = fe_max - j*rho); 0 when all-local.
+ *   status [n_inst]      : JDOB_ST_*.
+ *   mask [n_inst]        : offloading set M'_o, bit m = user m of the instance.
+ *   f_user [user_off[n_inst]] : optional (NULL = skip) device frequencies f_m* (D20).
+ *   counts [3*n_inst]    : optional (NULL = skip) literal Alg. 2 work counters per
+ *                          instance: (n~, j) pairs visited, pairs evaluated (guard
+ *                          passed), sum of B_o over evaluated pairs.
+ *   stats [n_buckets * JDOB_STATS_FIELDS] : optional (NULL = skip) energy-saving
+ *                          statistics (a12, R16), fields per bucket:
+ *                          [0] #OK instances, [1] sum r, [2] sum r^2, [3] max r,
+ *                          [4] min r, [5] sum E/M, [6] sum E_lc/M, [7] #offloading,
+ *                          [8] #status != OK, [9+n] #instances with n~* = n (n <= 63);
+ *                          r = 100 (E_lc - E) / E_lc.  Deterministic for a given
+ *                          n_inst (fixed reduction tree).
+ */
+typedef struct {
+    double *E, *E_lc, *t_free_next, *f_e;
+    int32_t *n_tilde, *j, *status;
+    uint32_t *mask;
+    double *f_user;
+    int64_t *counts;
+    double *stats;
+    int32_t n_buckets; /* 1 .. JDOB_MAX_BUCKETS when stats != NULL */
+} jdob_result;
+
+/*
+ * Bytes of caller-provided device workspace needed by jdob_solve_batch /
+ * jdob_eval (which = 0) or jdob_bruteforce (which = 1) for these models (a HOST
+ * array of n_models descriptors; only N and B_max are read).  Returns 0 on bad
+ * arguments.
+ */
+JDOB_API size_t jdob_workspace_bytes(const jdob_model *models, int32_t n_models, int32_t which);
+
+/*
+ * J-DOB over a batch of independent instances (rows a1-a8, a12 of DESIGN.md §Scope):
+ * model aggregates u, v, phi, psi; per instance LC energy (P:296,
+ * P:303), then Alg. 1: for n~ = 0..N-1 gamma, the sort by
+ * descending gamma (R2 tie-break), thresholds Eq. (fth) (R1), the Alg. 2
+ * edge-frequency sweep with greedy-batching set updates, the D6
+ * guard, closed forms D20-D22 and strict-minimum updates; n~ = N is
+ * local computing (R4).  Results are bit-identical to the CPU oracle under the
+ * arithmetic contract.
+ *   models   : HOST array of n_models descriptors (device table pointers).
+ *   b        : HOST struct of DEVICE arrays; b->n_models == n_models.
+ *   mode     : JDOB_MODE_*.
+ *   out      : HOST struct of DEVICE output arrays.
+ *   ws, ws_bytes : DEVICE workspace of >= jdob_workspace_bytes(models, n_models, 0).
+ *   stream   : cudaStream_t as void* (NULL = legacy default stream).
+ * Errors: JDOB_EINVAL (NULL required pointer, n_models < 1, N/B_max out of range,
+ * small workspace, bad mode, n_buckets out of range), JDOB_ECUDA.
+ */
+JDOB_API int jdob_solve_batch(const jdob_model *models, int32_t n_models, const jdob_batch *b, int32_t mode,
+                     const jdob_result *out, void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * Same computation from HOST buffers (the end-to-end public call): copies the
+ * model tables and the batch host->device, solves, copies E, E_lc, t_free_next,
+ * f_e, n_tilde, j, status, mask (and f_user/stats when non-NULL) back to the host
+ * arrays of `out`, and synchronises `stream` before returning.  Every pointer in
+ * models/b/out is a HOST pointer (pinned memory gives asynchronous copies).
+ * Device memory is stream-ordered (cudaMallocAsync) and freed before returning.
+ * If `h2d_bytes`/`d2h_bytes` are non-NULL they receive the bytes copied.
+ */
+JDOB_API int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob_batch *b, int32_t mode,
+                          const jdob_result *out, void *stream, int64_t *h2d_bytes, int64_t *d2h_bytes);
+
+/*
+ * Exhaustive search (rows a9-a10): argmin of the energy over candidate indices
+ * [idx_begin, idx_end) of ONE instance (b->n_inst == 1), lowest index on ties.
+ *   space 0 (general, reading R14): idx = vec*k + j with vec = sum_m n_m (N+1)^(M-1-m),
+ *           n_m in {0..N} the partition point of user m (N = local), same-sub-task
+ *           greedy batching b_n = #{m : n_m < n} (Fig. 1 caption P:75), ALAP batch
+ *           starts, exact D6'/D7'/D13 feasibility.
+ *   space 1 (identical, the (P1) space of P:224): idx = ((n~ 2^M + mask) k + j);
+ *           n~ = N means all local.
+ *   k = number of grid points f_e(j) = fe_max - j*rho >= fe_min.
+ * Outputs (DEVICE scalars): *E_min (+inf if no feasible candidate in range),
+ * *idx_min (-1 if none), *status (JDOB_ST_*; the search runs for OK and REQUIRE).
+ * Ranges beyond the space size are clipped.  Deterministic.  Unlike the other entry
+ * points this call performs one small synchronous device->host read (user_off[0..1]
+ * and model_id[0], 20 bytes) on `stream` to select the kernel specialisation for M;
+ * the search itself is asynchronous.
+ * Errors: JDOB_EINVAL (n_inst != 1, NULL pointers, idx_begin > idx_end, small
+ * workspace), JDOB_ECUDA.
+ */
+JDOB_API int jdob_bruteforce(const jdob_model *models, int32_t n_models, const jdob_batch *b, int32_t space,
+                    uint64_t idx_begin, uint64_t idx_end, double *E_min, int64_t *idx_min, int32_t *status,
+                    void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * Host helper: size of the brute-force index space of an instance with N, M, k
+ * (0 when >= 2^62).  Pure host arithmetic.
+ */
+JDOB_API uint64_t jdob_bf_space_size(int32_t space, int32_t N, int32_t M, int64_t k);
+
+/*
+ * Configuration evaluator (row a11): for given partition vectors and edge
+ * frequencies, E (D21 generalised), t_free_next (D22 generalised, ASAP, R15),
+ * device frequencies f* (D20) and violation bits: bit0 D6, bit1 any D7, bit2 any
+ * D8, bit3 non-positive device budget, bit4 Require, bit5 f_e out of box.  A
+ * constraint lhs <= rhs is violated when lhs > rhs + slack*|rhs|.
+ * Used to re-verify every plan jdob_solve_batch returns.
+ *   partition [user_off[n_inst]] (device int32): n_m in {0..N}, N = local; or NULL,
+ *     in which case the configurations are identical-offloading plans given by
+ *     plan_n_tilde [n_inst] and plan_mask [n_inst] (the n_tilde/mask outputs of
+ *     jdob_solve_batch: user m offloads after block n~ iff bit m of mask is set).
+ *   f_e [n_inst] (device): edge frequency per instance (ignored if all local).
+ *   E, t_free_next [n_inst], f_user [users] (may be NULL), violations [n_inst],
+ *   status [n_inst]: device outputs.
+ *   ws: workspace of >= jdob_workspace_bytes(models, n_models, 0) bytes.
+ * Errors: JDOB_EINVAL (NULL arrays, small workspace), JDOB_ECUDA.
+ */
+JDOB_API int jdob_eval(const jdob_model *models, int32_t n_models, const jdob_batch *b, const int32_t *partition,
+                       const int32_t *plan_n_tilde, const uint32_t *plan_mask, const double *f_e, double slack,
+                       double *E, double *t_free_next, double *f_user, uint32_t *violations, int32_t *status,
+                       void *ws, size_t ws_bytes, void *stream);
+
+/* Message of the last call-level error on this thread ("" if none). */
+JDOB_API const char *jdob_last_error(void);
+
+/* Library version string. */
+JDOB_API const char *jdob_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* JDOB_H */

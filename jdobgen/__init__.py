@@ -377,7 +377,7 @@ def random_batch(seed: int, n_inst: int, M_lo: int = 1, M_hi: int = 8, N_lo: int
             return int(choice(dr(user, fld), a, b))
         M = ch(0, 0, M_lo, M_hi)
         N = ch(0, 1, N_lo, N_hi)
-        B_max = M + ch(0, 2, 0, B_extra)
+        B_max = min(32, M + ch(0, 2, 0, B_extra))
         A = [0.0] + [float(round(un(n, 10, 0.2, 3.0) * 1e8)) for n in range(1, N + 1)]
         O = [float(round(un(n, 11, 0.05, 1.5) * 1e6)) for n in range(0, N + 1)]
         g = [1.0] * (N + 1)

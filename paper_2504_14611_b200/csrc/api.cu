@@ -1,0 +1,395 @@
+// api.cu -- the C ABI of libjdob.so (include/jdob.h): argument checks, workspace
+// layout, model-aggregate setup (K0) and kernel launches.  No torch types, no
+// exceptions across the boundary, nothing allocated beyond a call.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "jdob_dev.cuh"
+#include "kernels.h"
+
+namespace jdob {
+void launch_bruteforce_impl(const DevModel *models, const DevBatch &b, int model_id, int N, int M, int space,
+                            unsigned long long idx_begin, unsigned long long idx_end, void *ws, double *E_min,
+                            long long *idx_min, int *status, cudaStream_t s);
+size_t bf_workspace_bytes();
+}  // namespace jdob
+
+using namespace jdob;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+static int cuda_check(const char *where) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(JDOB_ECUDA, "%s: %s", where, cudaGetErrorString(e));
+    return JDOB_OK;
+}
+
+static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static size_t model_table_bytes(const jdob_model &m) {
+    const size_t n1 = (size_t)m.N + 1, b1 = (size_t)m.B_max + 1;
+    return 2 * al(n1 * sizeof(double)) + 4 * al(n1 * b1 * sizeof(double)) + al(sizeof(int));
+}
+
+static size_t stats_partial_bytes() {
+    return al((size_t)kStatsBlocks * JDOB_MAX_BUCKETS * kStatsF * sizeof(double));
+}
+
+static int check_models(const jdob_model *models, int32_t n_models) {
+    if (!models) return fail(JDOB_EINVAL, "models is NULL");
+    if (n_models < 1) return fail(JDOB_EINVAL, "n_models = %d < 1", n_models);
+    for (int i = 0; i < n_models; i++) {
+        const jdob_model &m = models[i];
+        if (m.N < 1 || m.N > JDOB_MAX_N) return fail(JDOB_EINVAL, "model %d: N = %d outside [1, %d]", i, m.N, JDOB_MAX_N);
+        if (m.B_max < 1 || m.B_max > JDOB_MAX_M)
+            return fail(JDOB_EINVAL, "model %d: B_max = %d outside [1, %d]", i, m.B_max, JDOB_MAX_M);
+        if (!m.A || !m.O || !m.g || !m.q || !m.d || !m.c) return fail(JDOB_EINVAL, "model %d: NULL table", i);
+    }
+    return JDOB_OK;
+}
+
+static size_t models_bytes(const jdob_model *models, int32_t n_models) {
+    size_t s = al((size_t)n_models * sizeof(DevModel));
+    for (int i = 0; i < n_models; i++) s += model_table_bytes(models[i]);
+    return s;
+}
+
+// Lays out the model part of the workspace and launches K0 (validation + aggregates).
+static int prepare_models(const jdob_model *models, int32_t n_models, char *ws, DevModel **dev_models,
+                          cudaStream_t s) {
+    DevModel *dst = (DevModel *)ws;
+    char *p = ws + al((size_t)n_models * sizeof(DevModel));
+    ModelChunk chunk;
+    chunk.count = 0;
+    chunk.dst = dst;
+    for (int i = 0; i < n_models; i++) {
+        const jdob_model &m = models[i];
+        const size_t n1 = (size_t)m.N + 1, b1 = (size_t)m.B_max + 1;
+        DevModel d;
+        d.N = m.N;
+        d.B1 = m.B_max + 1;
+        d.A = m.A;
+        d.O = m.O;
+        d.g = m.g;
+        d.q = m.q;
+        d.d = m.d;
+        d.c = m.c;
+        d.u = (double *)p;
+        p += al(n1 * sizeof(double));
+        d.v = (double *)p;
+        p += al(n1 * sizeof(double));
+        d.phi = (double *)p;
+        p += al(n1 * b1 * sizeof(double));
+        d.psi = (double *)p;
+        p += al(n1 * b1 * sizeof(double));
+        d.dA = (double *)p;
+        p += al(n1 * b1 * sizeof(double));
+        d.cA = (double *)p;
+        p += al(n1 * b1 * sizeof(double));
+        d.valid = (int *)p;
+        p += al(sizeof(int));
+        chunk.m[chunk.count++] = d;
+        if (chunk.count == kChunkModels || i == n_models - 1) {
+            launch_aggregates(chunk, s);
+            chunk.dst += chunk.count;
+            chunk.count = 0;
+        }
+    }
+    *dev_models = dst;
+    return cuda_check("aggregates");
+}
+
+static int check_batch(const jdob_batch *b, int32_t n_models) {
+    if (!b) return fail(JDOB_EINVAL, "batch is NULL");
+    if (b->n_inst < 0) return fail(JDOB_EINVAL, "n_inst < 0");
+    if (b->n_models != n_models) return fail(JDOB_EINVAL, "batch n_models %d != %d", b->n_models, n_models);
+    if (b->n_inst > 0 && (!b->model_id || !b->user_off || !b->zeta || !b->kappa || !b->f_min || !b->f_max || !b->R ||
+                          !b->p_u || !b->T || !b->t_free || !b->fe_min || !b->fe_max || !b->rho))
+        return fail(JDOB_EINVAL, "batch has a NULL array");
+    return JDOB_OK;
+}
+
+static DevBatch to_dev(const jdob_batch *b) {
+    DevBatch d;
+    d.n_inst = b->n_inst;
+    d.n_models = b->n_models;
+    d.model_id = b->model_id;
+    d.user_off = (const long long *)b->user_off;
+    d.zeta = b->zeta;
+    d.kappa = b->kappa;
+    d.f_min = b->f_min;
+    d.f_max = b->f_max;
+    d.R = b->R;
+    d.p_u = b->p_u;
+    d.T = b->T;
+    d.t_free = b->t_free;
+    d.fe_min = b->fe_min;
+    d.fe_max = b->fe_max;
+    d.rho = b->rho;
+    d.bucket = b->bucket;
+    return d;
+}
+
+static int num_sms() {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+}
+
+extern "C" {
+
+const char *jdob_last_error(void) { return g_err.c_str(); }
+
+const char *jdob_version(void) { return "jdob-b200 0.1 (sm_100a)"; }
+
+size_t jdob_workspace_bytes(const jdob_model *models, int32_t n_models, int32_t which) {
+    if (!models || n_models < 1) return 0;
+    for (int i = 0; i < n_models; i++)
+        if (models[i].N < 1 || models[i].N > JDOB_MAX_N || models[i].B_max < 1 || models[i].B_max > JDOB_MAX_M)
+            return 0;
+    size_t s = models_bytes(models, n_models);
+    if (which == 0) return s + stats_partial_bytes();
+    if (which == 1) return s + al(bf_workspace_bytes());
+    return 0;
+}
+
+uint64_t jdob_bf_space_size(int32_t space, int32_t N, int32_t M, int64_t k) {
+    if (N < 1 || M < 1 || M > JDOB_MAX_M || k < 1) return 0;
+    const unsigned long long lim = 1ull << 62;
+    unsigned long long s = (unsigned long long)k;
+    if (space == 0) {
+        for (int m = 0; m < M; m++) {
+            if (s > lim / (unsigned long long)(N + 1)) return 0;
+            s *= (unsigned long long)(N + 1);
+        }
+    } else if (space == 1) {
+        unsigned long long f = (unsigned long long)(N + 1) << M;
+        if (s > lim / f) return 0;
+        s *= f;
+    } else {
+        return 0;
+    }
+    return s;
+}
+
+int jdob_solve_batch(const jdob_model *models, int32_t n_models, const jdob_batch *b, int32_t mode,
+                     const jdob_result *out, void *ws, size_t ws_bytes, void *stream) {
+    g_err.clear();
+    int rc = check_models(models, n_models);
+    if (rc) return rc;
+    if ((rc = check_batch(b, n_models))) return rc;
+    if (mode < JDOB_MODE_FULL || mode > JDOB_MODE_BINARY) return fail(JDOB_EINVAL, "bad mode %d", mode);
+    if (!out) return fail(JDOB_EINVAL, "out is NULL");
+    if (b->n_inst > 0 && (!out->E || !out->E_lc || !out->t_free_next || !out->f_e || !out->n_tilde || !out->j ||
+                          !out->status || !out->mask))
+        return fail(JDOB_EINVAL, "result has a NULL required array");
+    if (out->stats && (out->n_buckets < 1 || out->n_buckets > JDOB_MAX_BUCKETS))
+        return fail(JDOB_EINVAL, "n_buckets = %d outside [1, %d]", out->n_buckets, JDOB_MAX_BUCKETS);
+    const size_t need = jdob_workspace_bytes(models, n_models, 0);
+    if (!ws || ws_bytes < need) return fail(JDOB_EINVAL, "workspace %zu bytes < %zu", ws_bytes, need);
+    cudaStream_t s = (cudaStream_t)stream;
+    DevModel *dm = nullptr;
+    if ((rc = prepare_models(models, n_models, (char *)ws, &dm, s))) return rc;
+    DevBatch db = to_dev(b);
+    DevResult dr;
+    dr.E = out->E;
+    dr.E_lc = out->E_lc;
+    dr.t_free_next = out->t_free_next;
+    dr.f_e = out->f_e;
+    dr.n_tilde = out->n_tilde;
+    dr.j = out->j;
+    dr.status = out->status;
+    dr.mask = out->mask;
+    dr.f_user = out->f_user;
+    dr.counts = (long long *)out->counts;
+    launch_solve(dm, db, dr, mode, s, num_sms());
+    if ((rc = cuda_check("solve"))) return rc;
+    if (out->stats) {
+        double *partials = (double *)((char *)ws + models_bytes(models, n_models));
+        launch_stats(db, dr, partials, out->stats, out->n_buckets, s);
+        if ((rc = cuda_check("stats"))) return rc;
+    }
+    return JDOB_OK;
+}
+
+int jdob_eval(const jdob_model *models, int32_t n_models, const jdob_batch *b, const int32_t *partition,
+              const int32_t *plan_n_tilde, const uint32_t *plan_mask, const double *f_e, double slack, double *E,
+              double *t_free_next, double *f_user, uint32_t *violations, int32_t *status, void *ws, size_t ws_bytes,
+              void *stream) {
+    g_err.clear();
+    int rc = check_models(models, n_models);
+    if (rc) return rc;
+    if ((rc = check_batch(b, n_models))) return rc;
+    if (b->n_inst > 0 && ((!partition && (!plan_n_tilde || !plan_mask)) || !f_e || !E || !t_free_next ||
+                          !violations || !status))
+        return fail(JDOB_EINVAL, "eval: NULL array");
+    const size_t need = jdob_workspace_bytes(models, n_models, 0);
+    if (!ws || ws_bytes < need) return fail(JDOB_EINVAL, "workspace %zu bytes < %zu", ws_bytes, need);
+    cudaStream_t s = (cudaStream_t)stream;
+    DevModel *dm = nullptr;
+    if ((rc = prepare_models(models, n_models, (char *)ws, &dm, s))) return rc;
+    launch_eval(dm, to_dev(b), partition, plan_n_tilde, plan_mask, f_e, slack, E, t_free_next, f_user, violations,
+                status, s);
+    return cuda_check("eval");
+}
+
+int jdob_bruteforce(const jdob_model *models, int32_t n_models, const jdob_batch *b, int32_t space,
+                    uint64_t idx_begin, uint64_t idx_end, double *E_min, int64_t *idx_min, int32_t *status, void *ws,
+                    size_t ws_bytes, void *stream) {
+    g_err.clear();
+    int rc = check_models(models, n_models);
+    if (rc) return rc;
+    if ((rc = check_batch(b, n_models))) return rc;
+    if (b->n_inst != 1) return fail(JDOB_EINVAL, "bruteforce needs n_inst == 1 (got %lld)", (long long)b->n_inst);
+    if (space != 0 && space != 1) return fail(JDOB_EINVAL, "bad space %d", space);
+    if (idx_begin > idx_end) return fail(JDOB_EINVAL, "idx_begin > idx_end");
+    if (!E_min || !idx_min || !status) return fail(JDOB_EINVAL, "bruteforce: NULL output");
+    const size_t need = jdob_workspace_bytes(models, n_models, 1);
+    if (!ws || ws_bytes < need) return fail(JDOB_EINVAL, "workspace %zu bytes < %zu", ws_bytes, need);
+    cudaStream_t s = (cudaStream_t)stream;
+    // one small synchronous read: M and the model id select the kernel specialisation
+    long long off[2] = {0, 0};
+    int mid = 0;
+    cudaMemcpyAsync(off, b->user_off, sizeof(off), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(&mid, b->model_id, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_check("bruteforce: read user_off");
+    const int M = (int)(off[1] - off[0]);
+    const int N = (mid >= 0 && mid < n_models) ? models[mid].N : 1;
+    DevModel *dm = nullptr;
+    if ((rc = prepare_models(models, n_models, (char *)ws, &dm, s))) return rc;
+    void *bws = (char *)ws + models_bytes(models, n_models);
+    launch_bruteforce_impl(dm, to_dev(b), (mid >= 0 && mid < n_models) ? mid : 0, N, M, space, idx_begin, idx_end,
+                           bws, E_min, (long long *)idx_min, status, s);
+    return cuda_check("bruteforce");
+}
+
+int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob_batch *b, int32_t mode,
+                          const jdob_result *out, void *stream, int64_t *h2d_bytes, int64_t *d2h_bytes) {
+    g_err.clear();
+    if (!models || n_models < 1) return fail(JDOB_EINVAL, "models");
+    for (int i = 0; i < n_models; i++) {
+        if (models[i].N < 1 || models[i].N > JDOB_MAX_N || models[i].B_max < 1 || models[i].B_max > JDOB_MAX_M)
+            return fail(JDOB_EINVAL, "model %d: N/B_max out of range", i);
+        if (!models[i].A || !models[i].O || !models[i].g || !models[i].q || !models[i].d || !models[i].c)
+            return fail(JDOB_EINVAL, "model %d: NULL table", i);
+    }
+    int rc = check_batch(b, n_models);
+    if (rc) return rc;
+    if (!out || !out->E || !out->E_lc || !out->t_free_next || !out->f_e || !out->n_tilde || !out->j ||
+        !out->status || !out->mask)
+        return fail(JDOB_EINVAL, "result has a NULL required array");
+    cudaStream_t s = (cudaStream_t)stream;
+    const long long n = b->n_inst;
+    const long long nu = n > 0 ? (long long)b->user_off[n] : 0;
+    // device layout: model tables | batch | outputs | workspace
+    size_t bytes = 0;
+    for (int i = 0; i < n_models; i++) {
+        const size_t n1 = (size_t)models[i].N + 1, b1 = (size_t)models[i].B_max + 1;
+        bytes += 4 * al(n1 * 8) + 2 * al(n1 * b1 * 8);
+    }
+    const size_t in_inst = al(n * 4) + al((n + 1) * 8) + 4 * al(n * 8) + (b->bucket ? al(n * 4) : 0);
+    const size_t in_user = 7 * al(nu * 8);
+    const size_t outb = 4 * al(n * 8) + 4 * al(n * 4) + (out->f_user ? al(nu * 8) : 0) +
+                        (out->counts ? al(n * 3 * 8) : 0) +
+                        (out->stats ? al((size_t)out->n_buckets * JDOB_STATS_FIELDS * 8) : 0);
+    const size_t wsb = jdob_workspace_bytes(models, n_models, 0);
+    bytes += in_inst + in_user + outb + al(wsb);
+    char *base = nullptr;
+    if (cudaMallocAsync((void **)&base, bytes, s) != cudaSuccess) return cuda_check("cudaMallocAsync");
+    char *p = base;
+    long long h2d = 0, d2h = 0;
+    auto put = [&](const void *src, size_t nb) -> void * {
+        void *d = p;
+        if (nb) cudaMemcpyAsync(d, src, nb, cudaMemcpyHostToDevice, s);
+        h2d += (long long)nb;
+        p += al(nb);
+        return d;
+    };
+    auto take = [&](size_t nb) -> void * {
+        void *d = p;
+        p += al(nb);
+        return d;
+    };
+    jdob_model dmods[64];
+    jdob_model *dm = n_models <= 64 ? dmods : new jdob_model[n_models];
+    for (int i = 0; i < n_models; i++) {
+        const size_t n1 = (size_t)models[i].N + 1, b1 = (size_t)models[i].B_max + 1;
+        dm[i].N = models[i].N;
+        dm[i].B_max = models[i].B_max;
+        dm[i].A = (const double *)put(models[i].A, n1 * 8);
+        dm[i].O = (const double *)put(models[i].O, n1 * 8);
+        dm[i].g = (const double *)put(models[i].g, n1 * 8);
+        dm[i].q = (const double *)put(models[i].q, n1 * 8);
+        dm[i].d = (const double *)put(models[i].d, n1 * b1 * 8);
+        dm[i].c = (const double *)put(models[i].c, n1 * b1 * 8);
+    }
+    jdob_batch db = *b;
+    db.model_id = (const int32_t *)put(b->model_id, n * 4);
+    db.user_off = (const int64_t *)put(b->user_off, (n + 1) * 8);
+    db.zeta = (const double *)put(b->zeta, nu * 8);
+    db.kappa = (const double *)put(b->kappa, nu * 8);
+    db.f_min = (const double *)put(b->f_min, nu * 8);
+    db.f_max = (const double *)put(b->f_max, nu * 8);
+    db.R = (const double *)put(b->R, nu * 8);
+    db.p_u = (const double *)put(b->p_u, nu * 8);
+    db.T = (const double *)put(b->T, nu * 8);
+    db.t_free = (const double *)put(b->t_free, n * 8);
+    db.fe_min = (const double *)put(b->fe_min, n * 8);
+    db.fe_max = (const double *)put(b->fe_max, n * 8);
+    db.rho = (const double *)put(b->rho, n * 8);
+    db.bucket = b->bucket ? (const int32_t *)put(b->bucket, n * 4) : nullptr;
+    jdob_result dr = *out;
+    dr.E = (double *)take(n * 8);
+    dr.E_lc = (double *)take(n * 8);
+    dr.t_free_next = (double *)take(n * 8);
+    dr.f_e = (double *)take(n * 8);
+    dr.n_tilde = (int32_t *)take(n * 4);
+    dr.j = (int32_t *)take(n * 4);
+    dr.status = (int32_t *)take(n * 4);
+    dr.mask = (uint32_t *)take(n * 4);
+    dr.f_user = out->f_user ? (double *)take(nu * 8) : nullptr;
+    dr.counts = out->counts ? (int64_t *)take(n * 3 * 8) : nullptr;
+    dr.stats = out->stats ? (double *)take((size_t)out->n_buckets * JDOB_STATS_FIELDS * 8) : nullptr;
+    void *ws = take(wsb);
+    rc = jdob_solve_batch(dm, n_models, &db, mode, &dr, ws, wsb, stream);
+    if (dm != dmods) delete[] dm;
+    if (rc == JDOB_OK) {
+        auto get = [&](void *dst, const void *src, size_t nb) {
+            if (nb) cudaMemcpyAsync(dst, src, nb, cudaMemcpyDeviceToHost, s);
+            d2h += (long long)nb;
+        };
+        get(out->E, dr.E, n * 8);
+        get(out->E_lc, dr.E_lc, n * 8);
+        get(out->t_free_next, dr.t_free_next, n * 8);
+        get(out->f_e, dr.f_e, n * 8);
+        get(out->n_tilde, dr.n_tilde, n * 4);
+        get(out->j, dr.j, n * 4);
+        get(out->status, dr.status, n * 4);
+        get(out->mask, dr.mask, n * 4);
+        if (out->f_user) get(out->f_user, dr.f_user, nu * 8);
+        if (out->counts) get(out->counts, dr.counts, n * 3 * 8);
+        if (out->stats) get(out->stats, dr.stats, (size_t)out->n_buckets * JDOB_STATS_FIELDS * 8);
+    }
+    cudaFreeAsync(base, s);
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (rc != JDOB_OK) return rc;
+    if (e != cudaSuccess) return fail(JDOB_ECUDA, "solve_batch_host: %s", cudaGetErrorString(e));
+    if (h2d_bytes) *h2d_bytes = h2d;
+    if (d2h_bytes) *d2h_bytes = d2h;
+    return JDOB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,318 @@
+// K2: exhaustive search over partition-point vectors x edge-grid points (rows a9-a10).
+//
+// Candidate idx = vec * k + j.  General space: vec = sum_m n_m (N+1)^(M-1-m) (user 0
+// most significant), n_m = N local.  Identical space ((P1)): vec = n~ 2^M + mask.
+// Objective and constraints: DESIGN.md reading R14 (same-sub-task greedy batching,
+// Fig. 1 caption P:75; ALAP batch starts; exact D6'/D7'/D13 feasibility, R10).
+//
+// Kernels: bf_setup (one warp: validation, k, LC terms, per-(n, user) hoists, 1/f_e
+// table) -> bf_main (persistent; lane = vector, inner loop over j; a vector's scan
+// stops at its first infeasible j, which is exact because D6' and D7' are monotone
+// in j -- DESIGN.md §Brute-force monotone stop) -> bf_final (fixed-order fold of the
+// per-block (E, idx) partials; lexicographic min = lowest index on ties).
+#include "jdob_dev.cuh"
+#include "kernels.h"
+
+namespace jdob {
+
+constexpr int kInvTab = 2048;  // 1/f_e(j) cached in shared memory for j < kInvTab
+
+// setup output, in the workspace
+struct BfHeader {
+    int status, M, N, B1;
+    long long k;
+    unsigned long long size;   // index-space size (0 when too big)
+    double t_free, fe_max, rho;
+};
+
+__global__ void k_bf_setup(const DevModel *models, DevBatch b, int space, BfHeader *hdr, double *tab /*[4][N+1][M]*/,
+                           double *user /*[4][32]: eloc fmin fmax T*/, double *invtab) {
+    const int lane = threadIdx.x & 31;
+    long long off, k;
+    int M;
+    const DevModel *mdp;
+    InstRegs x;
+    int st = warp_validate(models, b, 0, lane, x, M, k, mdp, off);
+    if (lane == 0) {
+        hdr->status = st;
+        hdr->M = M;
+        hdr->N = mdp ? mdp->N : 0;
+        hdr->B1 = mdp ? mdp->B1 : 0;
+        hdr->k = k;
+        hdr->size = 0ull;
+        hdr->t_free = b.t_free[0];
+        hdr->fe_max = b.fe_max[0];
+        hdr->rho = b.rho[0];
+    }
+    if (st != JDOB_ST_OK && st != JDOB_ST_REQUIRE) return;
+    const DevModel &md = *mdp;
+    const int N = md.N;
+    // index-space size (< 2^62)
+    if (lane == 0) {
+        const unsigned long long lim = 1ull << 62;
+        unsigned long long s = (unsigned long long)k;
+        bool big = false;
+        if (space == 0) {
+            for (int m = 0; m < M && !big; m++) {
+                if (s > lim / (unsigned long long)(N + 1)) big = true;
+                else s *= (unsigned long long)(N + 1);
+            }
+        } else {
+            unsigned long long f = (unsigned long long)(N + 1) << M;
+            if (s > lim / f) big = true;
+            else s *= f;
+        }
+        hdr->size = big ? 0ull : s;
+        if (big) hdr->status = JDOB_ST_TOOBIG;
+    }
+    const double vN = md.v[N], uN = md.u[N];
+    if (lane < M) {
+        const double floc = clampf((x.z * vN) / x.T, x.f0, x.f1);
+        user[0 * 32 + lane] = ((x.k * uN) * floc) * floc;
+        user[1 * 32 + lane] = x.f0;
+        user[2 * 32 + lane] = x.f1;
+        user[3 * 32 + lane] = x.T;
+        const int NM = (N + 1) * M;
+        for (int n = 0; n <= N; n++) {
+            const double OR = md.O[n] / x.R;
+            tab[0 * NM + n * M + lane] = OR;                  // O_n / R_m
+            tab[1 * NM + n * M + lane] = x.z * md.v[n];       // zeta_m v_n
+            tab[2 * NM + n * M + lane] = x.k * md.u[n];       // kappa_m u_n
+            tab[3 * NM + n * M + lane] = OR * x.p;            // (O_n / R_m) p_m
+        }
+    }
+    const long long kt = k < kInvTab ? k : kInvTab;
+    for (long long j = lane; j < kt; j += 32) invtab[j] = 1.0 / grid_fe(b.fe_max[0], b.rho[0], j);
+}
+
+template <int MAXM>
+__global__ void __launch_bounds__(kBfWarps * 32) k_bf_main(const DevModel *models, int model_id, int space,
+                                                           unsigned long long idx_begin, unsigned long long idx_end,
+                                                           const BfHeader *hdr, const double *tab,
+                                                           const double *user, const double *invtab,
+                                                           double *part_E, long long *part_idx) {
+    extern __shared__ double sm[];
+    const int st = hdr->status;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __shared__ double wE[kBfWarps];
+    __shared__ long long wI[kBfWarps];
+    double bestE = dinf();
+    long long bestI = -1;
+    if (st == JDOB_ST_OK || st == JDOB_ST_REQUIRE) {
+        const int M = hdr->M, N = hdr->N, B1 = hdr->B1;
+        const long long k = hdr->k;
+        const unsigned long long size = hdr->size;
+        const double t_free = hdr->t_free, fe_max = hdr->fe_max, rho = hdr->rho;
+        const DevModel &md = models[model_id];
+        const int NM = (N + 1) * M;
+        double *sOR = sm, *sZV = sm + NM, *sKU = sm + 2 * NM, *sUP = sm + 3 * NM;
+        double *sEl = sm + 4 * NM, *sFmin = sEl + 32, *sFmax = sEl + 64, *sT = sEl + 96;
+        double *sInv = sEl + 128;
+        const long long kt = k < kInvTab ? k : kInvTab;
+        for (int x = threadIdx.x; x < 4 * NM; x += blockDim.x) sm[x] = tab[x];
+        for (int x = threadIdx.x; x < 128; x += blockDim.x) sEl[x] = user[x];
+        for (long long x = threadIdx.x; x < kt; x += blockDim.x) sInv[x] = invtab[x];
+        __syncthreads();
+        if (idx_end > size) idx_end = size;
+        if (idx_begin < idx_end) {
+            const unsigned long long uk = (unsigned long long)k;
+            const unsigned long long vb = idx_begin / uk, ve = (idx_end + uk - 1) / uk;
+            const unsigned long long nvec = ve - vb;
+            const unsigned long long nchunks = (nvec + 31) / 32;
+            const unsigned long long gw = (unsigned long long)blockIdx.x * kBfWarps + w;
+            const unsigned long long nw = (unsigned long long)gridDim.x * kBfWarps;
+            const double *dA = md.dA, *cA = md.cA;
+            const unsigned long long radix = (unsigned long long)(N + 1);
+            for (unsigned long long c = gw; c < nchunks; c += nw) {
+                const unsigned long long vec = vb + c * 32 + lane;
+                if (vec >= ve) continue;
+                // decode the partition vector
+                int nv[MAXM];
+                if (space == 0) {
+                    unsigned long long t = vec;
+#pragma unroll
+                    for (int m = MAXM - 1; m >= 0; m--) {
+                        if (m < M) {
+                            nv[m] = (int)(t % radix);
+                            t /= radix;
+                        }
+                    }
+                    // (the loop walks m = M-1 .. 0 because m >= M entries are skipped)
+                } else {
+                    const unsigned long long mask = vec & ((1ull << M) - 1ull);
+                    const int nt = (int)(vec >> M);
+#pragma unroll
+                    for (int m = 0; m < MAXM; m++) nv[m] = (nt < N && ((mask >> m) & 1ull)) ? nt : N;
+                }
+                // batch sizes, suffix sums S_n and Psi (descending n), per-user S_{n_m + 1}
+                double Sm[MAXM];
+#pragma unroll
+                for (int m = 0; m < MAXM; m++) Sm[m] = 0.0;
+                double S = 0.0, Psi = 0.0, Smin = 0.0;
+                int nmin = N;
+                double l_o = dinf();
+#pragma unroll
+                for (int m = 0; m < MAXM; m++) {
+                    if (m < M && nv[m] < N) {
+                        if (nv[m] < nmin) nmin = nv[m];
+                        const double T = sT[m];
+                        if (T < l_o) l_o = T;
+                    }
+                }
+                for (int n = N; n >= 1; n--) {
+                    int bn = 0;
+#pragma unroll
+                    for (int m = 0; m < MAXM; m++) bn += (m < M && nv[m] < n) ? 1 : 0;
+                    if (bn > 0) {
+                        S = S + dA[n * B1 + bn];
+                        Psi = Psi + cA[n * B1 + bn];
+                    } else {
+                        S = S + 0.0;
+                        Psi = Psi + 0.0;
+                    }
+#pragma unroll
+                    for (int m = 0; m < MAXM; m++)
+                        if (m < M && nv[m] + 1 == n) Sm[m] = S;
+                    if (nmin + 1 == n) Smin = S;
+                }
+                const bool any = nmin < N;
+                const unsigned long long jlo = (vec == vb) ? idx_begin - vb * uk : 0ull;
+                const unsigned long long jhi = (vec == ve - 1) ? idx_end - (ve - 1) * uk : uk;
+                for (unsigned long long j = jlo; j < jhi; j++) {
+                    const double fe = grid_fe(fe_max, rho, (long long)j);
+                    const double inv = (j < (unsigned long long)kt) ? sInv[j] : 1.0 / fe;
+                    if (any && !(t_free + Smin * inv <= l_o)) break;  // D6' (monotone in j)
+                    double E = 0.0;
+                    bool feas = true;
+#pragma unroll
+                    for (int m = 0; m < MAXM; m++) {
+                        if (m >= M) break;
+                        const int n = nv[m];
+                        double e;
+                        if (n < N) {
+                            const int x = n * M + m;
+                            const double budget = (l_o - sOR[x]) - Sm[m] * inv;
+                            const double zv = sZV[x];
+                            double f;
+                            if (zv == 0.0) {
+                                if (!(budget >= 0.0)) {
+                                    feas = false;
+                                    break;
+                                }
+                                f = sFmin[m];
+                            } else {
+                                if (!(budget > 0.0)) {
+                                    feas = false;
+                                    break;
+                                }
+                                const double G = zv / budget;
+                                if (G > sFmax[m]) {
+                                    feas = false;
+                                    break;
+                                }
+                                f = (G < sFmin[m]) ? sFmin[m] : G;
+                            }
+                            e = ((sKU[x] * f) * f) + sUP[x];
+                        } else {
+                            e = sEl[m];
+                        }
+                        E = E + e;
+                    }
+                    if (!feas) break;  // D7' (monotone in j)
+                    E = E + (Psi * fe) * fe;
+                    if (E < bestE) {
+                        bestE = E;
+                        bestI = (long long)(vec * uk + j);
+                    }
+                }
+            }
+        }
+    }
+    // warp, then block argmin over (E, idx)
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+        double oE = __shfl_xor_sync(0xffffffffu, bestE, d);
+        long long oI = __shfl_xor_sync(0xffffffffu, bestI, d);
+        bool take = (oE < bestE) || (oE == bestE && oI >= 0 && (bestI < 0 || oI < bestI));
+        if (take) {
+            bestE = oE;
+            bestI = oI;
+        }
+    }
+    if (lane == 0) {
+        wE[w] = bestE;
+        wI[w] = bestI;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double E = wE[0];
+        long long I = wI[0];
+        for (int q = 1; q < kBfWarps; q++) {
+            if (wE[q] < E || (wE[q] == E && wI[q] >= 0 && (I < 0 || wI[q] < I))) {
+                E = wE[q];
+                I = wI[q];
+            }
+        }
+        part_E[blockIdx.x] = E;
+        part_idx[blockIdx.x] = I;
+    }
+}
+
+__global__ void k_bf_final(const BfHeader *hdr, const double *part_E, const long long *part_idx, int nblocks,
+                           double *E_min, long long *idx_min, int *status) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double E = dinf();
+    long long I = -1;
+    for (int q = 0; q < nblocks; q++) {
+        if (part_E[q] < E || (part_E[q] == E && part_idx[q] >= 0 && (I < 0 || part_idx[q] < I))) {
+            E = part_E[q];
+            I = part_idx[q];
+        }
+    }
+    *E_min = E;
+    *idx_min = I;
+    *status = hdr->status;
+}
+
+size_t bf_workspace_bytes() {
+    return 256 + sizeof(double) * (4 * 64 * 32 + 4 * 32 + kInvTab) + (sizeof(double) + sizeof(long long)) * kBfBlocks +
+           1024;
+}
+
+template <int MAXM>
+static void launch_main(const DevModel *models, int model_id, int space, unsigned long long ib, unsigned long long ie,
+                        const BfHeader *hdr, const double *tab, const double *user, const double *inv,
+                        double *part_E, long long *part_idx, size_t smem, cudaStream_t s) {
+    cudaFuncSetAttribute(k_bf_main<MAXM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_bf_main<MAXM><<<kBfBlocks, kBfWarps * 32, smem, s>>>(models, model_id, space, ib, ie, hdr, tab, user, inv,
+                                                         part_E, part_idx);
+}
+
+void launch_bruteforce_impl(const DevModel *models, const DevBatch &b, int model_id, int N, int M, int space,
+                            unsigned long long idx_begin, unsigned long long idx_end, void *ws, double *E_min,
+                            long long *idx_min, int *status, cudaStream_t s) {
+    char *p = (char *)ws;
+    BfHeader *hdr = (BfHeader *)p;
+    p += 256;
+    double *tab = (double *)p;
+    p += sizeof(double) * 4 * 64 * 32;
+    double *user = (double *)p;
+    p += sizeof(double) * 4 * 32;
+    double *inv = (double *)p;
+    p += sizeof(double) * kInvTab;
+    double *part_E = (double *)p;
+    p += sizeof(double) * kBfBlocks;
+    long long *part_idx = (long long *)p;
+    k_bf_setup<<<1, 32, 0, s>>>(models, b, space, hdr, tab, user, inv);
+    const int Mc = (M >= 1 && M <= kMaxM) ? M : 1;
+    const size_t smem = sizeof(double) * (4 * (size_t)(N + 1) * Mc + 128 + kInvTab);
+    if (Mc <= 8)
+        launch_main<8>(models, model_id, space, idx_begin, idx_end, hdr, tab, user, inv, part_E, part_idx, smem, s);
+    else if (Mc <= 16)
+        launch_main<16>(models, model_id, space, idx_begin, idx_end, hdr, tab, user, inv, part_E, part_idx, smem, s);
+    else
+        launch_main<32>(models, model_id, space, idx_begin, idx_end, hdr, tab, user, inv, part_E, part_idx, smem, s);
+    k_bf_final<<<1, 32, 0, s>>>(hdr, part_E, part_idx, kBfBlocks, E_min, idx_min, status);
+}
+
+}  // namespace jdob

@@ -1,0 +1,155 @@
+// K3: configuration evaluator (row a11): D20-D22 generalised to per-user
+// partition points (R14: same-sub-task greedy batching, ALAP batch starts; R15:
+// ASAP finishing time), with violation bits at a relative slack.
+// One thread per instance; the O(N) batch-size and suffix tables live in the
+// thread's local memory (this is a verification pass, not the inner loop).
+#include "jdob_dev.cuh"
+#include "kernels.h"
+
+namespace jdob {
+
+// n_m of user m (global user index u, local index m) of instance i: the given partition
+// vector, or the identical plan (n~, mask) of jdob_solve_batch.
+__device__ __forceinline__ int part_of(const int *partition, const int *plan_nt, const unsigned *plan_mask,
+                                       long long i, long long u, int m, int N) {
+    if (partition) return partition[u];
+    return ((plan_mask[i] >> m) & 1u) ? plan_nt[i] : N;
+}
+
+__global__ void k_eval(const DevModel *models, DevBatch b, const int *partition, const int *plan_nt,
+                       const unsigned *plan_mask, const double *f_e, double slack, double *E_out, double *tf_out,
+                       double *f_user, unsigned *viol_out, int *status_out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= b.n_inst) return;
+    const long long off = b.user_off[i];
+    const long long M64 = b.user_off[i + 1] - off;
+    const int mid = b.model_id[i];
+    const double t_free = b.t_free[i], fe_min = b.fe_min[i], fe_max = b.fe_max[i], rho = b.rho[i];
+    int st = JDOB_ST_OK;
+    if (mid < 0 || mid >= b.n_models) st = JDOB_ST_BADPARAM;
+    const DevModel *mdp = (st == JDOB_ST_OK) ? &models[mid] : nullptr;
+    if (st == JDOB_ST_OK && *mdp->valid == 0) st = JDOB_ST_BADMODEL;
+    if (st == JDOB_ST_OK && (M64 < 1 || M64 > kMaxM || M64 > mdp->B1 - 1)) st = JDOB_ST_BADPARAM;
+    const int M = (int)((M64 >= 1 && M64 <= kMaxM) ? M64 : 0);
+    const int N = mdp ? mdp->N : 0;
+    if (st == JDOB_ST_OK) {
+        for (int m = 0; m < M; m++) {
+            const long long u = off + m;
+            double z = b.zeta[u], k = b.kappa[u], f0 = b.f_min[u], f1 = b.f_max[u], R = b.R[u], p = b.p_u[u],
+                   T = b.T[u];
+            bool ok = dfinite(z) && dfinite(k) && dfinite(f0) && dfinite(f1) && dfinite(R) && dfinite(p) &&
+                      dfinite(T) && (z >= 0.0) && (k >= 0.0) && (f0 > 0.0) && (f0 <= f1) && (R > 0.0) &&
+                      (p >= 0.0) && (T > 0.0);
+            int nm = part_of(partition, plan_nt, plan_mask, i, u, m, N);
+            ok = ok && nm >= 0 && nm <= N;
+            if (!ok) st = JDOB_ST_BADPARAM;
+        }
+        bool ok = dfinite(t_free) && dfinite(fe_min) && dfinite(fe_max) && dfinite(rho) && (t_free >= 0.0) &&
+                  (fe_min > 0.0) && (fe_min <= fe_max) && (rho > 0.0);
+        if (!ok || grid_k(fe_min, fe_max, rho) > kMaxK) st = JDOB_ST_BADPARAM;
+    }
+    if (st == JDOB_ST_BADPARAM || st == JDOB_ST_BADMODEL) {
+        E_out[i] = dnan();
+        tf_out[i] = dnan();
+        viol_out[i] = 0u;
+        status_out[i] = st;
+        return;
+    }
+    const DevModel &md = *mdp;
+    const int B1 = md.B1;
+    const double vN = md.v[N], uN = md.u[N];
+    double Tmin = dinf();
+    for (int m = 0; m < M; m++) {
+        double T = b.T[off + m];
+        if ((b.zeta[off + m] * vN) / b.f_max[off + m] > T && st == JDOB_ST_OK) st = JDOB_ST_LOCAL_INFEASIBLE;
+        if (T < Tmin) Tmin = T;
+    }
+    if (st == JDOB_ST_OK && Tmin < t_free) st = JDOB_ST_REQUIRE;
+    unsigned viol = (Tmin < t_free) ? 16u : 0u;
+
+    int bcnt[kMaxN + 2];
+    double S[kMaxN + 2];
+    for (int n = 1; n <= N; n++) bcnt[n] = 0;
+    for (int m = 0; m < M; m++) {
+        int nm = part_of(partition, plan_nt, plan_mask, i, off + m, m, N);
+        for (int n = nm + 1; n <= N; n++) bcnt[n]++;  // b_n = #{m : n_m < n}
+    }
+    double Psi = 0.0;
+    S[N + 1] = 0.0;
+    for (int n = N; n >= 1; n--) {
+        const int bn = bcnt[n];
+        S[n] = S[n + 1] + (bn > 0 ? md.dA[n * B1 + bn] : 0.0);
+        Psi = Psi + (bn > 0 ? md.cA[n * B1 + bn] : 0.0);
+    }
+    bool any = false;
+    int nmin = N;
+    double l_o = dinf();
+    for (int m = 0; m < M; m++) {
+        int nm = part_of(partition, plan_nt, plan_mask, i, off + m, m, N);
+        if (nm < N) {
+            any = true;
+            if (nm < nmin) nmin = nm;
+            double T = b.T[off + m];
+            if (T < l_o) l_o = T;
+        }
+    }
+    const double fe = f_e[i];
+    const double inv = 1.0 / fe;
+    const double tol = slack * fabs(l_o);
+    double tf = t_free;
+    if (any) {
+        if (!(fe >= fe_min && fe <= fe_max)) viol |= 32u;
+        double start = t_free + S[nmin + 1] * inv;
+        if (start > l_o + tol) viol |= 1u;
+        tf = start;
+    }
+    double E = 0.0;
+    for (int m = 0; m < M; m++) {
+        const long long u = off + m;
+        const int nm = part_of(partition, plan_nt, plan_mask, i, u, m, N);
+        double e, f;
+        if (nm < N) {
+            double OR = md.O[nm] / b.R[u];
+            double zv = b.zeta[u] * md.v[nm];
+            double budget = (l_o - OR) - S[nm + 1] * inv;
+            if (zv == 0.0) {
+                if (budget < 0.0) viol |= 8u;
+                f = b.f_min[u];
+            } else if (budget > 0.0) {
+                f = clampf(zv / budget, b.f_min[u], b.f_max[u]);
+            } else {
+                viol |= 8u;
+                f = b.f_max[u];
+            }
+            e = ((b.kappa[u] * md.u[nm]) * f) * f + OR * b.p_u[u];
+            double arr = zv / f + OR;
+            double fin = arr + S[nm + 1] * inv;
+            if (fin > l_o + tol) viol |= 2u;
+            if (fin > tf) tf = fin;
+        } else {
+            double T = b.T[u];
+            f = clampf((b.zeta[u] * vN) / T, b.f_min[u], b.f_max[u]);
+            e = ((b.kappa[u] * uN) * f) * f;
+            if ((b.zeta[u] * vN) / f > T + slack * fabs(T)) viol |= 4u;
+        }
+        if (f_user) f_user[u] = f;
+        E = E + e;
+    }
+    E = E + (Psi * fe) * fe;
+    E_out[i] = E;
+    tf_out[i] = tf;
+    viol_out[i] = viol;
+    status_out[i] = st;
+}
+
+void launch_eval(const DevModel *models, const DevBatch &b, const int *partition, const int *plan_nt,
+                 const unsigned *plan_mask, const double *f_e, double slack, double *E, double *tf, double *f_user,
+                 unsigned *viol, int *status, cudaStream_t s) {
+    if (b.n_inst <= 0) return;
+    const int bs = 128;
+    long long grid = (b.n_inst + bs - 1) / bs;
+    k_eval<<<(unsigned)grid, bs, 0, s>>>(models, b, partition, plan_nt, plan_mask, f_e, slack, E, tf, f_user, viol,
+                                          status);
+}
+
+}  // namespace jdob

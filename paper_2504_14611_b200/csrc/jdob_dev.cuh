@@ -1,0 +1,144 @@
+// jdob_dev.cuh -- device-side data layout and helpers shared by the libjdob kernels.
+//
+// Compiled with --fmad=false: every double expression below rounds each operation
+// separately (IEEE-754 binary64, round-to-nearest-even), in the order fixed by
+// DESIGN.md §Arithmetic contract, so results are bit-identical to the CPU oracle.
+// Explicit __fma_rn() is used only where DESIGN.md §Exact shortcuts proves the
+// result bit-identical to the contract's plain expression.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/jdob.h"
+
+namespace jdob {
+
+constexpr int kMaxM = JDOB_MAX_M;
+constexpr int kMaxN = JDOB_MAX_N;
+constexpr int kMaxK = JDOB_MAX_K;
+constexpr int kStatsF = JDOB_STATS_FIELDS;
+
+// Device-side model descriptor: user tables + aggregate tables built by K0 in the
+// caller's workspace (DESIGN.md §Data layout).  All tables are row-major by n.
+struct DevModel {
+    int N, B1;                                // B1 = B_max + 1
+    const double *A, *O, *g, *q, *d, *c;      // inputs
+    double *u, *v;                            // [N+1]  prefix sums
+    double *phi, *psi;                        // [(N+1)*B1] phi_n~(b), psi_n~(b)
+    double *dA, *cA;                          // [(N+1)*B1] d_n(b) A_n, c_n(b) A_n
+    int *valid;                               // 1 = model passed validation
+};
+
+struct DevBatch {
+    long long n_inst;
+    int n_models;
+    const int *model_id;
+    const long long *user_off;
+    const double *zeta, *kappa, *f_min, *f_max, *R, *p_u, *T;
+    const double *t_free, *fe_min, *fe_max, *rho;
+    const int *bucket;
+};
+
+struct DevResult {
+    double *E, *E_lc, *t_free_next, *f_e;
+    int *n_tilde, *j, *status;
+    unsigned *mask;
+    double *f_user;
+    long long *counts;
+};
+
+__device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
+__device__ __forceinline__ double dnan() { return __longlong_as_double(0x7ff8000000000000LL); }
+__device__ __forceinline__ bool dfinite(double x) { return isfinite(x); }
+
+// D20 clamp: min{max{G, f_min}, f_max} -- same comparison order as the oracle.
+__device__ __forceinline__ double clampf(double G, double fmin, double fmax) {
+    double x = (G < fmin) ? fmin : G;
+    return (x > fmax) ? fmax : x;
+}
+
+// Edge grid (R7): f_e(j) = f_e,max - j*rho, one multiply then one subtract.
+__device__ __forceinline__ double grid_fe(double fe_max, double rho, long long j) {
+    return __dsub_rn(fe_max, __dmul_rn((double)j, rho));
+}
+
+// k = #{j >= 0 : f_e(j) >= f_e,min}; the predicate is monotone in j, so a binary
+// search over [0, kMaxK + 1] finds the first failing j exactly (equals the oracle's
+// literal walk).  Returns kMaxK + 1 when the grid is longer than kMaxK.
+__device__ __forceinline__ long long grid_k(double fe_min, double fe_max, double rho) {
+    long long lo = 0, hi = kMaxK + 1;  // answer in [lo, hi]
+    if (grid_fe(fe_max, rho, hi) >= fe_min) return kMaxK + 1;
+    while (lo < hi) {
+        long long mid = (lo + hi) >> 1;
+        if (grid_fe(fe_max, rho, mid) >= fe_min) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+struct InstRegs {  // lane-resident user parameters (lane = user)
+    double z, k, f0, f1, R, p, T;
+};
+
+// Warp-cooperative load and validation of instance i (lane = user), with the same
+// predicates and precedence as the oracle's check_inst: BADMODEL, then BADPARAM
+// (model id, M range, user boxes, edge boxes, grid length), then LOCAL_INFEASIBLE
+// (P:127), then REQUIRE.  Lanes >= M get T = +inf and zeros.
+__device__ __forceinline__ int warp_validate(const DevModel *models, const DevBatch &b, long long i, int lane,
+                                             InstRegs &x, int &M, long long &k, const DevModel *&mdp,
+                                             long long &off) {
+    off = b.user_off[i];
+    const long long M64 = b.user_off[i + 1] - off;
+    M = (M64 >= 1 && M64 <= kMaxM) ? (int)M64 : 0;
+    k = 0;
+    x.z = x.k = x.f0 = x.f1 = x.R = x.p = 0.0;
+    x.T = dinf();
+    const int mid = b.model_id[i];
+    if (mid < 0 || mid >= b.n_models) {
+        mdp = nullptr;
+        return JDOB_ST_BADPARAM;
+    }
+    mdp = &models[mid];
+    if (*mdp->valid == 0) return JDOB_ST_BADMODEL;
+    if (M64 < 1 || M64 > kMaxM || M64 > mdp->B1 - 1) return JDOB_ST_BADPARAM;
+    bool ok = true;
+    if (lane < M) {
+        const long long u = off + lane;
+        x.z = b.zeta[u];
+        x.k = b.kappa[u];
+        x.f0 = b.f_min[u];
+        x.f1 = b.f_max[u];
+        x.R = b.R[u];
+        x.p = b.p_u[u];
+        x.T = b.T[u];
+        ok = dfinite(x.z) && dfinite(x.k) && dfinite(x.f0) && dfinite(x.f1) && dfinite(x.R) && dfinite(x.p) &&
+             dfinite(x.T);
+        ok = ok && (x.z >= 0.0) && (x.k >= 0.0) && (x.f0 > 0.0) && (x.f0 <= x.f1) && (x.R > 0.0) &&
+             (x.p >= 0.0) && (x.T > 0.0);
+    }
+    if (__any_sync(0xffffffffu, !ok)) return JDOB_ST_BADPARAM;
+    const double t_free = b.t_free[i], fe_min = b.fe_min[i], fe_max = b.fe_max[i], rho = b.rho[i];
+    if (!(dfinite(t_free) && dfinite(fe_min) && dfinite(fe_max) && dfinite(rho) && (t_free >= 0.0) &&
+          (fe_min > 0.0) && (fe_min <= fe_max) && (rho > 0.0)))
+        return JDOB_ST_BADPARAM;
+    k = grid_k(fe_min, fe_max, rho);
+    if (k > kMaxK) return JDOB_ST_BADPARAM;
+    const double vN = mdp->v[mdp->N];
+    const bool infeas = (lane < M) && ((x.z * vN) / x.f1 > x.T);
+    if (__any_sync(0xffffffffu, infeas)) return JDOB_ST_LOCAL_INFEASIBLE;
+    double Tmin = x.T;
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+        double o = __shfl_xor_sync(0xffffffffu, Tmin, d);
+        Tmin = (o < Tmin) ? o : Tmin;
+    }
+    if (Tmin < t_free) return JDOB_ST_REQUIRE;
+    return JDOB_ST_OK;
+}
+
+__device__ __forceinline__ double shfl_d(double x, int src, unsigned mask = 0xffffffffu) {
+    return __shfl_sync(mask, x, src);
+}
+
+}  // namespace jdob

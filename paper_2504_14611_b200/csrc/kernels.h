@@ -1,0 +1,37 @@
+// kernels.h -- internal launch interface between the C-ABI layer (api.cu) and the kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "jdob_dev.cuh"
+
+namespace jdob {
+
+constexpr int kChunkModels = 8;  // model descriptors passed by value per K0 launch
+
+struct ModelChunk {
+    int count;
+    DevModel m[kChunkModels];
+    DevModel *dst;  // where K0 publishes the descriptors (workspace)
+};
+
+// Launch geometry of the solve kernel (one warp per instance, persistent grid).
+constexpr int kSolveWarps = 4;
+constexpr int kStatsBlocks = 296;    // fixed => deterministic statistics tree
+constexpr int kStatsWarps = 2;
+constexpr int kBfBlocks = 148 * 8;   // persistent brute-force grid
+constexpr int kBfWarps = 4;
+
+void launch_aggregates(const ModelChunk &chunk, cudaStream_t s);
+void launch_solve(const DevModel *models, const DevBatch &b, const DevResult &r, int mode, cudaStream_t s,
+                  int num_sms);
+void launch_stats(const DevBatch &b, const DevResult &r, double *partials, double *stats, int n_buckets,
+                  cudaStream_t s);
+void launch_eval(const DevModel *models, const DevBatch &b, const int *partition, const int *plan_nt,
+                 const unsigned *plan_mask, const double *f_e, double slack,
+                 double *E, double *tf, double *f_user, unsigned *viol, int *status, cudaStream_t s);
+void launch_bruteforce(const DevModel *models, const DevBatch &b, int space, unsigned long long idx_begin,
+                       unsigned long long idx_end, double *part_E, long long *part_idx, double *E_min,
+                       long long *idx_min, int *status, cudaStream_t s);
+
+}  // namespace jdob

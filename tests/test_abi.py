@@ -1,0 +1,85 @@
+"""CPU-side checks of the C ABI: the library builds, loads and exports every symbol
+include/jdob.h declares; host-only helpers work; argument errors are reported
+without touching a GPU."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2504_14611_b200 import build
+    build.build()
+    import paper_2504_14611_b200 as J
+    return J.lib()
+
+
+def declared_symbols():
+    h = open(os.path.join(ROOT, "include", "jdob.h")).read()
+    return sorted(set(re.findall(r"JDOB_API\s+[\w\s\*]+?\b(jdob_\w+)\s*\(", h)))
+
+
+def test_header_symbols_exported(L):
+    syms = declared_symbols()
+    assert len(syms) == 8, syms
+    for s in syms:
+        assert hasattr(L, s), s
+    import paper_2504_14611_b200 as J
+    assert sorted(J.EXPORTED) == syms
+
+
+def test_version_and_error(L):
+    assert b"sm_100a" in L.jdob_version()
+    assert L.jdob_last_error() == b""
+
+
+def test_bf_space_size(L):
+    import paper_2504_14611_b200 as J
+    assert J.bf_space_size(0, 11, 8, 64) == 12 ** 8 * 64 == 27_518_828_544
+    assert J.bf_space_size(1, 11, 8, 64) == 12 * 256 * 64 == 196_608
+    assert J.bf_space_size(0, 63, 11, 64) == 0          # >= 2^62 -> 0
+    assert J.bf_space_size(0, 4, 2, 3) == 75            # C1: 5^2 * 3
+    assert J.bf_space_size(1, 4, 2, 3) == 60            # C1: 5 * 4 * 3
+
+
+def test_workspace_bytes_host_only(L):
+    import paper_2504_14611_b200._binding as B
+    ms = (B.JModel * 2)(B.JModel(4, 2), B.JModel(19, 32))
+    assert L.jdob_workspace_bytes(ms, 2, 0) > 0
+    assert L.jdob_workspace_bytes(ms, 2, 1) > 0
+    bad = (B.JModel * 1)(B.JModel(0, 2))
+    assert L.jdob_workspace_bytes(bad, 1, 0) == 0
+    assert L.jdob_workspace_bytes(ms, 2, 7) == 0
+
+
+def test_argument_errors_without_gpu(L):
+    import paper_2504_14611_b200._binding as B
+    ms = (B.JModel * 1)(B.JModel(4, 2))             # NULL tables
+    b = B.JBatch()
+    r = B.JResult()
+    assert L.jdob_solve_batch(ms, 1, C.byref(b), 0, C.byref(r), None, 0, None) == B.EINVAL
+    assert b"NULL" in L.jdob_last_error()
+    assert L.jdob_solve_batch(None, 0, None, 0, None, None, 0, None) == B.EINVAL
+    assert L.jdob_bruteforce(ms, 1, C.byref(b), 0, 0, 1, None, None, None, None, 0, None) == B.EINVAL
+
+
+def test_no_cpu_fallback():
+    # the product package never imports the oracle
+    pkg = os.path.join(ROOT, "paper_2504_14611_b200")
+    for dp, _, fs in os.walk(pkg):
+        for f in fs:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                src = open(os.path.join(dp, f)).read()
+                assert "import oracle" not in src and "from oracle" not in src, f
+                assert "jdob_oracle" not in src, f
+
+
+def test_oracle_header_independent():
+    # the oracle shares no header with the CUDA path
+    src = open(os.path.join(ROOT, "oracle", "jdob_oracle.c")).read()
+    assert "#include \"" not in src
+    assert "jdob.h" not in src

@@ -1,0 +1,260 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Bar (BASELINE.json north_star): decisions and partition indices bit-exact; energies
+within relative 1e-9 -- the arithmetic contract makes them bit-identical, which is
+what these tests assert."""
+import numpy as np
+import pytest
+
+import jdobgen as g
+import oracle as O
+from tests.gpu_util import assert_bits_equal, assert_solve_parity, rel_close, to_np
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def J():
+    import paper_2504_14611_b200 as J
+    return J
+
+
+def run(J, batch, mode=0, counts=True, stats=False, n_buckets=None):
+    db = J.DeviceBatch(batch)
+    res = J.solve_batch(db, mode=mode, counts=counts, stats=stats, n_buckets=n_buckets)
+    import torch
+    torch.cuda.synchronize()
+    return db, to_np(res)
+
+
+@pytest.mark.parametrize("toy", ["toy-1", "toy-2", "toy-2-m1", "toy-2-tfree", "toy-4"])
+def test_toys(J, toy):
+    b = g.toy_instance(toy)
+    _, gpu = run(J, b)
+    orc = O.solve_batch(b, counts=True)
+    assert_solve_parity(gpu, orc, counts=True)
+
+
+@pytest.mark.parametrize("seed,M_hi,N_hi,k_max", [(101, 4, 3, 12), (102, 12, 8, 70), (103, 32, 12, 70),
+                                                 (104, 32, 5, 200), (105, 20, 19, 64)])
+def test_random_full(J, seed, M_hi, N_hi, k_max):
+    b = g.random_batch(seed=seed, n_inst=1500, M_lo=1, M_hi=M_hi, N_lo=1, N_hi=N_hi, k_max=k_max)
+    _, gpu = run(J, b)
+    orc = O.solve_batch(b, counts=True)
+    assert_solve_parity(gpu, orc, counts=True)
+
+
+@pytest.mark.parametrize("mode", [1, 2, 3])
+def test_random_modes(J, mode):
+    b = g.random_batch(seed=110 + mode, n_inst=800, M_lo=1, M_hi=16, N_lo=1, N_hi=8, k_max=64)
+    _, gpu = run(J, b, mode=mode)
+    orc = O.solve_batch(b, mode=mode, counts=True)
+    assert_solve_parity(gpu, orc, counts=True)
+
+
+def test_edge_cases(J):
+    """Degenerate inputs: statuses, M = 1 and M = 32, k = 1, equal-gamma ties, Require equality."""
+    parts = []
+    b = g.toy_instance("toy-1"); b.T[0] = 0.1; parts.append(b)                # LOCAL_INFEASIBLE
+    b = g.toy_instance("toy-1"); b.t_free[0] = 0.21; parts.append(b)           # REQUIRE
+    b = g.toy_instance("toy-1"); b.t_free[0] = 0.2; parts.append(b)            # Require with equality (allowed)
+    b = g.toy_instance("toy-1"); b.f_min[1] = 3e9; parts.append(b)             # BADPARAM
+    b = g.toy_instance("toy-1"); b.R[0] = np.nan; parts.append(b)              # BADPARAM (non-finite)
+    b = g.toy_instance("toy-1"); b.models[0].d[1 * 3 + 2] = 0.5; parts.append(b)  # BADMODEL
+    b = g.toy_instance("toy-1"); b.fe_min[0] = b.fe_max[0]; parts.append(b)    # k = 1
+    b = g.toy_instance("toy-1"); b.rho[0] = 1.0; parts.append(b)               # k > JDOB_MAX_K -> BADPARAM
+    b = g.toy_instance("toy-2"); b.T[:] = 0.2; parts.append(b)                 # exact gamma and T ties
+    b = g.toy_instance("toy-2"); b.zeta[:] = 0.0; parts.append(b)              # zeta = 0 (R9)
+    for b in parts:
+        _, gpu = run(J, b)
+        orc = O.solve_batch(b, counts=True)
+        assert_solve_parity(gpu, orc, counts=True, f_user=orc["status"][0] <= 2)
+    # M = 32 homogeneous users (all-equal gamma) on the C5 MobileNetV2 profile
+    m = g.profiles.mobilenetv2()
+    users = dict(zeta=g.profiles.ZETA, kappa=g.profiles.KAPPA, f_min=1.5e9, f_max=2.6e9, R=g.R_TABLE_I, p_u=1.0,
+                 T=[float(g.deadline_from_beta(m, g.profiles.ZETA, 2.6e9, 2.13))] * 32)
+    b = g.single_instance(m, users)
+    _, gpu = run(J, b)
+    assert_solve_parity(gpu, O.solve_batch(b, counts=True), counts=True)
+
+
+def test_empty_batch(J):
+    b = g.random_batch(seed=1, n_inst=3).subset(0, 0)
+    db = J.DeviceBatch(b)
+    res = J.solve_batch(db)
+    assert res["E"].numel() == 0
+
+
+@pytest.mark.parametrize("cfg,n", [("c2", 1 << 20), ("c3", 100_000), ("c5", 1_000_000)])
+def test_configs_full_size_sampled(J, cfg, n):
+    """BASELINE configs at full size in the bench launch configuration; oracle on a sample."""
+    b = g.config_batch(cfg, n_inst=n)
+    db, gpu = run(J, b, counts=True, stats=True, n_buckets=b.meta["n_buckets"])
+    rng = np.random.default_rng(7)
+    idx = np.unique(np.concatenate([rng.choice(b.n_inst, 1500, replace=False), [0, b.n_inst - 1]]))
+    sub = b.take(idx)
+    orc = O.solve_batch(sub, counts=True, threads=8)
+    o0 = b.user_off[idx]
+    uidx = np.concatenate([np.arange(b.user_off[i], b.user_off[i + 1]) for i in idx])
+    for f in ("E", "E_lc", "t_free_next", "f_e", "n_tilde", "j", "status", "mask"):
+        assert_bits_equal(gpu[f][idx], orc[f], f)
+    assert_bits_equal(gpu["f_user"][uidx], orc["f_user"], "f_user")
+    assert_bits_equal(gpu["counts"][idx], orc["counts"], "counts")
+    # invariants at full size
+    assert np.all(gpu["status"] == 0)
+    assert np.all(gpu["E"] <= gpu["E_lc"])
+    # statistics: oracle definition over the GPU's per-instance outputs
+    st_o = O.stats(b, dict(gpu, mask=gpu["mask"]), n_buckets=b.meta["n_buckets"])
+    st_g = gpu["stats"]
+    for f in (0, 3, 4, 7, 8):
+        assert_bits_equal(st_g[:, f], st_o[:, f], f"stats[{f}]")
+    assert_bits_equal(st_g[:, 9:73], st_o[:, 9:73], "stats hist")
+    for f in (1, 2, 5, 6):
+        assert rel_close(st_g[:, f], st_o[:, f], 1e-9), f
+
+
+def test_stats_small_exact(J):
+    b = g.random_batch(seed=120, n_inst=3000, M_hi=32, N_hi=6, k_max=40)
+    _, gpu = run(J, b, stats=True, n_buckets=32)
+    orc = O.solve_batch(b)
+    st = O.stats(b, orc, n_buckets=32)
+    for f in (0, 3, 4, 7, 8):
+        assert_bits_equal(gpu["stats"][:, f], st[:, f], f"stats[{f}]")
+    assert_bits_equal(gpu["stats"][:, 9:], st[:, 9:], "hist")
+    for f in (1, 2, 5, 6):
+        assert rel_close(gpu["stats"][:, f], st[:, f], 1e-9)
+
+
+def test_determinism(J):
+    b = g.config_batch("c3", n_inst=20000)
+    db = J.DeviceBatch(b)
+    r1 = to_np(J.solve_batch(db, counts=True, stats=True, n_buckets=3))
+    r2 = to_np(J.solve_batch(db, counts=True, stats=True, n_buckets=3))
+    for k in r1:
+        assert_bits_equal(r1[k].reshape(-1), r2[k].reshape(-1), k)
+
+
+def test_eval_parity_and_plan_feasibility(J):
+    import torch
+    b = g.random_batch(seed=130, n_inst=2000, M_hi=24, N_hi=10, k_max=64)
+    db = J.DeviceBatch(b)
+    res = J.solve_batch(db)
+    part = J.plan_partition(db, res)
+    fe = res["f_e"]
+    ev = to_np(J.eval_plans(db, part, fe, slack=1e-9))
+    ev2 = to_np(J.eval_plans(db, plans=res, slack=1e-9))
+    for f in ev:
+        assert_bits_equal(ev[f], ev2[f], "plan-form eval " + f)
+    rn = to_np(res)
+    assert np.all(ev["violations"] == 0)
+    assert_bits_equal(ev["E"], rn["E"], "eval E == plan E")
+    assert_bits_equal(ev["t_free_next"], rn["t_free_next"], "eval t_free == D22")
+    orc = O.eval_batch(b, part.cpu().numpy(), fe.cpu().numpy(), slack=1e-9)
+    for f in ("E", "t_free_next", "f_user", "status"):
+        assert_bits_equal(ev[f], orc[f], f)
+    assert_bits_equal(ev["violations"].view(np.uint32), orc["violations"], "violations")
+
+
+def test_eval_general_vectors(J):
+    import torch
+    b = g.random_batch(seed=131, n_inst=1500, M_hi=12, N_hi=8, k_max=30)
+    rng = np.random.default_rng(3)
+    part = np.concatenate([rng.integers(0, b.models[b.model_id[i]].N + 1, b.M(i)) for i in range(b.n_inst)])
+    fe = np.array([b.fe_max[i] - rng.integers(0, 5) * b.rho[i] for i in range(b.n_inst)])
+    db = J.DeviceBatch(b)
+    ev = to_np(J.eval_plans(db, torch.from_numpy(part.astype(np.int32)), torch.from_numpy(fe), slack=1e-9))
+    orc = O.eval_batch(b, part, fe, slack=1e-9)
+    for f in ("E", "t_free_next", "f_user", "status"):
+        assert_bits_equal(ev[f], orc[f], f)
+    assert_bits_equal(ev["violations"].view(np.uint32), orc["violations"], "violations")
+
+
+def test_host_api_matches_device(J):
+    b = g.random_batch(seed=140, n_inst=1000, M_hi=16, N_hi=8, k_max=50)
+    _, gpu = run(J, b, counts=False)
+    hb = J.HostBuffers(b, f_user=True)
+    h2d, d2h = J.solve_batch_host(hb)
+    assert h2d > 0 and d2h > 0
+    host = {k: v.numpy() for k, v in hb.out.items() if v is not None}
+    host["mask"] = host["mask"].view(np.uint32)
+    for f in ("E", "E_lc", "t_free_next", "f_e", "n_tilde", "j", "status", "mask", "f_user"):
+        assert_bits_equal(host[f], gpu[f], f)
+
+
+# ------------------------------- brute force -------------------------------------
+@pytest.mark.parametrize("toy", ["toy-1", "toy-2", "toy-2-m1", "toy-2-tfree", "toy-4"])
+@pytest.mark.parametrize("space", [0, 1])
+def test_bf_toys(J, toy, space):
+    b = g.toy_instance(toy)
+    db = J.DeviceBatch(b)
+    E, I, S = J.bruteforce(db, space)
+    Eo, Io, So = O.bf(b, space)
+    assert int(S.item()) == So == 0
+    assert_bits_equal(E.cpu().numpy(), np.array([Eo]), "E")
+    assert int(I.item()) == Io
+
+
+def test_bf_random_full_and_ranges(J):
+    b = g.random_batch(seed=150, n_inst=60, M_lo=1, M_hi=5, N_lo=1, N_hi=4, k_max=20, tfree_frac=0.4)
+    rng = np.random.default_rng(0)
+    for i in range(b.n_inst):
+        bi = b.subset(i, i + 1)
+        db = J.DeviceBatch(bi)
+        for space in (0, 1):
+            size = O.bf_space_size(bi, space)
+            ranges = [(0, size)]
+            for _ in range(2):
+                lo = int(rng.integers(0, size))
+                hi = int(rng.integers(lo, size + 1))
+                ranges.append((lo, hi))
+            for lo, hi in ranges:
+                E, I, S = J.bruteforce(db, space, lo, hi)
+                Eo, Io, So = O.bf(bi, space, lo, hi)
+                assert int(S.item()) == So
+                assert_bits_equal(E.cpu().numpy(), np.array([Eo]), f"E {i} {space} {lo} {hi}")
+                assert int(I.item()) == Io
+
+
+def test_bf_larger_M(J):
+    # M in 9..16 and 17..32 exercise the other kernel specialisations (small N keeps spaces small)
+    for seed, M_lo, M_hi, N_hi in ((151, 9, 12, 1), (152, 17, 20, 1)):
+        b = g.random_batch(seed=seed, n_inst=4, M_lo=M_lo, M_hi=M_hi, N_lo=1, N_hi=N_hi, k_max=4)
+        for i in range(b.n_inst):
+            bi = b.subset(i, i + 1)
+            db = J.DeviceBatch(bi)
+            size = O.bf_space_size(bi, 0)
+            hi = min(size, 3_000_000)
+            for space, end in ((0, hi), (1, None)):
+                E, I, S = J.bruteforce(db, space, 0, end if end is not None else O.bf_space_size(bi, 1))
+                Eo, Io, So = O.bf(bi, space, 0, end if end is not None else O.bf_space_size(bi, 1), threads=8)
+                assert_bits_equal(E.cpu().numpy(), np.array([Eo]), "E")
+                assert int(I.item()) == Io
+
+
+def test_bf_c4_full(J):
+    """C4 at full size (2.75e10 candidates) in the bench launch configuration: the winner
+    re-evaluated by the oracle, sampled sub-ranges equal, BF-general <= BF-identical <= J-DOB."""
+    b = g.config_batch("c4")
+    db = J.DeviceBatch(b)
+    size = O.bf_space_size(b, 0)
+    E, I, S = J.bruteforce(db, 0, 0, size)
+    E, I = float(E.item()), int(I.item())
+    assert int(S.item()) == 0 and I >= 0
+    assert O.bf_candidate(b, 0, I) == E
+    Ei, Ii, _ = O.bf(b, 1)
+    Eg, Ig, Sg = J.bruteforce(db, 1)
+    assert float(Eg.item()) == Ei and int(Ig.item()) == Ii
+    r = O.jdob(b)
+    assert E <= Ei <= r["E"] * (1 + 1e-12)
+    rng = np.random.default_rng(4)
+    for _ in range(6):
+        lo = int(rng.integers(0, size - 3_000_000))
+        hi = lo + int(rng.integers(1, 3_000_000))
+        Eg, Ig, _ = J.bruteforce(db, 0, lo, hi)
+        Eo, Io, _ = O.bf(b, 0, lo, hi, threads=8)
+        assert_bits_equal(Eg.cpu().numpy(), np.array([Eo]), "E range")
+        assert int(Ig.item()) == Io
+    # the range containing the winner
+    lo, hi = max(0, I - 1_000_000), min(size, I + 1_000_000)
+    Eo, Io, _ = O.bf(b, 0, lo, hi, threads=8)
+    assert Eo == E and Io == I
