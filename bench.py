@@ -161,9 +161,8 @@ def bf_leg(J, torch, world, rank, reps, dist):
     k = G.grid_size(float(b.fe_min[0]), float(b.fe_max[0]), float(b.rho[0]))
     N, M = b.models[0].N, b.M(0)
     size = J.bf_space_size(0, N, M, k)
-    V = size // k
-    lo = (V * rank // world) * k
-    hi = (V * (rank + 1) // world) * k
+    from paper_2504_14611_b200.dist import allreduce_argmin, bf_shard
+    lo, hi = bf_shard(size, k, world, rank)
     J.bruteforce(db, 0, lo, min(hi, lo + 64 * 1024 * k))     # warm-up (small)
     torch.cuda.synchronize()
     times = []
@@ -176,11 +175,7 @@ def bf_leg(J, torch, world, rank, reps, dist):
         s.record()
         E, I, S = J.bruteforce(db, 0, lo, hi)
         if dist:
-            Eg = E.clone()
-            dist.all_reduce(Eg, op=dist.ReduceOp.MIN)
-            Ic = torch.where(E == Eg, I, torch.full_like(I, 2 ** 62))
-            dist.all_reduce(Ic, op=dist.ReduceOp.MIN)
-            E, I = Eg, Ic
+            E, I = allreduce_argmin(E, I, dist)
         e.record()
         torch.cuda.synchronize()
         ms = s.elapsed_time(e)
@@ -235,20 +230,13 @@ def run_mine(args):
     ev = J.eval_plans(db, plans=res, f_user=False)
     stream = torch.cuda.current_stream()
 
+    from paper_2504_14611_b200.dist import allreduce_stats
+
     def step():
         J.solve_batch(db, stats=True, n_buckets=n_buckets, f_user=False, out=res)
         J.eval_plans(db, plans=res, f_user=False, out=ev)
         if dist:
-            st = res["stats"]
-            red = st.clone()
-            dist.all_reduce(red, op=dist.ReduceOp.SUM)
-            mx = st[:, 3].contiguous()
-            mn = st[:, 4].contiguous()
-            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-            dist.all_reduce(mn, op=dist.ReduceOp.MIN)
-            red[:, 3] = mx
-            red[:, 4] = mn
-            res["stats_global"] = red
+            res["stats_global"] = allreduce_stats(res["stats"], dist)
 
     for _ in range(args.warmup):
         step()
@@ -270,13 +258,7 @@ def run_mine(args):
         ev_e[i].record(stream)
         J.eval_plans(db, plans=res, f_user=False, out=ev)
         if dist:
-            st = res["stats"]
-            red = st.clone()
-            dist.all_reduce(red, op=dist.ReduceOp.SUM)
-            mx = st[:, 3].contiguous()
-            mn = st[:, 4].contiguous()
-            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-            dist.all_reduce(mn, op=dist.ReduceOp.MIN)
+            res["stats_global"] = allreduce_stats(res["stats"], dist)
     t_e.record(stream)
     torch.cuda.synchronize()
     if dist:

@@ -14,7 +14,7 @@ from typing import Optional
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libjdob.so")
+LIB_PATH = os.environ.get("JDOB_LIB") or os.path.join(HERE, "libjdob.so")
 
 MAX_M, MAX_N, MAX_K, STATS_FIELDS, MAX_BUCKETS = 32, 63, 65536, 80, 64
 OK, EINVAL, ETOOBIG, ECUDA = 0, 1, 2, 3

@@ -205,12 +205,19 @@ __global__ void __launch_bounds__(kBfWarps * 32) k_bf_main(const DevModel *model
                                     feas = false;
                                     break;
                                 }
-                                const double G = zv / budget;
-                                if (G > sFmax[m]) {
-                                    feas = false;
-                                    break;
+                                const double fmin = sFmin[m];
+                                // exact low-clamp shortcut (DESIGN.md §Exact shortcuts): zv <= f_min*budget
+                                // exactly => RN(zv/budget) <= f_min <= f_max, so f* = f_min, feasible.
+                                if (fmin >= 1e-100 && budget >= 1e-100 && __fma_rn(fmin, budget, -zv) >= 0.0) {
+                                    f = fmin;
+                                } else {
+                                    const double G = zv / budget;
+                                    if (G > sFmax[m]) {
+                                        feas = false;
+                                        break;
+                                    }
+                                    f = (G < fmin) ? fmin : G;
                                 }
-                                f = (G < sFmin[m]) ? sFmin[m] : G;
                             }
                             e = ((sKU[x] * f) * f) + sUP[x];
                         } else {

@@ -2,47 +2,61 @@
 //
 // One warp per instance (persistent grid-stride loop).  Per partition point n~ the
 // warp first works lane = user (gamma, hoists, all-pairs rank sort, suffix-min
-// deadlines, thresholds), then lane = edge-grid point j for the Alg. 2 sweep:
-// each lane finds its offloading set as the suffix of the sorted list starting at
-// p(j) = min{i >= i^ : !(f_e(j) < th_i)} -- equal to Alg. 2's sequential pointer
-// because the thresholds are exactly non-increasing from i^ (DESIGN.md §Sweep
-// equivalence) -- checks the D6 guard, evaluates D20-D21 in user-index order and
-// keeps a lane-local strict minimum.  A warp argmin over (E, n~, j) and the first
-// all-local evaluation (R8) give the Alg. 1 answer; the winner's D20/D22 values
-// are recomputed lane = user.
+// deadlines, thresholds), then lane = edge-grid point j for the Alg. 2 sweep.
+//
+// Sweep equivalence (DESIGN.md §Sweep equivalence): the thresholds are exactly
+// non-increasing from i^, so Alg. 2's sequential pointer at grid point j equals
+// p(j) = min{i >= i^ : !(f_e(j) < th_i)}, and user m (sorted position r_m) is in
+// the offloading set iff r_m >= i^ and !(f_e(j) < th_{r_m}).  Each lane therefore
+// finds B_o and l_o by a binary search over the thresholds, decides membership per
+// user with one comparison against the user's own threshold, checks the D6 guard,
+// evaluates D20-D21 in user-index order and keeps a lane-local strict minimum.  The
+// first j with an empty set (Alg. 2's break) is found by a ballot inside the chunk
+// loop.  A warp argmin over (E, n~, j) and the first all-local evaluation (R8) give
+// the Alg. 1 answer; the winner's D20/D22 values are recomputed lane = user.
+//
+// Division is the expensive operation on sm_100a (MUFU.RCP64H-bound, ~4.6/clk/SM
+// measured vs 64 DFMA/clk/SM).  Two exact shortcuts (DESIGN.md §Exact shortcuts)
+// skip it without changing a single result bit:
+//   * D20 low clamp: RN(zv/budget) <= f_min  <=  fma(f_min, budget, -zv) >= 0
+//   * D6 guard:      RN(phi/y) <= f_e        <=  fma(f_e, y, -phi) >= 0
+// (the sign of a correctly rounded fma is the sign of the exact value when the
+// operands are >= 1e-100); otherwise the literal division runs.  1/f_e(j) is
+// computed once per instance and cached in shared memory.  When every user of an
+// instance has the same (R, zeta, f_max) -- the paper's Table I setting -- gamma
+// is equal for all users at every n~, so the sort key reduces to (T, index) and
+// the order and suffix-min deadlines are computed once per instance.
 #include "jdob_dev.cuh"
 #include "kernels.h"
 
 namespace jdob {
 
-struct SolveSmem {
-    double eloc[kMaxM], fmin[kMaxM], fmax[kMaxM], T[kMaxM];
-    double OR[kMaxM], zv[kMaxM], ku[kMaxM], up[kMaxM], gam[kMaxM];
-    double th[kMaxM], L[kMaxM];
-    int rank[kMaxM], order[kMaxM];
+constexpr int kInvCache = 192;    // 1/f_e(j) cached for j < kInvCache
+constexpr double kTiny = 1e-100;  // exactness floor of the fma-sign shortcuts
+
+struct __align__(16) UserSlot {  // per user, per n~ (lane-broadcast reads)
+    double OR, zv;               // O_n~/R_m, zeta_m v_n~
+    double ku, up;               // kappa_m u_n~, (O_n~/R_m) p_m
+    double eloc, fmin;           // local energy e_loc,m, f_m,min
+    double thu, fmax;            // th_{r_m} if r_m >= i^ else +inf; f_m,max
 };
 
-// Alg. 1 lines 4-6 for partition point nt (P:269-273).  Returns i^ (M if none).
-__device__ __forceinline__ int setup_nt(const DevModel &md, int nt, int M, const InstRegs &x, SolveSmem &s,
-                                        int lane) {
-    const double v_nt = md.v[nt], u_nt = md.u[nt], O_nt = md.O[nt];
-    double gam = 0.0;
-    if (lane < M) {
-        double OR = O_nt / x.R;                              // Eq. (3)
-        double zv = x.z * v_nt;
-        gam = OR + zv / x.f1;                                // gamma
-        s.OR[lane] = OR;
-        s.zv[lane] = zv;
-        s.ku[lane] = x.k * u_nt;
-        s.up[lane] = OR * x.p;                               // Eq. (4)
-        s.gam[lane] = gam;
-    }
-    // rank under the key (gamma desc, T asc, index asc) (R2)
+struct SolveSmem {
+    UserSlot u[kMaxM];
+    double T[kMaxM], gam[kMaxM];
+    double th[kMaxM], L[kMaxM];
+    int rank[kMaxM], order[kMaxM];
+    double inv[kInvCache];
+};
+
+// Ranks under the key (gamma desc, T asc, index asc) (R2), then order[] and the
+// suffix-min deadlines L_i = min_{i' >= i} T_order[i'] (Eq. fth's min, R1).
+__device__ __forceinline__ void sort_users(int M, double gam, double T, SolveSmem &s, int lane) {
     int r = 0;
     for (int t = 0; t < M; t++) {
-        double gt = __shfl_sync(0xffffffffu, gam, t);
-        double Tt = __shfl_sync(0xffffffffu, x.T, t);
-        bool before = (gt > gam) || (gt == gam && (Tt < x.T || (Tt == x.T && t < lane)));
+        const double gt = __shfl_sync(0xffffffffu, gam, t);
+        const double Tt = __shfl_sync(0xffffffffu, T, t);
+        const bool before = (gt > gam) || (gt == gam && (Tt < T || (Tt == T && t < lane)));
         r += before ? 1 : 0;
     }
     if (lane < M) {
@@ -50,27 +64,47 @@ __device__ __forceinline__ int setup_nt(const DevModel &md, int nt, int M, const
         s.order[r] = lane;
     }
     __syncwarp();
-    // suffix-min deadline and thresholds over sorted positions (Eq. fth, R1)
-    double L = dinf(), gi = 0.0;
-    if (lane < M) {
-        int mi = s.order[lane];
-        L = s.T[mi];
-        gi = s.gam[mi];
-    }
+    double L = lane < M ? s.T[s.order[lane]] : dinf();
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-        double o = __shfl_down_sync(0xffffffffu, L, d);
+        const double o = __shfl_down_sync(0xffffffffu, L, d);
         if (lane + d < 32 && o < L) L = o;
     }
+    if (lane < M) s.L[lane] = L;
+    __syncwarp();
+}
+
+// Alg. 1 lines 4-6 for partition point nt (P:269-273).  Returns i^ (M if none).
+__device__ __forceinline__ int setup_nt(const DevModel &md, int nt, int M, const InstRegs &x, bool homog,
+                                        SolveSmem &s, int lane) {
+    const double v_nt = md.v[nt], u_nt = md.u[nt], O_nt = md.O[nt];
+    double gam = 0.0;
+    if (lane < M) {
+        const double OR = O_nt / x.R;  // Eq. (3)
+        const double zv = x.z * v_nt;
+        gam = OR + zv / x.f1;          // gamma
+        s.u[lane].OR = OR;
+        s.u[lane].zv = zv;
+        s.u[lane].ku = x.k * u_nt;
+        s.u[lane].up = OR * x.p;       // Eq. (4)
+        s.gam[lane] = gam;
+    }
+    if (!homog) sort_users(M, gam, x.T, s, lane);  // homogeneous: order fixed per instance
     double th = 0.0;
     if (lane < M) {
-        th = md.phi[nt * md.B1 + (M - lane)] / (L - gi);
+        const double gi = homog ? gam : s.gam[s.order[lane]];
+        th = md.phi[nt * md.B1 + (M - lane)] / (s.L[lane] - gi);  // Eq. (fth)
         s.th[lane] = th;
-        s.L[lane] = L;
     }
-    unsigned nn = __ballot_sync(0xffffffffu, lane < M && th >= 0.0);
+    const unsigned nn = __ballot_sync(0xffffffffu, lane < M && th >= 0.0);
+    const int ihat = nn ? (__ffs(nn) - 1) : M;
     __syncwarp();
-    return nn ? (__ffs(nn) - 1) : M;
+    if (lane < M) {
+        const int rm = s.rank[lane];
+        s.u[lane].thu = (rm >= ihat) ? s.th[rm] : dinf();
+    }
+    __syncwarp();
+    return ihat;
 }
 
 __device__ __forceinline__ void write_bad(const DevResult &r, long long i, long long off, int M, int N, double t_free,
@@ -93,16 +127,36 @@ __device__ __forceinline__ void write_bad(const DevResult &r, long long i, long 
     if (r.f_user && M >= 1 && M <= kMaxM && lane < M) r.f_user[off + lane] = dnan();
 }
 
-__device__ void solve_instance(long long i, const DevModel *models, const DevBatch &b, const DevResult &r, int mode,
-                               SolveSmem &s, int lane) {
+__device__ __forceinline__ void write_local(const DevResult &r, long long i, long long off, int M, int N,
+                                            double E_lc, double t_free, double floc, int st, int lane,
+                                            bool zero_counts) {
+    if (lane == 0) {
+        r.E[i] = E_lc;
+        r.E_lc[i] = E_lc;
+        r.t_free_next[i] = t_free;
+        r.f_e[i] = 0.0;
+        r.n_tilde[i] = N;
+        r.j[i] = 0;
+        r.status[i] = st;
+        r.mask[i] = 0u;
+        if (r.counts && zero_counts) {
+            r.counts[3 * i] = 0;
+            r.counts[3 * i + 1] = 0;
+            r.counts[3 * i + 2] = 0;
+        }
+    }
+    if (r.f_user && lane < M) r.f_user[off + lane] = floc;
+}
+
+__device__ __forceinline__ void solve_instance(long long i, const DevModel *models, const DevBatch &b,
+                                               const DevResult &r, int mode, SolveSmem &s, int lane) {
     __syncwarp();
     long long off, k;
     int M;
     const DevModel *mdp;
     InstRegs x;
-    int st = warp_validate(models, b, i, lane, x, M, k, mdp, off);
+    const int st = warp_validate(models, b, i, lane, x, M, k, mdp, off);
     const double t_free = b.t_free[i], fe_min = b.fe_min[i], fe_max = b.fe_max[i], rho = b.rho[i];
-    (void)fe_min;
     if (st == JDOB_ST_BADPARAM || st == JDOB_ST_BADMODEL) {
         write_bad(r, i, off, M, mdp ? mdp->N : 0, t_free, st, lane);
         return;
@@ -114,114 +168,97 @@ __device__ void solve_instance(long long i, const DevModel *models, const DevBat
     // LC (row a2): f_loc = clamp(zeta v_N / T), e_loc = ((kappa u_N) f) f
     double floc = 0.0, eloc = 0.0;
     if (lane < M) {
-        double G = (x.z * vN) / x.T;
-        floc = clampf(G, x.f0, x.f1);
+        floc = clampf((x.z * vN) / x.T, x.f0, x.f1);
         eloc = ((x.k * uN) * floc) * floc;
-        s.eloc[lane] = eloc;
-        s.fmin[lane] = x.f0;
-        s.fmax[lane] = x.f1;
+        s.u[lane].eloc = eloc;
+        s.u[lane].fmin = x.f0;
+        s.u[lane].fmax = x.f1;
     }
     s.T[lane] = x.T;  // +inf beyond M
     double E_lc = 0.0;
     for (int t = 0; t < M; t++) E_lc = E_lc + __shfl_sync(0xffffffffu, eloc, t);  // user-index order
-    __syncwarp();
-
     if (st != JDOB_ST_OK || mode == JDOB_MODE_LC) {
-        if (lane == 0) {
-            r.E[i] = E_lc;
-            r.E_lc[i] = E_lc;
-            r.t_free_next[i] = t_free;
-            r.f_e[i] = 0.0;
-            r.n_tilde[i] = N;
-            r.j[i] = 0;
-            r.status[i] = st;
-            r.mask[i] = 0u;
-            if (r.counts) {
-                r.counts[3 * i] = 0;
-                r.counts[3 * i + 1] = 0;
-                r.counts[3 * i + 2] = 0;
-            }
-        }
-        if (r.f_user && lane < M) r.f_user[off + lane] = floc;
+        write_local(r, i, off, M, N, E_lc, t_free, floc, st, lane, true);
         return;
     }
 
     const long long kk = (mode == JDOB_MODE_NO_EDGE_DVFS) ? 1 : k;
+    const long long kc = kk < kInvCache ? kk : kInvCache;
+    for (long long j = lane; j < kc; j += 32) s.inv[j] = 1.0 / grid_fe(fe_max, rho, j);
+    // instance-level flags (warp-uniform)
+    const double R0 = __shfl_sync(0xffffffffu, x.R, 0), z0 = __shfl_sync(0xffffffffu, x.z, 0);
+    const double f10 = __shfl_sync(0xffffffffu, x.f1, 0);
+    const bool homog = __all_sync(0xffffffffu, lane >= M || (x.R == R0 && x.z == z0 && x.f1 == f10));
+    const bool fast_min = __all_sync(0xffffffffu, lane >= M || x.f0 >= kTiny);
+    const bool guard_fast = fe_min >= kTiny;
+    if (homog) sort_users(M, 0.0, x.T, s, lane);  // equal gamma: key (T asc, index asc)
+    __syncwarp();
+
     const int B1 = md.B1;
     double bE = dinf();
     int bN = 0x7fffffff, bP = 0;
     long long bJ = 0;
-    int aN = N;          // first all-local evaluation key (R8); n~ = N at j = 0 by default (R4)
+    int aN = N;  // first all-local evaluation key (R8); n~ = N at j = 0 by default (R4)
     long long aJ = 0;
     long long c_visit = 0, c_eval = 0, c_member = 0;
 
     for (int nt = 0; nt < N; nt++) {
         if (mode == JDOB_MODE_BINARY && nt != 0) break;
-        const int ihat = setup_nt(md, nt, M, x, s, lane);
-        // first j whose offloading set is empty: f_e(j) < th_{M-1} (or j = 0 if i^ = NAN)
-        long long jb;
-        if (ihat == M) {
-            jb = 0;
-        } else {
-            const double thl = s.th[M - 1];
-            long long lo = 0, hi = kk;
+        const int ihat = setup_nt(md, nt, M, x, homog, s, lane);
+        const double *phi_row = md.phi + nt * B1;
+        const double *psi_row = md.psi + nt * B1;
+        for (long long j0 = 0; j0 < kk; j0 += 32) {
+            const long long j = j0 + lane;
+            const bool valid = j < kk;
+            const double fe = grid_fe(fe_max, rho, j);
+            // p(j): first sorted position >= i^ with !(f_e < th_i)  (M if the set is empty)
+            int lo = ihat, hi = M;
             while (lo < hi) {
-                long long md2 = (lo + hi) >> 1;
-                if (grid_fe(fe_max, rho, md2) < thl) hi = md2;
-                else lo = md2 + 1;
+                const int mm = (lo + hi) >> 1;
+                if (fe < s.th[mm]) lo = mm + 1;
+                else hi = mm;
             }
-            jb = lo;
-        }
-        if (jb < kk) {
-            if (aN == N) {
+            const int p = lo;
+            // Alg. 2's break: the first j with an empty set ends this n~'s sweep
+            const unsigned emp = __ballot_sync(0xffffffffu, valid && p == M);
+            const long long jb = emp ? j0 + (__ffs(emp) - 1) : kk;
+            if (emp && aN == N) {
                 aN = nt;
                 aJ = jb;
             }
-            if (lane == 0) {  // the all-local evaluation at jb (guard passes: 0 / inf = 0)
+            if (emp && lane == 0) {  // the all-local evaluation at jb (guard passes: 0 / inf = 0)
                 c_visit += 1;
                 c_eval += 1;
             }
-        }
-        const long long jend = (jb < kk) ? jb : kk;
-        const double *phi_row = md.phi + nt * B1;
-        const double *psi_row = md.psi + nt * B1;
-        for (long long j0 = 0; j0 < jend; j0 += 32) {
-            const long long j = j0 + lane;
-            if (j < jend) {
-                const double fe = grid_fe(fe_max, rho, j);
-                const double inv = 1.0 / fe;
-                int lo = ihat, hi = M;
-                while (lo < hi) {
-                    int mm = (lo + hi) >> 1;
-                    if (fe < s.th[mm]) lo = mm + 1;
-                    else hi = mm;
-                }
-                const int p = lo;
+            if (valid && j < jb) {
+                const double inv = (j < kInvCache) ? s.inv[j] : 1.0 / fe;
                 const int Bo = M - p;
                 const double lo_ = s.L[p];
                 const double phib = phi_row[Bo];
                 c_visit += 1;
-                if (fe >= phib / (lo_ - t_free)) {  // D6 guard
+                // D6 guard: f_e >= phi / (l_o - t_free), with the exact fma shortcut
+                const double y = lo_ - t_free;
+                const bool pass =
+                    (guard_fast && y >= kTiny && __fma_rn(fe, y, -phib) >= 0.0) || (fe >= phib / y);
+                if (pass) {
                     c_eval += 1;
                     c_member += Bo;
                     const double te = phib * inv;
                     double E = 0.0;
+#pragma unroll 4
                     for (int m = 0; m < M; m++) {
-                        double e;
-                        if (s.rank[m] >= p) {
-                            const double zv = s.zv[m];
-                            double f;
-                            if (zv == 0.0) {
-                                f = s.fmin[m];  // R9
-                            } else {
-                                const double budget = (lo_ - s.OR[m]) - te;
-                                f = clampf(zv / budget, s.fmin[m], s.fmax[m]);  // D20
-                            }
-                            e = ((s.ku[m] * f) * f) + s.up[m];  // D21 offloader term
-                        } else {
-                            e = s.eloc[m];
-                        }
-                        E = E + e;
+                        const double2 a = *reinterpret_cast<const double2 *>(&s.u[m].OR);    // OR, zv
+                        const double2 c = *reinterpret_cast<const double2 *>(&s.u[m].ku);    // ku, up
+                        const double2 d = *reinterpret_cast<const double2 *>(&s.u[m].eloc);  // eloc, fmin
+                        const double2 t = *reinterpret_cast<const double2 *>(&s.u[m].thu);   // thu, fmax
+                        const bool mem = !(fe < t.x);
+                        const double budget = (lo_ - a.x) - te;
+                        const bool low = (a.y == 0.0) ||  // R9
+                                         (fast_min && budget >= kTiny && __fma_rn(d.y, budget, -a.y) >= 0.0);
+                        double f = d.y;  // f_min
+                        if (mem && !low) f = clampf(a.y / budget, d.y, t.y);   // D20
+                        const double em = ((c.x * f) * f) + c.y;              // D21 offloader term
+                        E = E + (mem ? em : d.x);
                     }
                     E = E + (psi_row[Bo] * fe) * fe;
                     if (E < bE) {  // strict: lane keys ascend in (n~, j)
@@ -232,17 +269,18 @@ __device__ void solve_instance(long long i, const DevModel *models, const DevBat
                     }
                 }
             }
+            if (emp) break;
         }
         __syncwarp();
     }
     // warp argmin over (E, n~, j)
 #pragma unroll
     for (int d = 16; d >= 1; d >>= 1) {
-        double oE = __shfl_xor_sync(0xffffffffu, bE, d);
-        int oN = __shfl_xor_sync(0xffffffffu, bN, d);
-        long long oJ = __shfl_xor_sync(0xffffffffu, bJ, d);
-        int oP = __shfl_xor_sync(0xffffffffu, bP, d);
-        bool take = (oE < bE) || (oE == bE && (oN < bN || (oN == bN && oJ < bJ)));
+        const double oE = __shfl_xor_sync(0xffffffffu, bE, d);
+        const int oN = __shfl_xor_sync(0xffffffffu, bN, d);
+        const long long oJ = __shfl_xor_sync(0xffffffffu, bJ, d);
+        const int oP = __shfl_xor_sync(0xffffffffu, bP, d);
+        const bool take = (oE < bE) || (oE == bE && (oN < bN || (oN == bN && oJ < bJ)));
         if (take) {
             bE = oE;
             bN = oN;
@@ -265,21 +303,11 @@ __device__ void solve_instance(long long i, const DevModel *models, const DevBat
     }
     const bool offload_wins = (bE < E_lc) || (bE == E_lc && (bN < aN || (bN == aN && bJ < aJ)));
     if (!offload_wins) {
-        if (lane == 0) {
-            r.E[i] = E_lc;
-            r.E_lc[i] = E_lc;
-            r.t_free_next[i] = t_free;
-            r.f_e[i] = 0.0;
-            r.n_tilde[i] = N;
-            r.j[i] = 0;
-            r.status[i] = st;
-            r.mask[i] = 0u;
-        }
-        if (r.f_user && lane < M) r.f_user[off + lane] = floc;
+        write_local(r, i, off, M, N, E_lc, t_free, floc, st, lane, false);
         return;
     }
     // winner: recompute D20 and D22 lane = user (same arithmetic as the sweep)
-    setup_nt(md, bN, M, x, s, lane);
+    setup_nt(md, bN, M, x, homog, s, lane);
     const int Bo = M - bP;
     const double lo_ = s.L[bP];
     const double fe = grid_fe(fe_max, rho, bJ);
@@ -288,15 +316,17 @@ __device__ void solve_instance(long long i, const DevModel *models, const DevBat
     const bool member = (lane < M) && (s.rank[lane] >= bP);
     double f = floc, arr = t_free;
     if (member) {
-        const double zv = s.zv[lane];
-        if (zv == 0.0) f = x.f0;
-        else f = clampf(zv / ((lo_ - s.OR[lane]) - te), x.f0, x.f1);
-        arr = zv / f + s.OR[lane];
+        const UserSlot &us = s.u[lane];
+        const double budget = (lo_ - us.OR) - te;
+        const bool low = (us.zv == 0.0) ||
+                         (fast_min && budget >= kTiny && __fma_rn(x.f0, budget, -us.zv) >= 0.0);
+        f = low ? x.f0 : clampf(us.zv / budget, x.f0, x.f1);
+        arr = us.zv / f + us.OR;
         if (arr < t_free) arr = t_free;
     }
 #pragma unroll
     for (int d = 16; d >= 1; d >>= 1) {
-        double o = __shfl_xor_sync(0xffffffffu, arr, d);
+        const double o = __shfl_xor_sync(0xffffffffu, arr, d);
         arr = (o > arr) ? o : arr;
     }
     const unsigned mask = __ballot_sync(0xffffffffu, member);
@@ -313,13 +343,18 @@ __device__ void solve_instance(long long i, const DevModel *models, const DevBat
     if (r.f_user && lane < M) r.f_user[off + lane] = f;
 }
 
-__global__ void __launch_bounds__(kSolveWarps * 32) k_solve(const DevModel *models, DevBatch b, DevResult r, int mode) {
+#ifndef JDOB_SOLVE_MINB
+#define JDOB_SOLVE_MINB 5
+#endif
+
+__global__ void __launch_bounds__(kSolveWarps * 32, JDOB_SOLVE_MINB)
+    k_solve(const DevModel *models, DevBatch b, DevResult r, int mode) {
     __shared__ SolveSmem smem[kSolveWarps];
     const int lane = threadIdx.x & 31;
-    const int w = threadIdx.x >> 5;
-    const long long gw = (long long)blockIdx.x * kSolveWarps + w;
+    SolveSmem &s = smem[threadIdx.x >> 5];
+    const long long gw = (long long)blockIdx.x * kSolveWarps + (threadIdx.x >> 5);
     const long long nw = (long long)gridDim.x * kSolveWarps;
-    for (long long i = gw; i < b.n_inst; i += nw) solve_instance(i, models, b, r, mode, smem[w], lane);
+    for (long long i = gw; i < b.n_inst; i += nw) solve_instance(i, models, b, r, mode, s, lane);
 }
 
 void launch_solve(const DevModel *models, const DevBatch &b, const DevResult &r, int mode, cudaStream_t s,
@@ -328,7 +363,7 @@ void launch_solve(const DevModel *models, const DevBatch &b, const DevResult &r,
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve, kSolveWarps * 32, 0);
     if (per_sm < 1) per_sm = 1;
-    long long want = (b.n_inst + kSolveWarps - 1) / kSolveWarps;
+    const long long want = (b.n_inst + kSolveWarps - 1) / kSolveWarps;
     long long grid = (long long)num_sms * per_sm;
     if (want < grid) grid = want;
     k_solve<<<(unsigned)grid, kSolveWarps * 32, 0, s>>>(models, b, r, mode);

@@ -1,0 +1,17 @@
+#!/bin/bash
+# Profiling pass (run under gpurun on one B200): FP64 microbenchmark, ncu launch list of
+# the bench step, ncu --set full of the top kernels.  Outputs land in gpurun_out/.
+set -x
+OUT=${OUT:-gpurun_out}
+mkdir -p $OUT
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 --fmad=false -o /tmp/fp64mb tools/fp64_microbench.cu && /tmp/fp64mb > $OUT/fp64_microbench.jsonl
+python __graft_entry__.py
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
+    python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --bf-reps 1 > $OUT/launches_bench.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_solve -s 1 -c 1 -o $OUT/prof_solve -f \
+    python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-bf > $OUT/prof_solve.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_bf_main -c 1 -o $OUT/prof_bf -f \
+    python tools/profile_bf.py 0.0625 > $OUT/prof_bf.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_eval -c 1 -o $OUT/prof_eval -f \
+    python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --no-bf > $OUT/prof_eval.log 2>&1
+ls -la $OUT

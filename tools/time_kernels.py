@@ -1,0 +1,51 @@
+"""Quick kernel timing for optimisation experiments (JDOB_LIB selects a library build)."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import jdobgen as G  # noqa: E402
+import paper_2504_14611_b200 as J  # noqa: E402
+
+
+def t_solve(cfg, n):
+    b = G.config_batch(cfg, n_inst=n)
+    db = J.DeviceBatch(b)
+    res = J.solve_batch(db, f_user=False)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(5):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        J.solve_batch(db, f_user=False, out=res)
+        e.record()
+        torch.cuda.synchronize()
+        ts.append(s.elapsed_time(e))
+    ms = float(np.median(ts))
+    return {"cfg": cfg, "n": n, "ms": ms, "inst_per_s": n / ms * 1e3, "E_sum": float(res["E"].sum().item())}
+
+
+def t_bf(frac):
+    b = G.config_batch("c4")
+    db = J.DeviceBatch(b)
+    size = J.bf_space_size(0, b.models[0].N, b.M(0), 64)
+    hi = int(size * frac) // 64 * 64
+    J.bruteforce(db, 0, 0, hi // 16)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    E, I, S = J.bruteforce(db, 0, 0, hi)
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e)
+    return {"cfg": "c4bf", "cand": hi, "ms": ms, "cand_per_s": hi / ms * 1e3, "E": float(E.item()), "I": int(I.item())}
+
+
+if __name__ == "__main__":
+    lib = os.environ.get("JDOB_LIB", "default")
+    for r in (t_solve("c2", 1 << 20), t_solve("c3", 100_000), t_solve("c5", 1_000_000), t_bf(0.25)):
+        r["lib"] = os.path.basename(lib)
+        print(json.dumps(r), flush=True)
