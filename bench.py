@@ -34,10 +34,7 @@ sys.path.insert(0, ROOT)
 
 import jdobgen as G  # noqa: E402
 
-# FP64-pipe instructions of one correctly rounded double division in the sm_100a SASS of
-# the solve kernel (MUFU.RCP64H + DFMA/DMUL refinement + checks).
-W_DIV = 9
-PEAK_FP64_SM_PER_CLK = 64      # FP64 lanes per SM per clock (B200), DESIGN.md §Roofline
+PEAK_FP64_SM_PER_CLK = 64      # FP64 lanes per SM per clock (B200), DESIGN.md §7 (microbenchmarked)
 N_SMS = 148
 
 WORKLOADS = {
@@ -118,23 +115,26 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def fp64_work(batch, counts, mode_nts=None):
-    """FP64-pipe lane-instructions of K1's algorithmic work.
-
-    Per instance, from the literal Alg. 2 counters (n_visit, n_eval, n_member):
-      LC                     M (1 div + 6)
-      per n~ < N (setup)     M (3 div + 6) + M(M-1)/2 compares + M suffix-min
-      per visited (n~, j)    2 div (1/f_e, guard) + 3
-      per evaluated (n~, j)  (M - B_o) adds + 5 (edge term, compare)
-      per member evaluation  1 div + 8 (budget 2, clamp 2, energy 3, sum 1)
-    """
+def fp64_work(batch, counts):
+    """Algorithmic FP64 operations of K1 per launch: the literal Alg. 1/2 evaluation,
+    each +, -, x, / or comparison = 1 op, from the per-instance counters (n_visit, n_eval, n_member):
+      member evaluation 9, non-member term 1, evaluated pair 6, visited pair 4,
+      per n~ setup 6M + M(M-1)/2 + 3M, LC 8M."""
     M = np.diff(batch.user_off).astype(np.float64)
     N = np.array([batch.models[m].N for m in batch.model_id], np.float64)
     visit, ev, mem = (counts[:, 0].astype(np.float64), counts[:, 1].astype(np.float64),
                       counts[:, 2].astype(np.float64))
-    div = M + N * 3 * M + 2 * visit + mem
-    other = 6 * M + N * (6 * M + M * (M - 1) / 2 + M) + 3 * visit + (ev * M - mem) + 5 * ev + 8 * mem
-    return float(np.sum(div * W_DIV + other)), float(np.sum(div)), float(np.sum(other))
+    ops = 9 * mem + (ev * M - mem) + 6 * ev + 4 * visit + N * (6 * M + M * (M - 1) / 2 + 3 * M) + 8 * M
+    return float(np.sum(ops)), float(np.sum(mem))
+
+
+def ncu_traffic(kernel):
+    """dram read+write bytes per launch of `kernel` from the committed ncu --set full capture."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        return d.get(kernel)
+    except Exception:
+        return None
 
 
 def cpu_baseline(batch, seconds, label):
@@ -212,7 +212,7 @@ def run_mine(args):
     # untimed: algorithmic work counters (literal Alg. 2 counts, checked against the oracle in tests)
     res_c = J.solve_batch(db, counts=True, f_user=False)
     counts = res_c["counts"].cpu().numpy()
-    work, n_div, n_other = fp64_work(batch, counts)
+    work, n_member = fp64_work(batch, counts)
     # parity spot check against the oracle on 64 sampled instances (rank 0)
     parity = None
     if rank == 0:
@@ -310,7 +310,7 @@ def run_mine(args):
 
     if rank == 0:
         peak_clk = (clk or {}).get("sm_max_mhz") or 1965.0
-        peak = N_SMS * PEAK_FP64_SM_PER_CLK * peak_clk * 1e6 / 1e9   # G FP64-pipe lane-instr/s
+        peak = N_SMS * PEAK_FP64_SM_PER_CLK * peak_clk * 1e6 / 1e9   # G FP64 ops/s
         achieved = work / (solve_ms / 1e3) / 1e9
         line = {
             "metric": "J-DOB instances solved/s",
@@ -331,10 +331,13 @@ def run_mine(args):
                        "step": "jdob_solve_batch (K0+K1+K4 stats) + jdob_eval of every plan (K3) + NCCL stats allreduce",
                        "parallelism": f"dp{world}"},
             "roofline": {"bound": "alu", "kernel": "k_solve (K1)", "achieved": achieved, "peak": peak,
-                         "unit": "G FP64-pipe lane-instr/s", "frac": achieved / peak, "traffic": None,
-                         "work_per_launch": work, "div_per_launch": n_div, "w_div": W_DIV,
+                         "unit": "G FP64 op/s", "frac": achieved / peak,
+                         "traffic": ncu_traffic("k_solve") if args.workload == "c2" else None,
+                         "algorithmic_bytes": int(batch.nbytes()),
+                         "work_per_launch": work, "member_evals_per_launch": n_member,
                          "launch_ms": solve_ms,
-                         "peak_note": "148 SMs x 64 FP64 lanes/clk x max SM clock (DESIGN.md §Roofline)"},
+                         "peak_note": "148 SMs x 64 FP64 lanes/clk x max SM clock (DESIGN.md §7); "
+                                      "work = literal Alg. 1/2 FP64 ops, division = 1 op"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": 6 * K,

@@ -18,10 +18,10 @@
 // Division is the expensive operation on sm_100a (MUFU.RCP64H-bound, ~4.6/clk/SM
 // measured vs 64 DFMA/clk/SM).  Two exact shortcuts (DESIGN.md §Exact shortcuts)
 // skip it without changing a single result bit:
-//   * D20 low clamp: RN(zv/budget) <= f_min  <=  fma(f_min, budget, -zv) >= 0
-//   * D6 guard:      RN(phi/y) <= f_e        <=  fma(f_e, y, -phi) >= 0
-// (the sign of a correctly rounded fma is the sign of the exact value when the
-// operands are >= 1e-100); otherwise the literal division runs.  1/f_e(j) is
+//   * D20 low clamp: RN(zv/budget) <= f_min  <=  fma(f_min, budget, -zv) > 0
+//   * D6 guard:      RN(phi/y) <= f_e        <=  fma(f_e, y, -phi) > 0
+// (a correctly rounded fma is > 0 only if the exact value is > 0, and the exact
+// inequality implies the rounded one); otherwise the literal division runs.  1/f_e(j) is
 // computed once per instance and cached in shared memory.  When every user of an
 // instance has the same (R, zeta, f_max) -- the paper's Table I setting -- gamma
 // is equal for all users at every n~, so the sort key reduces to (T, index) and
@@ -32,7 +32,6 @@
 namespace jdob {
 
 constexpr int kInvCache = 192;    // 1/f_e(j) cached for j < kInvCache
-constexpr double kTiny = 1e-100;  // exactness floor of the fma-sign shortcuts
 
 struct __align__(16) UserSlot {  // per user, per n~ (lane-broadcast reads)
     double OR, zv;               // O_n~/R_m, zeta_m v_n~
@@ -43,6 +42,7 @@ struct __align__(16) UserSlot {  // per user, per n~ (lane-broadcast reads)
 
 struct SolveSmem {
     UserSlot u[kMaxM];
+    double R[kMaxM], z[kMaxM], f1[kMaxM], kap[kMaxM], pu[kMaxM];  // user parameters (lane = user)
     double T[kMaxM], gam[kMaxM];
     double th[kMaxM], L[kMaxM];
     int rank[kMaxM], order[kMaxM];
@@ -75,21 +75,20 @@ __device__ __forceinline__ void sort_users(int M, double gam, double T, SolveSme
 }
 
 // Alg. 1 lines 4-6 for partition point nt.  Returns i^ (M if none).
-__device__ __forceinline__ int setup_nt(const DevModel &md, int nt, int M, const InstRegs &x, bool homog,
-                                        SolveSmem &s, int lane) {
+__device__ __forceinline__ int setup_nt(const DevModel &md, int nt, int M, bool homog, SolveSmem &s, int lane) {
     const double v_nt = md.v[nt], u_nt = md.u[nt], O_nt = md.O[nt];
     double gam = 0.0;
     if (lane < M) {
-        const double OR = O_nt / x.R;  // Eq. (3)
-        const double zv = x.z * v_nt;
-        gam = OR + zv / x.f1;          // gamma
+        const double OR = O_nt / s.R[lane];  // Eq. (3)
+        const double zv = s.z[lane] * v_nt;
+        gam = OR + zv / s.f1[lane];          // gamma
         s.u[lane].OR = OR;
         s.u[lane].zv = zv;
-        s.u[lane].ku = x.k * u_nt;
-        s.u[lane].up = OR * x.p;       // Eq. (4)
+        s.u[lane].ku = s.kap[lane] * u_nt;
+        s.u[lane].up = OR * s.pu[lane];      // Eq. (4)
         s.gam[lane] = gam;
     }
-    if (!homog) sort_users(M, gam, x.T, s, lane);  // homogeneous: order fixed per instance
+    if (!homog) sort_users(M, gam, s.T[lane], s, lane);  // homogeneous: order fixed per instance
     double th = 0.0;
     if (lane < M) {
         const double gi = homog ? gam : s.gam[s.order[lane]];
@@ -148,6 +147,7 @@ __device__ __forceinline__ void write_local(const DevResult &r, long long i, lon
     if (r.f_user && lane < M) r.f_user[off + lane] = floc;
 }
 
+template <bool COUNTS>
 __device__ __forceinline__ void solve_instance(long long i, const DevModel *models, const DevBatch &b,
                                                const DevResult &r, int mode, SolveSmem &s, int lane) {
     __syncwarp();
@@ -156,7 +156,7 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
     const DevModel *mdp;
     InstRegs x;
     const int st = warp_validate(models, b, i, lane, x, M, k, mdp, off);
-    const double t_free = b.t_free[i], fe_min = b.fe_min[i], fe_max = b.fe_max[i], rho = b.rho[i];
+    const double t_free = b.t_free[i], fe_max = b.fe_max[i], rho = b.rho[i];
     if (st == JDOB_ST_BADPARAM || st == JDOB_ST_BADMODEL) {
         write_bad(r, i, off, M, mdp ? mdp->N : 0, t_free, st, lane);
         return;
@@ -173,6 +173,11 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
         s.u[lane].eloc = eloc;
         s.u[lane].fmin = x.f0;
         s.u[lane].fmax = x.f1;
+        s.R[lane] = x.R;
+        s.z[lane] = x.z;
+        s.f1[lane] = x.f1;
+        s.kap[lane] = x.k;
+        s.pu[lane] = x.p;
     }
     s.T[lane] = x.T;  // +inf beyond M
     double E_lc = 0.0;
@@ -189,22 +194,19 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
     const double R0 = __shfl_sync(0xffffffffu, x.R, 0), z0 = __shfl_sync(0xffffffffu, x.z, 0);
     const double f10 = __shfl_sync(0xffffffffu, x.f1, 0);
     const bool homog = __all_sync(0xffffffffu, lane >= M || (x.R == R0 && x.z == z0 && x.f1 == f10));
-    const bool fast_min = __all_sync(0xffffffffu, lane >= M || x.f0 >= kTiny);
-    const bool guard_fast = fe_min >= kTiny;
     if (homog) sort_users(M, 0.0, x.T, s, lane);  // equal gamma: key (T asc, index asc)
     __syncwarp();
 
     const int B1 = md.B1;
     double bE = dinf();
-    int bN = 0x7fffffff, bP = 0;
-    long long bJ = 0;
+    int bN = 0x7fffffff, bP = 0, bJ = 0;
     int aN = N;  // first all-local evaluation key (R8); n~ = N at j = 0 by default (R4)
-    long long aJ = 0;
+    int aJ = 0;
     long long c_visit = 0, c_eval = 0, c_member = 0;
 
     for (int nt = 0; nt < N; nt++) {
         if (mode == JDOB_MODE_BINARY && nt != 0) break;
-        const int ihat = setup_nt(md, nt, M, x, homog, s, lane);
+        const int ihat = setup_nt(md, nt, M, homog, s, lane);
         const double *phi_row = md.phi + nt * B1;
         const double *psi_row = md.psi + nt * B1;
         for (long long j0 = 0; j0 < kk; j0 += 32) {
@@ -224,9 +226,9 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
             const long long jb = emp ? j0 + (__ffs(emp) - 1) : kk;
             if (emp && aN == N) {
                 aN = nt;
-                aJ = jb;
+                aJ = (int)jb;
             }
-            if (emp && lane == 0) {  // the all-local evaluation at jb (guard passes: 0 / inf = 0)
+            if (COUNTS && emp && lane == 0) {  // the all-local evaluation at jb (guard passes: 0 / inf = 0)
                 c_visit += 1;
                 c_eval += 1;
             }
@@ -235,14 +237,15 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
                 const int Bo = M - p;
                 const double lo_ = s.L[p];
                 const double phib = phi_row[Bo];
-                c_visit += 1;
+                if (COUNTS) c_visit += 1;
                 // D6 guard: f_e >= phi / (l_o - t_free), with the exact fma shortcut
                 const double y = lo_ - t_free;
-                const bool pass =
-                    (guard_fast && y >= kTiny && __fma_rn(fe, y, -phib) >= 0.0) || (fe >= phib / y);
+                const bool pass = (__fma_rn(fe, y, -phib) > 0.0) || (fe >= phib / y);
                 if (pass) {
-                    c_eval += 1;
-                    c_member += Bo;
+                    if (COUNTS) {
+                        c_eval += 1;
+                        c_member += Bo;
+                    }
                     const double te = phib * inv;
                     double E = 0.0;
 #pragma unroll 4
@@ -253,10 +256,9 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
                         const double2 t = *reinterpret_cast<const double2 *>(&s.u[m].thu);   // thu, fmax
                         const bool mem = !(fe < t.x);
                         const double budget = (lo_ - a.x) - te;
-                        const bool low = (a.y == 0.0) ||  // R9
-                                         (fast_min && budget >= kTiny && __fma_rn(d.y, budget, -a.y) >= 0.0);
-                        double f = d.y;  // f_min
-                        if (mem && !low) f = clampf(a.y / budget, d.y, t.y);   // D20
+                        const bool low = __fma_rn(d.y, budget, -a.y) > 0.0;  // f_min budget > zv exactly
+                        double f = d.y;                                       // f_min
+                        if (mem && !low) f = (a.y == 0.0) ? d.y : clampf(a.y / budget, d.y, t.y);  // R9, D20
                         const double em = ((c.x * f) * f) + c.y;              // D21 offloader term
                         E = E + (mem ? em : d.x);
                     }
@@ -264,7 +266,7 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
                     if (E < bE) {  // strict: lane keys ascend in (n~, j)
                         bE = E;
                         bN = nt;
-                        bJ = j;
+                        bJ = (int)j;
                         bP = p;
                     }
                 }
@@ -278,7 +280,7 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
     for (int d = 16; d >= 1; d >>= 1) {
         const double oE = __shfl_xor_sync(0xffffffffu, bE, d);
         const int oN = __shfl_xor_sync(0xffffffffu, bN, d);
-        const long long oJ = __shfl_xor_sync(0xffffffffu, bJ, d);
+        const int oJ = __shfl_xor_sync(0xffffffffu, bJ, d);
         const int oP = __shfl_xor_sync(0xffffffffu, bP, d);
         const bool take = (oE < bE) || (oE == bE && (oN < bN || (oN == bN && oJ < bJ)));
         if (take) {
@@ -288,7 +290,7 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
             bP = oP;
         }
     }
-    if (r.counts) {
+    if (COUNTS) {
 #pragma unroll
         for (int d = 16; d >= 1; d >>= 1) {
             c_visit += __shfl_xor_sync(0xffffffffu, c_visit, d);
@@ -307,7 +309,7 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
         return;
     }
     // winner: recompute D20 and D22 lane = user (same arithmetic as the sweep)
-    setup_nt(md, bN, M, x, homog, s, lane);
+    setup_nt(md, bN, M, homog, s, lane);
     const int Bo = M - bP;
     const double lo_ = s.L[bP];
     const double fe = grid_fe(fe_max, rho, bJ);
@@ -318,9 +320,8 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
     if (member) {
         const UserSlot &us = s.u[lane];
         const double budget = (lo_ - us.OR) - te;
-        const bool low = (us.zv == 0.0) ||
-                         (fast_min && budget >= kTiny && __fma_rn(x.f0, budget, -us.zv) >= 0.0);
-        f = low ? x.f0 : clampf(us.zv / budget, x.f0, x.f1);
+        const bool low = (us.zv == 0.0) || (__fma_rn(us.fmin, budget, -us.zv) > 0.0);
+        f = low ? us.fmin : clampf(us.zv / budget, us.fmin, us.fmax);
         arr = us.zv / f + us.OR;
         if (arr < t_free) arr = t_free;
     }
@@ -344,9 +345,10 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
 }
 
 #ifndef JDOB_SOLVE_MINB
-#define JDOB_SOLVE_MINB 5
+#define JDOB_SOLVE_MINB 6
 #endif
 
+template <bool COUNTS>
 __global__ void __launch_bounds__(kSolveWarps * 32, JDOB_SOLVE_MINB)
     k_solve(const DevModel *models, DevBatch b, DevResult r, int mode) {
     __shared__ SolveSmem smem[kSolveWarps];
@@ -354,19 +356,21 @@ __global__ void __launch_bounds__(kSolveWarps * 32, JDOB_SOLVE_MINB)
     SolveSmem &s = smem[threadIdx.x >> 5];
     const long long gw = (long long)blockIdx.x * kSolveWarps + (threadIdx.x >> 5);
     const long long nw = (long long)gridDim.x * kSolveWarps;
-    for (long long i = gw; i < b.n_inst; i += nw) solve_instance(i, models, b, r, mode, s, lane);
+    for (long long i = gw; i < b.n_inst; i += nw) solve_instance<COUNTS>(i, models, b, r, mode, s, lane);
 }
 
 void launch_solve(const DevModel *models, const DevBatch &b, const DevResult &r, int mode, cudaStream_t s,
                   int num_sms) {
     if (b.n_inst <= 0) return;
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve, kSolveWarps * 32, 0);
+    if (r.counts) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve<true>, kSolveWarps * 32, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve<false>, kSolveWarps * 32, 0);
     if (per_sm < 1) per_sm = 1;
     const long long want = (b.n_inst + kSolveWarps - 1) / kSolveWarps;
     long long grid = (long long)num_sms * per_sm;
     if (want < grid) grid = want;
-    k_solve<<<(unsigned)grid, kSolveWarps * 32, 0, s>>>(models, b, r, mode);
+    if (r.counts) k_solve<true><<<(unsigned)grid, kSolveWarps * 32, 0, s>>>(models, b, r, mode);
+    else k_solve<false><<<(unsigned)grid, kSolveWarps * 32, 0, s>>>(models, b, r, mode);
 }
 
 }  // namespace jdob
