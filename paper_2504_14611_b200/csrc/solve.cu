@@ -254,11 +254,15 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
                         const double2 c = *reinterpret_cast<const double2 *>(&s.u[m].ku);    // ku, up
                         const double2 d = *reinterpret_cast<const double2 *>(&s.u[m].eloc);  // eloc, fmin
                         const double2 t = *reinterpret_cast<const double2 *>(&s.u[m].thu);   // thu, fmax
-                        const bool mem = !(fe < t.x);
+                        // f_e, th >= 0 (or +inf): IEEE order = integer order of the bit patterns
+                        const bool mem = __double_as_longlong(fe) >= __double_as_longlong(t.x);
                         const double budget = (lo_ - a.x) - te;
                         const bool low = __fma_rn(d.y, budget, -a.y) > 0.0;  // f_min budget > zv exactly
                         double f = d.y;                                       // f_min
-                        if (mem && !low) f = (a.y == 0.0) ? d.y : clampf(a.y / budget, d.y, t.y);  // R9, D20
+                        if (mem && !low) {
+                            // R9 (zv = 0 -> f_min) tested on the bits, inside the rare branch
+                            if ((__double_as_longlong(a.y) << 1) != 0) f = clampf(a.y / budget, d.y, t.y);  // D20
+                        }
                         const double em = ((c.x * f) * f) + c.y;              // D21 offloader term
                         E = E + (mem ? em : d.x);
                     }
@@ -345,7 +349,7 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
 }
 
 #ifndef JDOB_SOLVE_MINB
-#define JDOB_SOLVE_MINB 6
+#define JDOB_SOLVE_MINB 7
 #endif
 
 template <bool COUNTS>
