@@ -142,6 +142,22 @@ static DevBatch to_dev(const jdob_batch *b) {
     return d;
 }
 
+// Keep the device's default memory pool from returning memory to the OS at every
+// synchronisation, so jdob_solve_batch_host's stream-ordered buffers are reused.
+static void keep_pool_warm() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    static bool done[64] = {false};
+    if (dev >= 0 && dev < 64 && !done[dev]) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            unsigned long long thr = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        done[dev] = true;
+    }
+}
+
 static int num_sms() {
     int dev = 0, n = 0;
     cudaGetDevice(&dev);
@@ -291,10 +307,15 @@ int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob
     if (!out || !out->E || !out->E_lc || !out->t_free_next || !out->f_e || !out->n_tilde || !out->j ||
         !out->status || !out->mask)
         return fail(JDOB_EINVAL, "result has a NULL required array");
+    if (out->stats && (out->n_buckets < 1 || out->n_buckets > JDOB_MAX_BUCKETS))
+        return fail(JDOB_EINVAL, "n_buckets = %d outside [1, %d]", out->n_buckets, JDOB_MAX_BUCKETS);
+    if (mode < JDOB_MODE_FULL || mode > JDOB_MODE_BINARY) return fail(JDOB_EINVAL, "bad mode %d", mode);
     cudaStream_t s = (cudaStream_t)stream;
+    keep_pool_warm();
     const long long n = b->n_inst;
     const long long nu = n > 0 ? (long long)b->user_off[n] : 0;
-    // device layout: model tables | batch | outputs | workspace
+    constexpr int NS = 2;  // copy/compute pipeline depth
+    // device layout: model tables | batch | outputs | NS workspaces
     size_t bytes = 0;
     for (int i = 0; i < n_models; i++) {
         const size_t n1 = (size_t)models[i].N + 1, b1 = (size_t)models[i].B_max + 1;
@@ -306,20 +327,13 @@ int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob
                         (out->counts ? al(n * 3 * 8) : 0) +
                         (out->stats ? al((size_t)out->n_buckets * JDOB_STATS_FIELDS * 8) : 0);
     const size_t wsb = jdob_workspace_bytes(models, n_models, 0);
-    bytes += in_inst + in_user + outb + al(wsb);
+    bytes += in_inst + in_user + outb + NS * al(wsb);
     char *base = nullptr;
     if (cudaMallocAsync((void **)&base, bytes, s) != cudaSuccess) return cuda_check("cudaMallocAsync");
     char *p = base;
     long long h2d = 0, d2h = 0;
-    auto put = [&](const void *src, size_t nb) -> void * {
-        void *d = p;
-        if (nb) cudaMemcpyAsync(d, src, nb, cudaMemcpyHostToDevice, s);
-        h2d += (long long)nb;
-        p += al(nb);
-        return d;
-    };
-    auto take = [&](size_t nb) -> void * {
-        void *d = p;
+    auto take = [&](size_t nb) -> char * {
+        char *d = p;
         p += al(nb);
         return d;
     };
@@ -327,30 +341,35 @@ int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob
     jdob_model *dm = n_models <= 64 ? dmods : new jdob_model[n_models];
     for (int i = 0; i < n_models; i++) {
         const size_t n1 = (size_t)models[i].N + 1, b1 = (size_t)models[i].B_max + 1;
+        const double *src[6] = {models[i].A, models[i].O, models[i].g, models[i].q, models[i].d, models[i].c};
+        const size_t nb[6] = {n1 * 8, n1 * 8, n1 * 8, n1 * 8, n1 * b1 * 8, n1 * b1 * 8};
+        const double *dst[6];
+        for (int t = 0; t < 6; t++) {
+            char *d = take(nb[t]);
+            cudaMemcpyAsync(d, src[t], nb[t], cudaMemcpyHostToDevice, s);
+            h2d += (long long)nb[t];
+            dst[t] = (const double *)d;
+        }
         dm[i].N = models[i].N;
         dm[i].B_max = models[i].B_max;
-        dm[i].A = (const double *)put(models[i].A, n1 * 8);
-        dm[i].O = (const double *)put(models[i].O, n1 * 8);
-        dm[i].g = (const double *)put(models[i].g, n1 * 8);
-        dm[i].q = (const double *)put(models[i].q, n1 * 8);
-        dm[i].d = (const double *)put(models[i].d, n1 * b1 * 8);
-        dm[i].c = (const double *)put(models[i].c, n1 * b1 * 8);
+        dm[i].A = dst[0];
+        dm[i].O = dst[1];
+        dm[i].g = dst[2];
+        dm[i].q = dst[3];
+        dm[i].d = dst[4];
+        dm[i].c = dst[5];
     }
+    // full-size device arrays; chunks are views (user indices stay global)
     jdob_batch db = *b;
-    db.model_id = (const int32_t *)put(b->model_id, n * 4);
-    db.user_off = (const int64_t *)put(b->user_off, (n + 1) * 8);
-    db.zeta = (const double *)put(b->zeta, nu * 8);
-    db.kappa = (const double *)put(b->kappa, nu * 8);
-    db.f_min = (const double *)put(b->f_min, nu * 8);
-    db.f_max = (const double *)put(b->f_max, nu * 8);
-    db.R = (const double *)put(b->R, nu * 8);
-    db.p_u = (const double *)put(b->p_u, nu * 8);
-    db.T = (const double *)put(b->T, nu * 8);
-    db.t_free = (const double *)put(b->t_free, n * 8);
-    db.fe_min = (const double *)put(b->fe_min, n * 8);
-    db.fe_max = (const double *)put(b->fe_max, n * 8);
-    db.rho = (const double *)put(b->rho, n * 8);
-    db.bucket = b->bucket ? (const int32_t *)put(b->bucket, n * 4) : nullptr;
+    db.model_id = (const int32_t *)take(n * 4);
+    db.user_off = (const int64_t *)take((n + 1) * 8);
+    const double **uf[7] = {&db.zeta, &db.kappa, &db.f_min, &db.f_max, &db.R, &db.p_u, &db.T};
+    const double *uh[7] = {b->zeta, b->kappa, b->f_min, b->f_max, b->R, b->p_u, b->T};
+    for (int t = 0; t < 7; t++) *uf[t] = (const double *)take(nu * 8);
+    const double **inf[4] = {&db.t_free, &db.fe_min, &db.fe_max, &db.rho};
+    const double *ih[4] = {b->t_free, b->fe_min, b->fe_max, b->rho};
+    for (int t = 0; t < 4; t++) *inf[t] = (const double *)take(n * 8);
+    db.bucket = b->bucket ? (const int32_t *)take(n * 4) : nullptr;
     jdob_result dr = *out;
     dr.E = (double *)take(n * 8);
     dr.E_lc = (double *)take(n * 8);
@@ -363,28 +382,106 @@ int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob
     dr.f_user = out->f_user ? (double *)take(nu * 8) : nullptr;
     dr.counts = out->counts ? (int64_t *)take(n * 3 * 8) : nullptr;
     dr.stats = out->stats ? (double *)take((size_t)out->n_buckets * JDOB_STATS_FIELDS * 8) : nullptr;
-    void *ws = take(wsb);
-    rc = jdob_solve_batch(dm, n_models, &db, mode, &dr, ws, wsb, stream);
-    if (dm != dmods) delete[] dm;
-    if (rc == JDOB_OK) {
-        auto get = [&](void *dst, const void *src, size_t nb) {
-            if (nb) cudaMemcpyAsync(dst, src, nb, cudaMemcpyDeviceToHost, s);
+    void *ws[NS];
+    for (int k = 0; k < NS; k++) ws[k] = take(wsb);
+
+    // pipeline: chunk c copies in, solves and copies out on stream c % NS, so the copies of one
+    // chunk overlap the solve of the other (copy engines and SMs run concurrently)
+    cudaStream_t st[NS];
+    cudaEvent_t ev0, evs[NS];
+    cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming);
+    cudaEventRecord(ev0, s);
+    for (int k = 0; k < NS; k++) {
+        cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&evs[k], cudaEventDisableTiming);
+        cudaStreamWaitEvent(st[k], ev0, 0);
+    }
+    const long long per = 131072;
+    long long nchunks = (n + per - 1) / per;
+    if (nchunks < 1) nchunks = 1;
+    if (nchunks > 64) nchunks = 64;
+    for (long long c = 0; c < nchunks && rc == JDOB_OK; c++) {
+        cudaStream_t ss = st[c % NS];
+        const long long i0 = n * c / nchunks, i1 = n * (c + 1) / nchunks;
+        if (i1 <= i0) continue;
+        const long long u0 = b->user_off[i0], u1 = b->user_off[i1];
+        auto h2 = [&](const void *dst, const void *src, size_t nb) {
+            if (nb) cudaMemcpyAsync((void *)dst, src, nb, cudaMemcpyHostToDevice, ss);
+            h2d += (long long)nb;
+        };
+        h2(db.model_id + i0, b->model_id + i0, (i1 - i0) * 4);
+        // user_off[i0..i1] (the shared boundary element is written with identical bytes by both chunks)
+        h2(db.user_off + i0, b->user_off + i0, (i1 - i0 + 1) * 8);
+        for (int t = 0; t < 7; t++) h2(*uf[t] + u0, uh[t] + u0, (u1 - u0) * 8);
+        for (int t = 0; t < 4; t++) h2(*inf[t] + i0, ih[t] + i0, (i1 - i0) * 8);
+        if (b->bucket) h2(db.bucket + i0, b->bucket + i0, (i1 - i0) * 4);
+        jdob_batch cb = db;
+        cb.n_inst = i1 - i0;
+        cb.model_id = db.model_id + i0;
+        cb.user_off = db.user_off + i0;
+        cb.t_free = db.t_free + i0;
+        cb.fe_min = db.fe_min + i0;
+        cb.fe_max = db.fe_max + i0;
+        cb.rho = db.rho + i0;
+        cb.bucket = db.bucket ? db.bucket + i0 : nullptr;
+        jdob_result cr = dr;
+        cr.E = dr.E + i0;
+        cr.E_lc = dr.E_lc + i0;
+        cr.t_free_next = dr.t_free_next + i0;
+        cr.f_e = dr.f_e + i0;
+        cr.n_tilde = dr.n_tilde + i0;
+        cr.j = dr.j + i0;
+        cr.status = dr.status + i0;
+        cr.mask = dr.mask + i0;
+        cr.counts = dr.counts ? dr.counts + 3 * i0 : nullptr;
+        cr.stats = nullptr;
+        rc = jdob_solve_batch(dm, n_models, &cb, mode, &cr, ws[c % NS], wsb, (void *)ss);
+        if (rc != JDOB_OK) break;
+        auto d2 = [&](void *dst, const void *src, size_t nb) {
+            if (nb) cudaMemcpyAsync(dst, src, nb, cudaMemcpyDeviceToHost, ss);
             d2h += (long long)nb;
         };
-        get(out->E, dr.E, n * 8);
-        get(out->E_lc, dr.E_lc, n * 8);
-        get(out->t_free_next, dr.t_free_next, n * 8);
-        get(out->f_e, dr.f_e, n * 8);
-        get(out->n_tilde, dr.n_tilde, n * 4);
-        get(out->j, dr.j, n * 4);
-        get(out->status, dr.status, n * 4);
-        get(out->mask, dr.mask, n * 4);
-        if (out->f_user) get(out->f_user, dr.f_user, nu * 8);
-        if (out->counts) get(out->counts, dr.counts, n * 3 * 8);
-        if (out->stats) get(out->stats, dr.stats, (size_t)out->n_buckets * JDOB_STATS_FIELDS * 8);
+        d2(out->E + i0, cr.E, (i1 - i0) * 8);
+        d2(out->E_lc + i0, cr.E_lc, (i1 - i0) * 8);
+        d2(out->t_free_next + i0, cr.t_free_next, (i1 - i0) * 8);
+        d2(out->f_e + i0, cr.f_e, (i1 - i0) * 8);
+        d2(out->n_tilde + i0, cr.n_tilde, (i1 - i0) * 4);
+        d2(out->j + i0, cr.j, (i1 - i0) * 4);
+        d2(out->status + i0, cr.status, (i1 - i0) * 4);
+        d2(out->mask + i0, cr.mask, (i1 - i0) * 4);
+        if (out->f_user) d2(out->f_user + u0, dr.f_user + u0, (u1 - u0) * 8);
+        if (out->counts) d2(out->counts + 3 * i0, cr.counts, (i1 - i0) * 3 * 8);
     }
+    for (int k = 0; k < NS; k++) {
+        cudaEventRecord(evs[k], st[k]);
+        cudaStreamWaitEvent(s, evs[k], 0);
+    }
+    if (rc == JDOB_OK && out->stats && n > 0) {
+        DevResult r2;
+        r2.E = dr.E;
+        r2.E_lc = dr.E_lc;
+        r2.t_free_next = dr.t_free_next;
+        r2.f_e = dr.f_e;
+        r2.n_tilde = dr.n_tilde;
+        r2.j = dr.j;
+        r2.status = dr.status;
+        r2.mask = dr.mask;
+        r2.f_user = dr.f_user;
+        r2.counts = (long long *)dr.counts;
+        double *partials = (double *)((char *)ws[0] + models_bytes(models, n_models));
+        launch_stats(to_dev(&db), r2, partials, dr.stats, out->n_buckets, s);
+        cudaMemcpyAsync(out->stats, dr.stats, (size_t)out->n_buckets * JDOB_STATS_FIELDS * 8,
+                        cudaMemcpyDeviceToHost, s);
+        d2h += (long long)out->n_buckets * JDOB_STATS_FIELDS * 8;
+    }
+    if (dm != dmods) delete[] dm;
     cudaFreeAsync(base, s);
     cudaError_t e = cudaStreamSynchronize(s);
+    for (int k = 0; k < NS; k++) {
+        cudaStreamDestroy(st[k]);
+        cudaEventDestroy(evs[k]);
+    }
+    cudaEventDestroy(ev0);
     if (rc != JDOB_OK) return rc;
     if (e != cudaSuccess) return fail(JDOB_ECUDA, "solve_batch_host: %s", cudaGetErrorString(e));
     if (h2d_bytes) *h2d_bytes = h2d;

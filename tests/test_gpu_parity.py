@@ -181,6 +181,20 @@ def test_host_api_matches_device(J):
         assert_bits_equal(host[f], gpu[f], f)
 
 
+def test_host_api_chunked_pipeline(J):
+    # > 131072 instances: several copy/compute pipeline chunks on two internal streams
+    b = g.config_batch("c3", n_inst=300_000)
+    _, gpu = run(J, b, counts=True, stats=True, n_buckets=3)
+    hb = J.HostBuffers(b, f_user=True, stats=True, n_buckets=3)
+    h2d, d2h = J.solve_batch_host(hb)
+    assert h2d >= b.nbytes()
+    host = {k: v.numpy() for k, v in hb.out.items() if v is not None}
+    host["mask"] = host["mask"].view(np.uint32)
+    for f in ("E", "E_lc", "t_free_next", "f_e", "n_tilde", "j", "status", "mask", "f_user"):
+        assert_bits_equal(host[f], gpu[f], f)
+    assert_bits_equal(host["stats"].reshape(3, -1), gpu["stats"], "stats")
+
+
 # ------------------------------- brute force -------------------------------------
 @pytest.mark.parametrize("toy", ["toy-1", "toy-2", "toy-2-m1", "toy-2-tfree", "toy-4"])
 @pytest.mark.parametrize("space", [0, 1])
