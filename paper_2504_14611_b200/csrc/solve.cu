@@ -16,16 +16,19 @@
 // the Alg. 1 answer; the winner's D20/D22 values are recomputed lane = user.
 //
 // Division is the expensive operation on sm_100a (MUFU.RCP64H-bound, ~4.6/clk/SM
-// measured vs 64 DFMA/clk/SM).  Two exact shortcuts (DESIGN.md §Exact shortcuts)
-// skip it without changing a single result bit:
-//   * D20 low clamp: RN(zv/budget) <= f_min  <=  fma(f_min, budget, -zv) > 0
-//   * D6 guard:      RN(phi/y) <= f_e        <=  fma(f_e, y, -phi) > 0
-// (a correctly rounded fma is > 0 only if the exact value is > 0, and the exact
-// inequality implies the rounded one); otherwise the literal division runs.  1/f_e(j) is
+// measured vs 64 DFMA/clk/SM), so the sweep avoids it where that is exact
+// (DESIGN.md §4): the D20 low clamp RN(zv/budget) <= f_min is implied by
+// fma(f_min, budget, -zv) > 0 (a correctly rounded fma is > 0 only if the exact
+// value is, and the exact inequality implies the rounded one), otherwise the literal
+// division runs; the D6 guard quotient phi(B_o)/(l_o - t_free) depends only on the
+// set start p, so it is formed once per (n~, p) in setup, not per grid point.  1/f_e(j) is
 // computed once per instance and cached in shared memory.  When every user of an
 // instance has the same (R, zeta, f_max) -- the paper's Table I setting -- gamma
 // is equal for all users at every n~, so the sort key reduces to (T, index) and
-// the order and suffix-min deadlines are computed once per instance.
+// the order and suffix-min deadlines are computed once per instance; if moreover
+// f_min, kappa and p_u agree ("uniform users": all of Table I's experiments, where
+// only deadlines differ), every member of a configuration has the same budget, f*
+// and offloader energy, which are then formed once per (n~, j) instead of per user.
 #include "jdob_dev.cuh"
 #include "kernels.h"
 
@@ -36,15 +39,17 @@ constexpr int kInvCache = 192;    // 1/f_e(j) cached for j < kInvCache
 struct __align__(16) UserSlot {  // per user, per n~ (lane-broadcast reads)
     double OR, zv;               // O_n~/R_m, zeta_m v_n~
     double ku, up;               // kappa_m u_n~, (O_n~/R_m) p_m
-    double eloc, fmin;           // local energy e_loc,m, f_m,min
-    double thu, fmax;            // th_{r_m} if r_m >= i^ else +inf; f_m,max
+    double eloc, thu;            // local energy e_loc,m; th_{r_m} if r_m >= i^ else +inf
+    double fmin, fmax;           // f_m,min, f_m,max
 };
 
 struct SolveSmem {
     UserSlot u[kMaxM];
     double R[kMaxM], z[kMaxM], f1[kMaxM], kap[kMaxM], pu[kMaxM];  // user parameters (lane = user)
     double T[kMaxM], gam[kMaxM];
-    double th[kMaxM], L[kMaxM];
+    double th[kMaxM];
+    double2 Lg[kMaxM];                   // per sorted position p: {l_o = L_p, guard threshold phi/(L_p - t_free)}
+    double2 pp[kMaxM];                   // per sorted position p: {phi_n~(M - p), psi_n~(M - p)}
     int rank[kMaxM], order[kMaxM];
     double inv[kInvCache];
 };
@@ -70,12 +75,13 @@ __device__ __forceinline__ void sort_users(int M, double gam, double T, SolveSme
         const double o = __shfl_down_sync(0xffffffffu, L, d);
         if (lane + d < 32 && o < L) L = o;
     }
-    if (lane < M) s.L[lane] = L;
+    if (lane < M) s.Lg[lane].x = L;
     __syncwarp();
 }
 
 // Alg. 1 lines 4-6 for partition point nt.  Returns i^ (M if none).
-__device__ __forceinline__ int setup_nt(const DevModel &md, int nt, int M, bool homog, SolveSmem &s, int lane) {
+__device__ __forceinline__ int setup_nt(const DevModel &md, int nt, int M, bool homog, double t_free, SolveSmem &s,
+                                        int lane) {
     const double v_nt = md.v[nt], u_nt = md.u[nt], O_nt = md.O[nt];
     double gam = 0.0;
     if (lane < M) {
@@ -92,8 +98,12 @@ __device__ __forceinline__ int setup_nt(const DevModel &md, int nt, int M, bool 
     double th = 0.0;
     if (lane < M) {
         const double gi = homog ? gam : s.gam[s.order[lane]];
-        th = md.phi[nt * md.B1 + (M - lane)] / (s.L[lane] - gi);  // Eq. (fth)
+        const double phi = md.phi[nt * md.B1 + (M - lane)], psi = md.psi[nt * md.B1 + (M - lane)];
+        const double L = s.Lg[lane].x;
+        th = phi / (L - gi);                          // Eq. (fth)
         s.th[lane] = th;
+        s.Lg[lane].y = phi / (L - t_free);            // D6 guard threshold of the set starting at p = lane
+        s.pp[lane] = make_double2(phi, psi);
     }
     const unsigned nn = __ballot_sync(0xffffffffu, lane < M && th >= 0.0);
     const int ihat = nn ? (__ffs(nn) - 1) : M;
@@ -194,6 +204,9 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
     const double R0 = __shfl_sync(0xffffffffu, x.R, 0), z0 = __shfl_sync(0xffffffffu, x.z, 0);
     const double f10 = __shfl_sync(0xffffffffu, x.f1, 0);
     const bool homog = __all_sync(0xffffffffu, lane >= M || (x.R == R0 && x.z == z0 && x.f1 == f10));
+    const double f00 = __shfl_sync(0xffffffffu, x.f0, 0), k0 = __shfl_sync(0xffffffffu, x.k, 0);
+    const double p0 = __shfl_sync(0xffffffffu, x.p, 0);
+    const bool uni = homog && __all_sync(0xffffffffu, lane >= M || (x.f0 == f00 && x.k == k0 && x.p == p0));
     if (homog) sort_users(M, 0.0, x.T, s, lane);  // equal gamma: key (T asc, index asc)
     __syncwarp();
 
@@ -206,9 +219,7 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
 
     for (int nt = 0; nt < N; nt++) {
         if (mode == JDOB_MODE_BINARY && nt != 0) break;
-        const int ihat = setup_nt(md, nt, M, homog, s, lane);
-        const double *phi_row = md.phi + nt * B1;
-        const double *psi_row = md.psi + nt * B1;
+        const int ihat = setup_nt(md, nt, M, homog, t_free, s, lane);
         for (long long j0 = 0; j0 < kk; j0 += 32) {
             const long long j = j0 + lane;
             const bool valid = j < kk;
@@ -235,38 +246,56 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
             if (valid && j < jb) {
                 const double inv = (j < kInvCache) ? s.inv[j] : 1.0 / fe;
                 const int Bo = M - p;
-                const double lo_ = s.L[p];
-                const double phib = phi_row[Bo];
+                const double2 lg = s.Lg[p];  // l_o, phi / (l_o - t_free)
+                const double2 pq = s.pp[p];  // phi_n~(B_o), psi_n~(B_o)
+                const double lo_ = lg.x, phib = pq.x;
                 if (COUNTS) c_visit += 1;
-                // D6 guard: f_e >= phi / (l_o - t_free), with the exact fma shortcut
-                const double y = lo_ - t_free;
-                const bool pass = (__fma_rn(fe, y, -phib) > 0.0) || (fe >= phib / y);
-                if (pass) {
+                // D6 guard: f_e >= phi / (l_o - t_free); the quotient depends only on p
+                if (fe >= lg.y) {
                     if (COUNTS) {
                         c_eval += 1;
                         c_member += Bo;
                     }
                     const double te = phib * inv;
                     double E = 0.0;
+                    const long long feb = __double_as_longlong(fe);
+                    if (uni) {
+                        // Uniform users (same R, zeta, f_min, f_max, kappa, p_u; Table I): every member
+                        // has the same budget, f* and offloader term, so D20/D21 are formed once and
+                        // only the user-order sum runs over M.  Same operations, same bits.
+                        const UserSlot &u0 = s.u[0];
+                        const double budget = (lo_ - u0.OR) - te;
+                        double f = u0.fmin;
+                        if (!(__fma_rn(u0.fmin, budget, -u0.zv) > 0.0) && u0.zv != 0.0)
+                            f = clampf(u0.zv / budget, u0.fmin, u0.fmax);  // D20 (R9 when zv = 0)
+                        const double em = ((u0.ku * f) * f) + u0.up;       // D21 offloader term
 #pragma unroll 4
-                    for (int m = 0; m < M; m++) {
-                        const double2 a = *reinterpret_cast<const double2 *>(&s.u[m].OR);    // OR, zv
-                        const double2 c = *reinterpret_cast<const double2 *>(&s.u[m].ku);    // ku, up
-                        const double2 d = *reinterpret_cast<const double2 *>(&s.u[m].eloc);  // eloc, fmin
-                        const double2 t = *reinterpret_cast<const double2 *>(&s.u[m].thu);   // thu, fmax
-                        // f_e, th >= 0 (or +inf): IEEE order = integer order of the bit patterns
-                        const bool mem = __double_as_longlong(fe) >= __double_as_longlong(t.x);
-                        const double budget = (lo_ - a.x) - te;
-                        const bool low = __fma_rn(d.y, budget, -a.y) > 0.0;  // f_min budget > zv exactly
-                        double f = d.y;                                       // f_min
-                        if (mem && !low) {
-                            // R9 (zv = 0 -> f_min) tested on the bits, inside the rare branch
-                            if ((__double_as_longlong(a.y) << 1) != 0) f = clampf(a.y / budget, d.y, t.y);  // D20
+                        for (int m = 0; m < M; m++) {
+                            const double2 et = *reinterpret_cast<const double2 *>(&s.u[m].eloc);  // eloc, thu
+                            const bool mem = feb >= __double_as_longlong(et.y);
+                            E = E + (mem ? em : et.x);
                         }
-                        const double em = ((c.x * f) * f) + c.y;              // D21 offloader term
-                        E = E + (mem ? em : d.x);
+                    } else {
+#pragma unroll 4
+                        for (int m = 0; m < M; m++) {
+                            const double2 a = *reinterpret_cast<const double2 *>(&s.u[m].OR);    // OR, zv
+                            const double2 c = *reinterpret_cast<const double2 *>(&s.u[m].ku);    // ku, up
+                            const double2 d = *reinterpret_cast<const double2 *>(&s.u[m].eloc);  // eloc, thu
+                            const double2 t = *reinterpret_cast<const double2 *>(&s.u[m].fmin);  // fmin, fmax
+                            // f_e, th >= 0 (or +inf): IEEE order = integer order of the bit patterns
+                            const bool mem = feb >= __double_as_longlong(d.y);
+                            const double budget = (lo_ - a.x) - te;
+                            const bool low = __fma_rn(t.x, budget, -a.y) > 0.0;  // f_min budget > zv exactly
+                            double f = t.x;                                       // f_min
+                            if (mem && !low) {
+                                // R9 (zv = 0 -> f_min) tested on the bits, inside the rare branch
+                                if ((__double_as_longlong(a.y) << 1) != 0) f = clampf(a.y / budget, t.x, t.y);
+                            }
+                            const double em = ((c.x * f) * f) + c.y;  // D21 offloader term
+                            E = E + (mem ? em : d.x);
+                        }
                     }
-                    E = E + (psi_row[Bo] * fe) * fe;
+                    E = E + (pq.y * fe) * fe;
                     if (E < bE) {  // strict: lane keys ascend in (n~, j)
                         bE = E;
                         bN = nt;
@@ -313,9 +342,9 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
         return;
     }
     // winner: recompute D20 and D22 lane = user (same arithmetic as the sweep)
-    setup_nt(md, bN, M, homog, s, lane);
+    setup_nt(md, bN, M, homog, t_free, s, lane);
     const int Bo = M - bP;
-    const double lo_ = s.L[bP];
+    const double lo_ = s.Lg[bP].x;
     const double fe = grid_fe(fe_max, rho, bJ);
     const double inv = 1.0 / fe;
     const double te = md.phi[bN * B1 + Bo] * inv;

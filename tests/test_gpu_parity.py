@@ -44,6 +44,32 @@ def test_random_full(J, seed, M_hi, N_hi, k_max):
     assert_solve_parity(gpu, orc, counts=True)
 
 
+def uniformise(b, seed=0):
+    """Copy user 0's device parameters to every user of each instance (only T differs),
+    keeping every user locally feasible: the kernel's uniform-users path."""
+    rng = np.random.default_rng(seed)
+    for i in range(b.n_inst):
+        o0, o1 = int(b.user_off[i]), int(b.user_off[i + 1])
+        for f in ("zeta", "kappa", "f_min", "f_max", "R", "p_u"):
+            getattr(b, f)[o0:o1] = getattr(b, f)[o0]
+        lat = float(g.min_local_latency(b.models[b.model_id[i]], np.array([b.zeta[o0]]), np.array([b.f_max[o0]]))[0])
+        beta = rng.uniform(0, 10, o1 - o0)
+        if rng.uniform() < 0.3:
+            beta[:] = beta[0]
+        b.T[o0:o1] = (1.0 + beta) * lat
+        if b.t_free[i] > b.T[o0:o1].min():
+            b.t_free[i] = 0.5 * b.T[o0:o1].min()
+    return b
+
+
+@pytest.mark.parametrize("seed,M_hi,N_hi,k_max", [(161, 8, 6, 40), (162, 32, 19, 200)])
+def test_random_uniform_users(J, seed, M_hi, N_hi, k_max):
+    b = uniformise(g.random_batch(seed=seed, n_inst=1500, M_lo=1, M_hi=M_hi, N_lo=1, N_hi=N_hi, k_max=k_max), seed)
+    _, gpu = run(J, b)
+    orc = O.solve_batch(b, counts=True)
+    assert_solve_parity(gpu, orc, counts=True)
+
+
 @pytest.mark.parametrize("mode", [1, 2, 3])
 def test_random_modes(J, mode):
     b = g.random_batch(seed=110 + mode, n_inst=800, M_lo=1, M_hi=16, N_lo=1, N_hi=8, k_max=64)
