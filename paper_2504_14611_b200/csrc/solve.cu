@@ -232,6 +232,7 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
                 else hi = mm;
             }
             const int p = lo;
+            const long long feb = __double_as_longlong(fe);
             // Alg. 2's break: the first j with an empty set ends this n~'s sweep
             const unsigned emp = __ballot_sync(0xffffffffu, valid && p == M);
             const long long jb = emp ? j0 + (__ffs(emp) - 1) : kk;
@@ -258,7 +259,6 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
                     }
                     const double te = phib * inv;
                     double E = 0.0;
-                    const long long feb = __double_as_longlong(fe);
                     if (uni) {
                         // Uniform users (same R, zeta, f_min, f_max, kappa, p_u; Table I): every member
                         // has the same budget, f* and offloader term, so D20/D21 are formed once and
