@@ -86,7 +86,10 @@ __global__ void k_bf_setup(const DevModel *models, DevBatch b, int space, BfHead
 }
 
 template <int MAXM>
-__global__ void __launch_bounds__(kBfWarps * 32) k_bf_main(const DevModel *models, int model_id, int space,
+#ifndef JDOB_BF_MINB
+#define JDOB_BF_MINB 4
+#endif
+__global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const DevModel *models, int model_id, int space,
                                                            unsigned long long idx_begin, unsigned long long idx_end,
                                                            const BfHeader *hdr, const double *tab,
                                                            const double *user, const double *invtab,
@@ -176,6 +179,24 @@ __global__ void __launch_bounds__(kBfWarps * 32) k_bf_main(const DevModel *model
                     if (nmin + 1 == n) Smin = S;
                 }
                 const bool any = nmin < N;
+                // per-vector hoists: REG (M <= 8) keeps l_o - O/R, zeta v, kappa u, (O/R) p per user in
+                // registers, so the candidate loop reads no shared memory for offloaders
+                constexpr bool REG = MAXM <= 8;
+                double lo[REG ? MAXM : 1], zvr[REG ? MAXM : 1], kur[REG ? MAXM : 1], upr[REG ? MAXM : 1];
+                unsigned offm = 0u;
+#pragma unroll
+                for (int m = 0; m < MAXM; m++) {
+                    if (m < M && nv[m] < N) {
+                        offm |= 1u << m;
+                        if constexpr (REG) {
+                            const int x = nv[m] * M + m;
+                            lo[m] = l_o - sOR[x];
+                            zvr[m] = sZV[x];
+                            kur[m] = sKU[x];
+                            upr[m] = sUP[x];
+                        }
+                    }
+                }
                 const unsigned long long jlo = (vec == vb) ? idx_begin - vb * uk : 0ull;
                 const unsigned long long jhi = (vec == ve - 1) ? idx_end - (ve - 1) * uk : uk;
                 for (unsigned long long j = jlo; j < jhi; j++) {
@@ -187,39 +208,45 @@ __global__ void __launch_bounds__(kBfWarps * 32) k_bf_main(const DevModel *model
 #pragma unroll
                     for (int m = 0; m < MAXM; m++) {
                         if (m >= M) break;
-                        const int n = nv[m];
                         double e;
-                        if (n < N) {
-                            const int x = n * M + m;
-                            const double budget = (l_o - sOR[x]) - Sm[m] * inv;
-                            const double zv = sZV[x];
-                            double f;
-                            if (zv == 0.0) {
-                                if (!(budget >= 0.0)) {
-                                    feas = false;
-                                    break;
-                                }
-                                f = sFmin[m];
+                        if ((offm >> m) & 1u) {
+                            double lom, zv, ku, up;
+                            if constexpr (REG) {
+                                lom = lo[m];
+                                zv = zvr[m];
+                                ku = kur[m];
+                                up = upr[m];
                             } else {
-                                if (!(budget > 0.0)) {
-                                    feas = false;
-                                    break;
-                                }
-                                const double fmin = sFmin[m];
-                                // exact low-clamp shortcut (DESIGN.md §Exact shortcuts): zv <= f_min*budget
-                                // exactly => RN(zv/budget) <= f_min <= f_max, so f* = f_min, feasible.
-                                if (fmin >= 1e-100 && budget >= 1e-100 && __fma_rn(fmin, budget, -zv) >= 0.0) {
-                                    f = fmin;
-                                } else {
-                                    const double G = zv / budget;
-                                    if (G > sFmax[m]) {
+                                const int x = nv[m] * M + m;
+                                lom = l_o - sOR[x];
+                                zv = sZV[x];
+                                ku = sKU[x];
+                                up = sUP[x];
+                            }
+                            const double budget = lom - Sm[m] * inv;  // (l_o - O/R) - S_{n_m+1}/f_e
+                            double f = sFmin[m];
+                            // exact low clamp: fmin*budget > zv exactly => budget > 0 and
+                            // RN(zv/budget) <= f_min <= f_max: feasible with f* = f_min (R9 when zv = 0)
+                            if (!(__fma_rn(f, budget, -zv) > 0.0)) {
+                                if (zv == 0.0) {
+                                    if (!(budget >= 0.0)) {
                                         feas = false;
                                         break;
                                     }
-                                    f = (G < fmin) ? fmin : G;
+                                } else {
+                                    if (!(budget > 0.0)) {
+                                        feas = false;
+                                        break;
+                                    }
+                                    const double G = zv / budget;
+                                    if (G > sFmax[m]) {  // D7' with D13 (exact, R10)
+                                        feas = false;
+                                        break;
+                                    }
+                                    f = (G < f) ? f : G;
                                 }
                             }
-                            e = ((sKU[x] * f) * f) + sUP[x];
+                            e = ((ku * f) * f) + up;
                         } else {
                             e = sEl[m];
                         }
