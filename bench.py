@@ -196,11 +196,11 @@ def run_mine(args):
     import torch
     world, rank, local = dist_env()
     dist = None
-    if world > 1:
+    torch.cuda.set_device(local)
+    if world > 1 or "TORCHELASTIC_RUN_ID" in os.environ:   # launched by torchrun (also at N = 1)
         import torch.distributed as D
         D.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = D
-    torch.cuda.set_device(local)
     import paper_2504_14611_b200 as J
     label, n_default = WORKLOADS[args.workload]
     n = args.n_inst or n_default
