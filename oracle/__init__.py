@@ -55,6 +55,12 @@ class OResult(C.Structure):
                 ("n_visit", C.c_longlong), ("n_eval", C.c_longlong), ("n_member", C.c_longlong)]
 
 
+class OOgResult(C.Structure):
+    _fields_ = [("E", C.c_double), ("t_free_next", C.c_double), ("status", C.c_int), ("n_groups", C.c_int),
+                ("group_of", C.c_int * 32), ("part", C.c_int * 32), ("f_user", C.c_double * 32),
+                ("group_fe", C.c_double * 32), ("group_start", C.c_int * 33)]
+
+
 class OBatch(C.Structure):
     _fields_ = [("models", C.POINTER(OModel)), ("model_id", C.POINTER(C.c_int)),
                 ("user_off", C.POINTER(C.c_longlong))] + \
@@ -99,6 +105,7 @@ def lib():
             L.oracle_stats.argtypes = [C.c_longlong, P(C.c_longlong), P(C.c_int), C.c_int, P(C.c_double),
                                        P(C.c_double), P(C.c_int), P(C.c_uint), P(C.c_int), P(C.c_double)]
             L.oracle_grid_k.argtypes = [P(OInst)]
+            L.oracle_og.argtypes = [P(OModel), P(OInst), C.c_int, P(OOgResult)]
             _lib = L
     return _lib
 
@@ -310,3 +317,29 @@ def partition_from_plan(batch, res) -> np.ndarray:
         for u in range(batch.M(i)):
             part[o0 + u] = res["n_tilde"][i] if (int(res["mask"][i]) >> u) & 1 else N
     return part
+
+
+def og(batch, i=0, mode=MODE_FULL) -> dict:
+    """Outer grouping DP over deadline-sorted users with the inner J-DOB (reading R21)."""
+    keep = _Keep()
+    r = OOgResult()
+    lib().oracle_og(C.byref(_omodel(batch.models[batch.model_id[i]], keep)), C.byref(_oinst(batch, i, keep)),
+                    mode, C.byref(r))
+    M = batch.M(i)
+    ng = r.n_groups
+    return dict(E=r.E, t_free_next=r.t_free_next, status=r.status, n_groups=ng,
+                group_of=np.array(r.group_of[:M]), part=np.array(r.part[:M]), f_user=np.array(r.f_user[:M]),
+                group_fe=np.array(r.group_fe[:ng]), group_start=np.array(r.group_start[:ng + 1]))
+
+
+def og_batch(batch, mode=MODE_FULL) -> dict:
+    n = batch.n_inst
+    rs = [og(batch, i, mode) for i in range(n)]
+    out = dict(E=np.array([r["E"] for r in rs]), t_free_next=np.array([r["t_free_next"] for r in rs]),
+               status=np.array([r["status"] for r in rs], np.int32),
+               n_groups=np.array([r["n_groups"] for r in rs], np.int32),
+               group_of=np.concatenate([r["group_of"] for r in rs]).astype(np.int32),
+               part=np.concatenate([r["part"] for r in rs]).astype(np.int32),
+               f_user=np.concatenate([r["f_user"] for r in rs]),
+               group_fe=np.stack([np.pad(r["group_fe"], (0, 32 - len(r["group_fe"]))) for r in rs]))
+    return out

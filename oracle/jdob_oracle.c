@@ -861,3 +861,132 @@ int oracle_stats(long long n_inst, const long long *user_off, const int *bucket,
 }
 
 int oracle_grid_k(const o_inst *in) { return (int)o_grid_k(in); }
+
+/* ------------------------------------------------------------------ */
+/* Outer grouping (reading R21).              */
+/* "an outer module that groups users by deadline similarity"; */
+/* the paper uses the dynamic program for optimal grouping (OG) of its  */
+/* reference [shi2022multiuser] whose internals it does not */
+/* print; we follow SPEC S:295-303: users sorted by deadline (ascending,*/
+/* ties by index), a DP over prefixes where cell i keeps the           */
+/* lexicographically best (energy, t_free) of the first i sorted users, */
+/* transition j -> i = group {j..i-1} solved by the inner J-DOB with    */
+/* t_free = cell j's t_free (a failed Require is costed all-local with  */
+/* t_free unchanged, which the inner solver's REQUIRE status returns);  */
+/* strict improvement, so ties keep the smallest j.                    */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    double E, t_free_next;
+    int status, n_groups;
+    int group_of[O_MAXM];     /* per user (input index): group number in execution order */
+    int part[O_MAXM];         /* per user: partition point, N = local */
+    double f_user[O_MAXM];
+    double group_fe[O_MAXM];  /* per group: f_e, 0 = all local */
+    int group_start[O_MAXM + 1];
+} o_og_result;
+
+static void o_group_inst(const o_inst *in, const int *sorted, int j, int i, double t_free, double *buf, o_inst *g) {
+    int n = i - j;
+    double *z = buf, *k = buf + 32, *f0 = buf + 64, *f1 = buf + 96, *R = buf + 128, *p = buf + 160, *T = buf + 192;
+    for (int q = 0; q < n; q++) {
+        int u = sorted[j + q];
+        z[q] = in->zeta[u];
+        k[q] = in->kappa[u];
+        f0[q] = in->f_min[u];
+        f1[q] = in->f_max[u];
+        R[q] = in->R[u];
+        p[q] = in->p_u[u];
+        T[q] = in->T[u];
+    }
+    g->M = n;
+    g->zeta = z;
+    g->kappa = k;
+    g->f_min = f0;
+    g->f_max = f1;
+    g->R = R;
+    g->p_u = p;
+    g->T = T;
+    g->t_free = t_free;
+    g->fe_min = in->fe_min;
+    g->fe_max = in->fe_max;
+    g->rho = in->rho;
+}
+
+int oracle_og(const o_model *m, const o_inst *in, int mode, o_og_result *r) {
+    memset(r, 0, sizeof(*r));
+    int st = oracle_check_inst(m, in);
+    if (st == O_ST_REQUIRE) st = O_ST_OK; /* the DP costs a failed Require per group */
+    r->status = st;
+    int M = in->M;
+    if (st != O_ST_OK) {
+        o_result lr;
+        oracle_jdob(m, in, 1, &lr); /* LC answer (or NaN for malformed input) */
+        r->E = lr.E;
+        r->t_free_next = in->t_free;
+        r->n_groups = 0;
+        for (int u = 0; u < M && u < O_MAXM; u++) {
+            r->part[u] = m->N;
+            r->f_user[u] = lr.f_user[u];
+        }
+        return st;
+    }
+    /* deadline order, ties by index (insertion sort) */
+    int sorted[O_MAXM];
+    for (int u = 0; u < M; u++) sorted[u] = u;
+    for (int a = 1; a < M; a++) {
+        int x = sorted[a], b = a - 1;
+        while (b >= 0 && (in->T[x] < in->T[sorted[b]])) {
+            sorted[b + 1] = sorted[b];
+            b--;
+        }
+        sorted[b + 1] = x;
+    }
+    double cE[O_MAXM + 1], cT[O_MAXM + 1];
+    int from[O_MAXM + 1];
+    cE[0] = 0.0;
+    cT[0] = in->t_free;
+    from[0] = -1;
+    double buf[224];
+    for (int i = 1; i <= M; i++) {
+        cE[i] = O_INF;
+        cT[i] = O_INF;
+        from[i] = -1;
+        for (int j = 0; j < i; j++) {
+            o_inst g;
+            o_group_inst(in, sorted, j, i, cT[j], buf, &g);
+            o_result gr;
+            oracle_jdob(m, &g, mode, &gr);
+            double E = cE[j] + gr.E;
+            double tf = gr.t_free_next;
+            if (E < cE[i] || (E == cE[i] && tf < cT[i])) {
+                cE[i] = E;
+                cT[i] = tf;
+                from[i] = j;
+            }
+        }
+    }
+    /* backtrack and re-solve the chosen groups for the schedule */
+    int starts[O_MAXM + 1], ng = 0;
+    for (int i = M; i > 0; i = from[i]) starts[ng++] = from[i];
+    r->E = cE[M];
+    r->t_free_next = cT[M];
+    r->n_groups = ng;
+    for (int gi = 0; gi < ng; gi++) {
+        int j = starts[ng - 1 - gi];
+        int i = (gi + 1 < ng) ? starts[ng - 2 - gi] : M;
+        r->group_start[gi] = j;
+        o_inst g;
+        o_group_inst(in, sorted, j, i, cT[j], buf, &g);
+        o_result gr;
+        oracle_jdob(m, &g, mode, &gr);
+        r->group_fe[gi] = gr.f_e;
+        for (int q = 0; q < i - j; q++) {
+            int u = sorted[j + q];
+            r->group_of[u] = gi;
+            r->part[u] = ((gr.mask >> q) & 1u) ? gr.n_tilde : m->N;
+            r->f_user[u] = gr.f_user[q];
+        }
+    }
+    r->group_start[ng] = M;
+    return st;
+}
