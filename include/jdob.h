@@ -235,6 +235,44 @@ JDOB_API int jdob_eval(const jdob_model *models, int32_t n_models, const jdob_ba
                        double *E, double *t_free_next, double *f_user, uint32_t *violations, int32_t *status,
                        void *ws, size_t ws_bytes, void *stream);
 
+/*
+ * Outputs of jdob_solve_grouped (DEVICE pointers, caller-allocated).
+ *   E [n_inst]            : total energy of the grouped schedule.
+ *   t_free_next [n_inst]  : GPU-available time after the last group.
+ *   n_groups [n_inst]     : number of groups (0 for a non-OK status).
+ *   status [n_inst]       : JDOB_ST_* (a failed Require is costed inside the DP, so REQUIRE is
+ *                           never reported here).
+ *   group_of [users]      : group of each user, numbered in execution order (ascending deadlines).
+ *   partition [users]     : partition point of each user (N = local).
+ *   f_user [users]        : device frequency f* of each user (may be NULL).
+ *   group_fe [n_inst*32]  : edge frequency of group g at [i*32 + g] (0.0 = all-local group).
+ */
+typedef struct {
+    double *E, *t_free_next;
+    int32_t *n_groups, *status;
+    int32_t *group_of, *partition;
+    double *f_user, *group_fe;
+} jdob_grouped_result;
+
+/* Workspace bytes of jdob_solve_grouped for a batch of n_inst instances and n_users users. */
+JDOB_API size_t jdob_grouped_workspace_bytes(const jdob_model *models, int32_t n_models, int64_t n_inst,
+                                            int64_t n_users);
+
+/*
+ * Outer grouping over deadline-sorted users with J-DOB as the inner module (
+ * PAPER.md: "an outer module that groups users by deadline similarity" P:183, the optimal-
+ * grouping DP of the different-deadline experiments P:430-431, reading R21 = SPEC S:295-303):
+ * users sorted by deadline (ties by index); cell i of a DP over prefixes keeps the
+ * lexicographically best (energy, t_free) of the first i users; the transition j -> i is the
+ * group of sorted users j..i-1 solved by jdob (mode `mode`) at t_free = cell j's t_free; a
+ * group whose earliest deadline is below that t_free is costed all-local (Alg. 1's Require,
+ * P:259).  Bit-identical to the CPU oracle.  Performs one small synchronous device->host read
+ * (the largest M, 4 bytes) to size the DP stages.
+ * Errors: JDOB_EINVAL (NULL pointers, small workspace), JDOB_ECUDA.
+ */
+JDOB_API int jdob_solve_grouped(const jdob_model *models, int32_t n_models, const jdob_batch *b, int32_t mode,
+                                const jdob_grouped_result *out, void *ws, size_t ws_bytes, void *stream);
+
 /* Message of the last call-level error on this thread ("" if none). */
 JDOB_API const char *jdob_last_error(void);
 

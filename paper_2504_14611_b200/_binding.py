@@ -41,6 +41,11 @@ class JResult(C.Structure):
                                           "f_user", "counts", "stats")] + [("n_buckets", C.c_int32)]
 
 
+class JGrouped(C.Structure):
+    _fields_ = [(f, C.c_void_p) for f in ("E", "t_free_next", "n_groups", "status", "group_of", "partition", "f_user",
+                                          "group_fe")]
+
+
 _lock = threading.Lock()
 _lib = None
 
@@ -71,6 +76,10 @@ def lib():
             L.jdob_eval.argtypes = [_P(JModel), C.c_int32, _P(JBatch), C.c_void_p, C.c_void_p, C.c_void_p,
                                     C.c_void_p, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                     C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
+            L.jdob_grouped_workspace_bytes.argtypes = [_P(JModel), C.c_int32, C.c_int64, C.c_int64]
+            L.jdob_grouped_workspace_bytes.restype = C.c_size_t
+            L.jdob_solve_grouped.argtypes = [_P(JModel), C.c_int32, _P(JBatch), C.c_int32, _P(JGrouped), C.c_void_p,
+                                             C.c_size_t, C.c_void_p]
             L.jdob_last_error.restype = C.c_char_p
             L.jdob_version.restype = C.c_char_p
             _lib = L
@@ -78,7 +87,8 @@ def lib():
 
 
 EXPORTED = ("jdob_workspace_bytes", "jdob_solve_batch", "jdob_solve_batch_host", "jdob_bruteforce",
-            "jdob_bf_space_size", "jdob_eval", "jdob_last_error", "jdob_version")
+            "jdob_bf_space_size", "jdob_eval", "jdob_grouped_workspace_bytes", "jdob_solve_grouped",
+            "jdob_last_error", "jdob_version")
 
 
 def _check(rc):
@@ -302,3 +312,30 @@ def solve_batch_host(hb: HostBuffers, mode: int = MODE_FULL, stream=None):
     _check(lib().jdob_solve_batch_host(hb.jmodels, hb.n_models, C.byref(hb.jbatch), int(mode), C.byref(r),
                                        _stream_handle(stream), C.byref(h2d), C.byref(d2h)))
     return h2d.value, d2h.value
+
+
+def solve_grouped(db: DeviceBatch, mode: int = MODE_FULL, f_user: bool = True, stream=None) -> dict:
+    """jdob_solve_grouped: outer grouping DP over deadline-sorted users with J-DOB inside (NEXT-1)."""
+    torch = _torch()
+    dev = db.device
+    n, nu = db.n_inst, db.n_users
+    out = dict(E=torch.empty(n, dtype=torch.float64, device=dev),
+               t_free_next=torch.empty(n, dtype=torch.float64, device=dev),
+               n_groups=torch.empty(n, dtype=torch.int32, device=dev),
+               status=torch.empty(n, dtype=torch.int32, device=dev),
+               group_of=torch.empty(nu, dtype=torch.int32, device=dev),
+               partition=torch.empty(nu, dtype=torch.int32, device=dev),
+               f_user=torch.empty(nu, dtype=torch.float64, device=dev) if f_user else None,
+               group_fe=torch.empty((n, MAX_M), dtype=torch.float64, device=dev))
+    nb = int(lib().jdob_grouped_workspace_bytes(db.jmodels, db.n_models, n, nu))
+    if nb == 0:
+        raise JdobError("jdob_grouped_workspace_bytes returned 0")
+    key = ("grouped", nb)
+    if key not in db._ws:
+        db._ws[key] = torch.empty(nb, dtype=torch.uint8, device=dev)
+    ws = db._ws[key]
+    r = JGrouped(*[_ptr(out[f]) for f in ("E", "t_free_next", "n_groups", "status", "group_of", "partition",
+                                          "f_user", "group_fe")])
+    _check(lib().jdob_solve_grouped(db.jmodels, db.n_models, C.byref(db.jbatch), int(mode), C.byref(r),
+                                    ws.data_ptr(), ws.numel(), _stream_handle(stream)))
+    return out

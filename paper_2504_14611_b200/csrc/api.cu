@@ -127,6 +127,7 @@ static DevBatch to_dev(const jdob_batch *b) {
     d.n_models = b->n_models;
     d.model_id = b->model_id;
     d.user_off = (const long long *)b->user_off;
+    d.user_end = nullptr;
     d.zeta = b->zeta;
     d.kappa = b->kappa;
     d.f_min = b->f_min;
@@ -239,6 +240,89 @@ int jdob_solve_batch(const jdob_model *models, int32_t n_models, const jdob_batc
         if ((rc = cuda_check("stats"))) return rc;
     }
     return JDOB_OK;
+}
+
+static size_t og_work_bytes(int64_t n, int64_t nu) {
+    const size_t ns = (size_t)n * kMaxM, nc = (size_t)n * kCells;
+    return 9 * al(nu * 8) + 2 * al(nc * 8) + al(nc * 4) + 2 * al(n * 4) + al(8) + 2 * al(ns * 8) + al(ns * 4) +
+           4 * al(ns * 8) + 4 * al(ns * 8) + 4 * al(ns * 4);
+}
+
+size_t jdob_grouped_workspace_bytes(const jdob_model *models, int32_t n_models, int64_t n_inst, int64_t n_users) {
+    const size_t base = jdob_workspace_bytes(models, n_models, 0);
+    if (base == 0 || n_inst < 0 || n_users < 0) return 0;
+    return base + og_work_bytes(n_inst, n_users);
+}
+
+int jdob_solve_grouped(const jdob_model *models, int32_t n_models, const jdob_batch *b, int32_t mode,
+                       const jdob_grouped_result *out, void *ws, size_t ws_bytes, void *stream) {
+    g_err.clear();
+    int rc = check_models(models, n_models);
+    if (rc) return rc;
+    if ((rc = check_batch(b, n_models))) return rc;
+    if (mode < JDOB_MODE_FULL || mode > JDOB_MODE_BINARY) return fail(JDOB_EINVAL, "bad mode %d", mode);
+    if (!out || (b->n_inst > 0 && (!out->E || !out->t_free_next || !out->n_groups || !out->status ||
+                                   !out->group_of || !out->partition || !out->group_fe)))
+        return fail(JDOB_EINVAL, "grouped result has a NULL required array");
+    cudaStream_t s = (cudaStream_t)stream;
+    const long long n = b->n_inst;
+    if (n == 0) return JDOB_OK;
+    long long nu = 0;
+    cudaMemcpyAsync(&nu, b->user_off + n, sizeof(long long), cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_check("grouped: read user_off");
+    const size_t need = jdob_grouped_workspace_bytes(models, n_models, n, nu);
+    if (!ws || ws_bytes < need) return fail(JDOB_EINVAL, "workspace %zu bytes < %zu", ws_bytes, need);
+    DevModel *dm = nullptr;
+    if ((rc = prepare_models(models, n_models, (char *)ws, &dm, s))) return rc;
+    char *p = (char *)ws + jdob_workspace_bytes(models, n_models, 0);
+    auto take = [&](size_t nb) -> char * {
+        char *d = p;
+        p += al(nb);
+        return d;
+    };
+    const size_t ns = (size_t)n * kMaxM, nc = (size_t)n * kCells;
+    OgWork w;
+    w.sz = (double *)take(nu * 8);
+    w.sk = (double *)take(nu * 8);
+    w.sf0 = (double *)take(nu * 8);
+    w.sf1 = (double *)take(nu * 8);
+    w.sR = (double *)take(nu * 8);
+    w.sp = (double *)take(nu * 8);
+    w.sT = (double *)take(nu * 8);
+    w.perm = (long long *)take(nu * 8);
+    w.fs = (double *)take(nu * 8);
+    w.cE = (double *)take(nc * 8);
+    w.cT = (double *)take(nc * 8);
+    w.from = (int *)take(nc * 4);
+    w.status = (int *)take(n * 4);
+    w.ngroups = (int *)take(n * 4);
+    w.mmax = (int *)take(8);
+    w.s_off = (long long *)take(ns * 8);
+    w.s_end = (long long *)take(ns * 8);
+    w.s_model = (int *)take(ns * 4);
+    w.s_tfree = (double *)take(ns * 8);
+    w.s_femin = (double *)take(ns * 8);
+    w.s_femax = (double *)take(ns * 8);
+    w.s_rho = (double *)take(ns * 8);
+    w.r_E = (double *)take(ns * 8);
+    w.r_Elc = (double *)take(ns * 8);
+    w.r_tf = (double *)take(ns * 8);
+    w.r_fe = (double *)take(ns * 8);
+    w.r_nt = (int *)take(ns * 4);
+    w.r_j = (int *)take(ns * 4);
+    w.r_st = (int *)take(ns * 4);
+    w.r_mask = (unsigned *)take(ns * 4);
+    GroupedOut o;
+    o.E = out->E;
+    o.t_free_next = out->t_free_next;
+    o.n_groups = out->n_groups;
+    o.status = out->status;
+    o.group_of = out->group_of;
+    o.partition = out->partition;
+    o.f_user = out->f_user;
+    o.group_fe = out->group_fe;
+    if (launch_grouped(dm, to_dev(b), mode, w, o, s, num_sms())) return cuda_check("grouped");
+    return cuda_check("grouped");
 }
 
 int jdob_eval(const jdob_model *models, int32_t n_models, const jdob_batch *b, const int32_t *partition,

@@ -35,6 +35,7 @@ struct DevBatch {
     int n_models;
     const int *model_id;
     const long long *user_off;
+    const long long *user_end;  // internal: if set, instance i's users end at user_end[i] (overlapping views)
     const double *zeta, *kappa, *f_min, *f_max, *R, *p_u, *T;
     const double *t_free, *fe_min, *fe_max, *rho;
     const int *bucket;
@@ -89,7 +90,7 @@ __device__ __forceinline__ int warp_validate(const DevModel *models, const DevBa
                                              InstRegs &x, int &M, long long &k, const DevModel *&mdp,
                                              long long &off) {
     off = b.user_off[i];
-    const long long M64 = b.user_off[i + 1] - off;
+    const long long M64 = (b.user_end ? b.user_end[i] : b.user_off[i + 1]) - off;
     M = (M64 >= 1 && M64 <= kMaxM) ? (int)M64 : 0;
     k = 0;
     x.z = x.k = x.f0 = x.f1 = x.R = x.p = 0.0;

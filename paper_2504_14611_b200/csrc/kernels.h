@@ -22,7 +22,33 @@ constexpr int kStatsWarps = 2;
 constexpr int kBfBlocks = 148 * 8;   // persistent brute-force grid
 constexpr int kBfWarps = 4;
 
+// outer grouping (K5) work arrays, all in the caller's workspace
+constexpr int kCells = kMaxM + 1;
+struct OgWork {
+    double *sz, *sk, *sf0, *sf1, *sR, *sp, *sT;  // [users] user parameters in deadline order
+    long long *perm;                             // [users] sorted position -> input user index
+    double *fs;                                  // [users] f* of the final pass (sorted order)
+    double *cE, *cT;                             // [n_inst * kCells] DP cells
+    int *from;                                   // [n_inst * kCells]
+    int *status, *ngroups;                       // [n_inst]
+    int *mmax;                                   // [1]
+    long long *s_off, *s_end;                    // [n_inst * kMaxM] stage views
+    int *s_model;
+    double *s_tfree, *s_femin, *s_femax, *s_rho;
+    double *r_E, *r_Elc, *r_tf, *r_fe;           // [n_inst * kMaxM] stage results
+    int *r_nt, *r_j, *r_st;
+    unsigned *r_mask;
+};
+struct GroupedOut {
+    double *E, *t_free_next;
+    int *n_groups, *status;
+    int *group_of, *partition;
+    double *f_user, *group_fe;
+};
+
 void launch_aggregates(const ModelChunk &chunk, cudaStream_t s);
+int launch_grouped(const DevModel *models, const DevBatch &b, int mode, const OgWork &w, const GroupedOut &o,
+                   cudaStream_t s, int num_sms);
 void launch_solve(const DevModel *models, const DevBatch &b, const DevResult &r, int mode, cudaStream_t s,
                   int num_sms);
 void launch_stats(const DevBatch &b, const DevResult &r, double *partials, double *stats, int n_buckets,

@@ -298,3 +298,47 @@ def test_bf_c4_full(J):
     lo, hi = max(0, I - 1_000_000), min(size, I + 1_000_000)
     Eo, Io, _ = O.bf(b, 0, lo, hi, threads=8)
     assert Eo == E and Io == I
+
+
+# ------------------------------- outer grouping (NEXT-1) --------------------------
+def _og_parity(J, b, mode=0):
+    db = J.DeviceBatch(b)
+    res = J.solve_grouped(db, mode=mode)
+    import torch
+    torch.cuda.synchronize()
+    gpu = {k: v.cpu().numpy() for k, v in res.items() if v is not None}
+    orc = O.og_batch(b, mode=mode)
+    for f in ("E", "t_free_next", "status", "n_groups", "group_of", "part", "f_user"):
+        gf = "partition" if f == "part" else f
+        assert_bits_equal(gpu[gf].reshape(-1), orc[f].reshape(-1), "og " + f)
+    assert_bits_equal(gpu["group_fe"], orc["group_fe"], "og group_fe")
+
+
+def test_og_toys(J):
+    for T in ([0.2, 0.6], [0.2, 0.2], [0.6, 0.2]):
+        b = g.toy_instance("toy-2")
+        b.T[:] = T
+        _og_parity(J, b)
+
+
+@pytest.mark.parametrize("seed,M_hi,N_hi", [(171, 6, 5), (172, 16, 8)])
+def test_og_random(J, seed, M_hi, N_hi):
+    b = g.random_batch(seed=seed, n_inst=300, M_lo=1, M_hi=M_hi, N_lo=1, N_hi=N_hi, k_max=40, tfree_frac=0.4)
+    _og_parity(J, b)
+
+
+def test_og_c3_sample(J):
+    # the paper's different-deadline setting: OG + J-DOB on C3-like instances
+    b = g.config_batch("c3", n_inst=400)
+    _og_parity(J, b)
+    b = g.config_batch("c3", n_inst=200)
+    _og_parity(J, b, mode=2)
+
+
+def test_og_statuses(J):
+    parts = []
+    b = g.toy_instance("toy-1"); b.T[0] = 0.1; parts.append(b)        # LOCAL_INFEASIBLE
+    b = g.toy_instance("toy-1"); b.t_free[0] = 0.21; parts.append(b)   # Require fails for the first group
+    b = g.toy_instance("toy-1"); b.f_min[1] = 3e9; parts.append(b)     # BADPARAM
+    for b in parts:
+        _og_parity(J, b)
