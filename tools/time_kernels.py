@@ -44,8 +44,27 @@ def t_bf(frac):
     return {"cfg": "c4bf", "cand": hi, "ms": ms, "cand_per_s": hi / ms * 1e3, "E": float(E.item()), "I": int(I.item())}
 
 
+def t_grouped(cfg, n):
+    b = G.config_batch(cfg, n_inst=n)
+    db = J.DeviceBatch(b)
+    J.solve_grouped(db, f_user=False)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    r = J.solve_grouped(db, f_user=False)
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e)
+    return {"cfg": cfg + "_grouped", "n": n, "ms": ms, "inst_per_s": n / ms * 1e3,
+            "mean_groups": float(r["n_groups"].float().mean().item())}
+
+
 if __name__ == "__main__":
     lib = os.environ.get("JDOB_LIB", "default")
-    for r in (t_solve("c2", 1 << 20), t_solve("c3", 100_000), t_solve("c5", 1_000_000), t_bf(0.25)):
+    which = sys.argv[1:] or ["c2", "c3", "c5", "bf"]
+    todo = {"c2": lambda: t_solve("c2", 1 << 20), "c3": lambda: t_solve("c3", 100_000),
+            "c5": lambda: t_solve("c5", 1_000_000), "bf": lambda: t_bf(0.25),
+            "og": lambda: t_grouped("c3", 100_000)}
+    for r in (todo[w]() for w in which):
         r["lib"] = os.path.basename(lib)
         print(json.dumps(r), flush=True)
