@@ -272,7 +272,7 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
 #pragma unroll 4
                         for (int m = 0; m < M; m++) {
                             const double2 et = *reinterpret_cast<const double2 *>(&s.u[m].eloc);  // eloc, thu
-                            const bool mem = feb >= __double_as_longlong(et.y);
+                            const bool mem = !(fe < et.y);  // FP64-pipe compare: the ALU pipe is the busier one here
                             E = E + (mem ? em : et.x);
                         }
                     } else {
