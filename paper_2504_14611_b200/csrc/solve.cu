@@ -36,15 +36,12 @@ namespace jdob {
 
 constexpr int kInvCache = 192;    // 1/f_e(j) cached for j < kInvCache
 
-struct __align__(16) UserSlot {  // per user, per n~ (lane-broadcast reads)
-    double OR, zv;               // O_n~/R_m, zeta_m v_n~
-    double ku, up;               // kappa_m u_n~, (O_n~/R_m) p_m
-    double eloc, thu;            // local energy e_loc,m; th_{r_m} if r_m >= i^ else +inf
-    double fmin, fmax;           // f_m,min, f_m,max
-};
-
 struct SolveSmem {
-    UserSlot u[kMaxM];
+    // per-user values as 16-byte pairs (lane stride 16 B: 4-way store conflicts at most)
+    double2 orzv[kMaxM];                 // O_n~/R_m, zeta_m v_n~
+    double2 kuup[kMaxM];                 // kappa_m u_n~, (O_n~/R_m) p_m
+    double2 et[kMaxM];                   // e_loc,m, th_{r_m} if r_m >= i^ else +inf
+    double2 fmm[kMaxM];                  // f_m,min, f_m,max
     double R[kMaxM], z[kMaxM], f1[kMaxM], kap[kMaxM], pu[kMaxM];  // user parameters (lane = user)
     double T[kMaxM], gam[kMaxM];
     double th[kMaxM];
@@ -80,18 +77,18 @@ __device__ __forceinline__ void sort_users(int M, double gam, double T, SolveSme
 }
 
 // Alg. 1 lines 4-6 for partition point nt.  Returns i^ (M if none).
-__device__ __forceinline__ int setup_nt(const DevModel &md, int nt, int M, bool homog, double t_free, SolveSmem &s,
-                                        int lane) {
+__device__ __forceinline__ int setup_nt(const DevModel &md, int nt, int M, bool homog, bool uni, double t_free,
+                                        SolveSmem &s, int lane) {
     const double v_nt = md.v[nt], u_nt = md.u[nt], O_nt = md.O[nt];
     double gam = 0.0;
     if (lane < M) {
         const double OR = O_nt / s.R[lane];  // Eq. (3)
         const double zv = s.z[lane] * v_nt;
         gam = OR + zv / s.f1[lane];          // gamma
-        s.u[lane].OR = OR;
-        s.u[lane].zv = zv;
-        s.u[lane].ku = s.kap[lane] * u_nt;
-        s.u[lane].up = OR * s.pu[lane];      // Eq. (4)
+        if (!uni || lane == 0) {             // uniform users: one copy serves every member
+            s.orzv[lane] = make_double2(OR, zv);
+            s.kuup[lane] = make_double2(s.kap[lane] * u_nt, OR * s.pu[lane]);  // Eq. (4)
+        }
         s.gam[lane] = gam;
     }
     if (!homog) sort_users(M, gam, s.T[lane], s, lane);  // homogeneous: order fixed per instance
@@ -110,7 +107,7 @@ __device__ __forceinline__ int setup_nt(const DevModel &md, int nt, int M, bool 
     __syncwarp();
     if (lane < M) {
         const int rm = s.rank[lane];
-        s.u[lane].thu = (rm >= ihat) ? s.th[rm] : dinf();
+        s.et[lane].y = (rm >= ihat) ? s.th[rm] : dinf();
     }
     __syncwarp();
     return ihat;
@@ -180,9 +177,8 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
     if (lane < M) {
         floc = clampf((x.z * vN) / x.T, x.f0, x.f1);
         eloc = ((x.k * uN) * floc) * floc;
-        s.u[lane].eloc = eloc;
-        s.u[lane].fmin = x.f0;
-        s.u[lane].fmax = x.f1;
+        s.et[lane].x = eloc;
+        s.fmm[lane] = make_double2(x.f0, x.f1);
         s.R[lane] = x.R;
         s.z[lane] = x.z;
         s.f1[lane] = x.f1;
@@ -219,7 +215,7 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
 
     for (int nt = 0; nt < N; nt++) {
         if (mode == JDOB_MODE_BINARY && nt != 0) break;
-        const int ihat = setup_nt(md, nt, M, homog, t_free, s, lane);
+        const int ihat = setup_nt(md, nt, M, homog, uni, t_free, s, lane);
         for (long long j0 = 0; j0 < kk; j0 += 32) {
             const long long j = j0 + lane;
             const bool valid = j < kk;
@@ -263,25 +259,25 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
                         // Uniform users (same R, zeta, f_min, f_max, kappa, p_u; Table I): every member
                         // has the same budget, f* and offloader term, so D20/D21 are formed once and
                         // only the user-order sum runs over M.  Same operations, same bits.
-                        const UserSlot &u0 = s.u[0];
-                        const double budget = (lo_ - u0.OR) - te;
-                        double f = u0.fmin;
-                        if (!(__fma_rn(u0.fmin, budget, -u0.zv) > 0.0) && u0.zv != 0.0)
-                            f = clampf(u0.zv / budget, u0.fmin, u0.fmax);  // D20 (R9 when zv = 0)
-                        const double em = ((u0.ku * f) * f) + u0.up;       // D21 offloader term
+                        const double2 a0 = s.orzv[0], c0 = s.kuup[0], t0 = s.fmm[0];
+                        const double budget = (lo_ - a0.x) - te;
+                        double f = t0.x;
+                        if (!(__fma_rn(t0.x, budget, -a0.y) > 0.0) && a0.y != 0.0)
+                            f = clampf(a0.y / budget, t0.x, t0.y);  // D20 (R9 when zv = 0)
+                        const double em = ((c0.x * f) * f) + c0.y;  // D21 offloader term
 #pragma unroll 4
                         for (int m = 0; m < M; m++) {
-                            const double2 et = *reinterpret_cast<const double2 *>(&s.u[m].eloc);  // eloc, thu
+                            const double2 et = s.et[m];     // eloc, thu
                             const bool mem = !(fe < et.y);  // FP64-pipe compare: the ALU pipe is the busier one here
                             E = E + (mem ? em : et.x);
                         }
                     } else {
 #pragma unroll 4
                         for (int m = 0; m < M; m++) {
-                            const double2 a = *reinterpret_cast<const double2 *>(&s.u[m].OR);    // OR, zv
-                            const double2 c = *reinterpret_cast<const double2 *>(&s.u[m].ku);    // ku, up
-                            const double2 d = *reinterpret_cast<const double2 *>(&s.u[m].eloc);  // eloc, thu
-                            const double2 t = *reinterpret_cast<const double2 *>(&s.u[m].fmin);  // fmin, fmax
+                            const double2 a = s.orzv[m];  // OR, zv
+                            const double2 c = s.kuup[m];  // ku, up
+                            const double2 d = s.et[m];    // eloc, thu
+                            const double2 t = s.fmm[m];   // fmin, fmax
                             // f_e, th >= 0 (or +inf): IEEE order = integer order of the bit patterns
                             const bool mem = feb >= __double_as_longlong(d.y);
                             const double budget = (lo_ - a.x) - te;
@@ -342,7 +338,7 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
         return;
     }
     // winner: recompute D20 and D22 lane = user (same arithmetic as the sweep)
-    setup_nt(md, bN, M, homog, t_free, s, lane);
+    setup_nt(md, bN, M, homog, false, t_free, s, lane);  // per-user copies for the winner
     const int Bo = M - bP;
     const double lo_ = s.Lg[bP].x;
     const double fe = grid_fe(fe_max, rho, bJ);
@@ -351,11 +347,11 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
     const bool member = (lane < M) && (s.rank[lane] >= bP);
     double f = floc, arr = t_free;
     if (member) {
-        const UserSlot &us = s.u[lane];
-        const double budget = (lo_ - us.OR) - te;
-        const bool low = (us.zv == 0.0) || (__fma_rn(us.fmin, budget, -us.zv) > 0.0);
-        f = low ? us.fmin : clampf(us.zv / budget, us.fmin, us.fmax);
-        arr = us.zv / f + us.OR;
+        const double2 a = s.orzv[lane], t = s.fmm[lane];  // (O/R, zv), (f_min, f_max)
+        const double budget = (lo_ - a.x) - te;
+        const bool low = (a.y == 0.0) || (__fma_rn(t.x, budget, -a.y) > 0.0);
+        f = low ? t.x : clampf(a.y / budget, t.x, t.y);
+        arr = a.y / f + a.x;
         if (arr < t_free) arr = t_free;
     }
 #pragma unroll
