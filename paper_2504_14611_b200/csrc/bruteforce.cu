@@ -66,6 +66,11 @@ __global__ void k_bf_setup(const DevModel *models, DevBatch b, int space, BfHead
         if (big) hdr->status = JDOB_ST_TOOBIG;
     }
     const double vN = md.v[N], uN = md.u[N];
+    // all 32 entries are written (zeros beyond M) so the main kernel's tile copy reads initialised memory
+    user[0 * 32 + lane] = 0.0;
+    user[1 * 32 + lane] = 0.0;
+    user[2 * 32 + lane] = 0.0;
+    user[3 * 32 + lane] = 0.0;
     if (lane < M) {
         const double floc = clampf((x.z * vN) / x.T, x.f0, x.f1);
         user[0 * 32 + lane] = ((x.k * uN) * floc) * floc;

@@ -1,0 +1,28 @@
+"""Small end-to-end run of every kernel for compute-sanitizer (memcheck / racecheck / synccheck / initcheck)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import jdobgen as G  # noqa: E402
+import paper_2504_14611_b200 as J  # noqa: E402
+
+b = G.random_batch(seed=5, n_inst=64, M_lo=1, M_hi=32, N_lo=1, N_hi=12, k_max=70, tfree_frac=0.4)
+db = J.DeviceBatch(b)
+res = J.solve_batch(db, counts=True, stats=True, n_buckets=32)
+J.eval_plans(db, plans=res)
+J.eval_plans(db, J.plan_partition(db, res), res["f_e"])
+J.solve_grouped(J.DeviceBatch(b.subset(0, 16)))
+c = G.config_batch("c3", n_inst=64)
+J.solve_batch(J.DeviceBatch(c), stats=True, n_buckets=3)
+t = G.toy_instance("toy-4")
+dt = J.DeviceBatch(t)
+J.bruteforce(dt, 0)
+J.bruteforce(dt, 1)
+small = G.random_batch(seed=9, n_inst=1, M_lo=9, M_hi=9, N_lo=1, N_hi=1, k_max=3)
+J.bruteforce(J.DeviceBatch(small), 0)
+hb = J.HostBuffers(c, stats=True, n_buckets=3)
+J.solve_batch_host(hb)
+torch.cuda.synchronize()
+print("sanitize run ok")
