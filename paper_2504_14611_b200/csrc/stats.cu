@@ -100,13 +100,18 @@ __global__ void __launch_bounds__(kStatsWarps * 32) k_stats_partial(DevBatch b, 
     }
 }
 
+// one warp per output element: lane l folds partials l, l+32, ... in order, then a fixed
+// xor-butterfly combines the lanes -- a fixed tree, so the result is run-to-run identical
 __global__ void k_stats_final(const double *partials, int n_blocks, int n_buckets, double *stats) {
-    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n_buckets * kStatsF; x += gridDim.x * blockDim.x) {
-        const int f = x % kStatsF;
-        double v = partials[x];
-        for (int blk = 1; blk < n_blocks; blk++) v = combine(f, v, partials[(size_t)blk * n_buckets * kStatsF + x]);
-        stats[x] = v;
-    }
+    const int lane = threadIdx.x & 31;
+    const int x = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (x >= n_buckets * kStatsF) return;
+    const int f = x % kStatsF;
+    double v = field_init(f);
+    for (int blk = lane; blk < n_blocks; blk += 32) v = combine(f, v, partials[(size_t)blk * n_buckets * kStatsF + x]);
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) v = combine(f, v, __shfl_xor_sync(0xffffffffu, v, d));
+    if (lane == 0) stats[x] = v;
 }
 
 void launch_stats(const DevBatch &b, const DevResult &r, double *partials, double *stats, int n_buckets,
@@ -115,7 +120,8 @@ void launch_stats(const DevBatch &b, const DevResult &r, double *partials, doubl
     cudaFuncSetAttribute(k_stats_partial, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kStatsWarps * JDOB_MAX_BUCKETS * kStatsF * (int)sizeof(double));
     k_stats_partial<<<kStatsBlocks, kStatsWarps * 32, smem, s>>>(b, r, partials, n_buckets);
-    k_stats_final<<<(n_buckets * kStatsF + 255) / 256, 256, 0, s>>>(partials, kStatsBlocks, n_buckets, stats);
+    const int warps = n_buckets * kStatsF;
+    k_stats_final<<<(warps * 32 + 255) / 256, 256, 0, s>>>(partials, kStatsBlocks, n_buckets, stats);
 }
 
 }  // namespace jdob
