@@ -216,22 +216,31 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
     for (int nt = 0; nt < N; nt++) {
         if (mode == JDOB_MODE_BINARY && nt != 0) break;
         const int ihat = setup_nt(md, nt, M, homog, uni, t_free, s, lane);
-        for (long long j0 = 0; j0 < kk; j0 += 32) {
-            const long long j = j0 + lane;
-            const bool valid = j < kk;
-            const double fe = grid_fe(fe_max, rho, j);
+        // two grid points per lane (j0 + lane and j0 + 32 + lane): the two energy chains are
+        // independent, which doubles the instruction-level parallelism of the sweep and lets both
+        // share each user's shared-memory loads
+        for (long long j0 = 0; j0 < kk; j0 += 64) {
+            const long long jA = j0 + lane, jB = jA + 32;
+            const bool vA = jA < kk, vB = jB < kk;
+            const double feA = grid_fe(fe_max, rho, jA), feB = grid_fe(fe_max, rho, jB);
             // p(j): first sorted position >= i^ with !(f_e < th_i)  (M if the set is empty)
-            int lo = ihat, hi = M;
-            while (lo < hi) {
-                const int mm = (lo + hi) >> 1;
-                if (fe < s.th[mm]) lo = mm + 1;
-                else hi = mm;
+            int loA = ihat, hiA = M, loB = ihat, hiB = M;
+            while (loA < hiA) {
+                const int mm = (loA + hiA) >> 1;
+                if (feA < s.th[mm]) loA = mm + 1;
+                else hiA = mm;
             }
-            const int p = lo;
-            const long long feb = __double_as_longlong(fe);
+            while (loB < hiB) {
+                const int mm = (loB + hiB) >> 1;
+                if (feB < s.th[mm]) loB = mm + 1;
+                else hiB = mm;
+            }
+            const int pA = loA, pB = loB;
             // Alg. 2's break: the first j with an empty set ends this n~'s sweep
-            const unsigned emp = __ballot_sync(0xffffffffu, valid && p == M);
-            const long long jb = emp ? j0 + (__ffs(emp) - 1) : kk;
+            const unsigned empA = __ballot_sync(0xffffffffu, vA && pA == M);
+            const unsigned empB = __ballot_sync(0xffffffffu, vB && pB == M);
+            const long long jb = empA ? j0 + (__ffs(empA) - 1) : (empB ? j0 + 32 + (__ffs(empB) - 1) : kk);
+            const bool emp = (empA | empB) != 0u;
             if (emp && aN == N) {
                 aN = nt;
                 aJ = (int)jb;
@@ -240,65 +249,84 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
                 c_visit += 1;
                 c_eval += 1;
             }
-            if (valid && j < jb) {
-                const double inv = (j < kInvCache) ? s.inv[j] : 1.0 / fe;
-                const int Bo = M - p;
-                const double2 lg = s.Lg[p];  // l_o, phi / (l_o - t_free)
-                const double2 pq = s.pp[p];  // phi_n~(B_o), psi_n~(B_o)
-                const double lo_ = lg.x, phib = pq.x;
-                if (COUNTS) c_visit += 1;
-                // D6 guard: f_e >= phi / (l_o - t_free); the quotient depends only on p
-                if (fe >= lg.y) {
-                    if (COUNTS) {
-                        c_eval += 1;
-                        c_member += Bo;
-                    }
-                    const double te = phib * inv;
-                    double E = 0.0;
-                    if (uni) {
-                        // Uniform users (same R, zeta, f_min, f_max, kappa, p_u; Table I): every member
-                        // has the same budget, f* and offloader term, so D20/D21 are formed once and
-                        // only the user-order sum runs over M.  Same operations, same bits.
-                        const double2 a0 = s.orzv[0], c0 = s.kuup[0], t0 = s.fmm[0];
-                        const double budget = (lo_ - a0.x) - te;
-                        double f = t0.x;
-                        if (!(__fma_rn(t0.x, budget, -a0.y) > 0.0) && a0.y != 0.0)
-                            f = clampf(a0.y / budget, t0.x, t0.y);  // D20 (R9 when zv = 0)
-                        const double em = ((c0.x * f) * f) + c0.y;  // D21 offloader term
+            const bool actA = vA && jA < jb, actB = vB && jB < jb;
+            const int qA = actA ? pA : 0, qB = actB ? pB : 0;  // p < M for active grid points
+            const double2 lgA = s.Lg[qA], lgB = s.Lg[qB];     // l_o, phi / (l_o - t_free)
+            const double2 pqA = s.pp[qA], pqB = s.pp[qB];     // phi_n~(B_o), psi_n~(B_o)
+            // D6 guard: f_e >= phi / (l_o - t_free); the quotient depends only on p
+            const bool passA = actA && feA >= lgA.y, passB = actB && feB >= lgB.y;
+            if (COUNTS) {
+                c_visit += (actA ? 1 : 0) + (actB ? 1 : 0);
+                c_eval += (passA ? 1 : 0) + (passB ? 1 : 0);
+                c_member += (passA ? M - pA : 0) + (passB ? M - pB : 0);
+            }
+            if (!(passA || passB)) {
+                if (emp) break;
+                continue;
+            }
+            const double invA = (jA < kInvCache) ? s.inv[jA] : 1.0 / feA;
+            const double invB = (jB < kInvCache) ? s.inv[jB] : 1.0 / feB;
+            const double teA = pqA.x * invA, teB = pqB.x * invB;
+            double EA = 0.0, EB = 0.0;
+            if (uni) {
+                // Uniform users (same R, zeta, f_min, f_max, kappa, p_u; Table I): every member
+                // has the same budget, f* and offloader term, so D20/D21 are formed once and
+                // only the user-order sum runs over M.  Same operations, same bits.
+                const double2 a0 = s.orzv[0], c0 = s.kuup[0], t0 = s.fmm[0];
+                const double budA = (lgA.x - a0.x) - teA, budB = (lgB.x - a0.x) - teB;
+                double fA = t0.x, fB = t0.x;
+                if (passA && !(__fma_rn(t0.x, budA, -a0.y) > 0.0) && a0.y != 0.0)
+                    fA = clampf(a0.y / budA, t0.x, t0.y);  // D20 (R9 when zv = 0)
+                if (passB && !(__fma_rn(t0.x, budB, -a0.y) > 0.0) && a0.y != 0.0)
+                    fB = clampf(a0.y / budB, t0.x, t0.y);
+                const double emA = ((c0.x * fA) * fA) + c0.y;  // D21 offloader term
+                const double emB = ((c0.x * fB) * fB) + c0.y;
 #pragma unroll 4
-                        for (int m = 0; m < M; m++) {
-                            const double2 et = s.et[m];     // eloc, thu
-                            const bool mem = !(fe < et.y);  // FP64-pipe compare: the ALU pipe is the busier one here
-                            E = E + (mem ? em : et.x);
-                        }
-                    } else {
-#pragma unroll 4
-                        for (int m = 0; m < M; m++) {
-                            const double2 a = s.orzv[m];  // OR, zv
-                            const double2 c = s.kuup[m];  // ku, up
-                            const double2 d = s.et[m];    // eloc, thu
-                            const double2 t = s.fmm[m];   // fmin, fmax
-                            // f_e, th >= 0 (or +inf): IEEE order = integer order of the bit patterns
-                            const bool mem = feb >= __double_as_longlong(d.y);
-                            const double budget = (lo_ - a.x) - te;
-                            const bool low = __fma_rn(t.x, budget, -a.y) > 0.0;  // f_min budget > zv exactly
-                            double f = t.x;                                       // f_min
-                            if (mem && !low) {
-                                // R9 (zv = 0 -> f_min) tested on the bits, inside the rare branch
-                                if ((__double_as_longlong(a.y) << 1) != 0) f = clampf(a.y / budget, t.x, t.y);
-                            }
-                            const double em = ((c.x * f) * f) + c.y;  // D21 offloader term
-                            E = E + (mem ? em : d.x);
-                        }
-                    }
-                    E = E + (pq.y * fe) * fe;
-                    if (E < bE) {  // strict: lane keys ascend in (n~, j)
-                        bE = E;
-                        bN = nt;
-                        bJ = (int)j;
-                        bP = p;
-                    }
+                for (int m = 0; m < M; m++) {
+                    const double2 et = s.et[m];  // eloc, thu
+                    EA = EA + ((!(feA < et.y)) ? emA : et.x);
+                    EB = EB + ((!(feB < et.y)) ? emB : et.x);
                 }
+            } else {
+                const long long fbA = __double_as_longlong(feA), fbB = __double_as_longlong(feB);
+#pragma unroll 2
+                for (int m = 0; m < M; m++) {
+                    const double2 a = s.orzv[m];  // OR, zv
+                    const double2 c = s.kuup[m];  // ku, up
+                    const double2 d = s.et[m];    // eloc, thu
+                    const double2 t = s.fmm[m];   // fmin, fmax
+                    // f_e, th >= 0 (or +inf): IEEE order = integer order of the bit patterns
+                    const long long thb = __double_as_longlong(d.y);
+                    const bool memA = fbA >= thb, memB = fbB >= thb;
+                    const double budA = (lgA.x - a.x) - teA, budB = (lgB.x - a.x) - teB;
+                    double fA = t.x, fB = t.x;  // f_min unless f_min budget > zv fails exactly
+                    const bool needA = passA && memA && !(__fma_rn(t.x, budA, -a.y) > 0.0);
+                    const bool needB = passB && memB && !(__fma_rn(t.x, budB, -a.y) > 0.0);
+                    if (needA || needB) {
+                        // R9 (zv = 0 -> f_min) tested on the bits, inside the rare branch
+                        const bool nz = (__double_as_longlong(a.y) << 1) != 0;
+                        if (needA && nz) fA = clampf(a.y / budA, t.x, t.y);  // D20
+                        if (needB && nz) fB = clampf(a.y / budB, t.x, t.y);
+                    }
+                    const double emA = ((c.x * fA) * fA) + c.y;  // D21 offloader term
+                    const double emB = ((c.x * fB) * fB) + c.y;
+                    EA = EA + (memA ? emA : d.x);
+                    EB = EB + (memB ? emB : d.x);
+                }
+            }
+            EA = EA + (pqA.y * feA) * feA;
+            EB = EB + (pqB.y * feB) * feB;
+            if (passA && EA < bE) {  // strict: lane keys ascend in (n~, j)
+                bE = EA;
+                bN = nt;
+                bJ = (int)jA;
+                bP = pA;
+            }
+            if (passB && EB < bE) {
+                bE = EB;
+                bN = nt;
+                bJ = (int)jB;
+                bP = pB;
             }
             if (emp) break;
         }
@@ -374,7 +402,7 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
 }
 
 #ifndef JDOB_SOLVE_MINB
-#define JDOB_SOLVE_MINB 7
+#define JDOB_SOLVE_MINB 5
 #endif
 
 template <bool COUNTS>
