@@ -204,65 +204,118 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                 }
                 const unsigned long long jlo = (vec == vb) ? idx_begin - vb * uk : 0ull;
                 const unsigned long long jhi = (vec == ve - 1) ? idx_end - (ve - 1) * uk : uk;
-                for (unsigned long long j = jlo; j < jhi; j++) {
-                    const double fe = grid_fe(fe_max, rho, (long long)j);
-                    const double inv = (j < (unsigned long long)kt) ? sInv[j] : 1.0 / fe;
-                    if (any && !(t_free + Smin * inv <= l_o)) break;  // D6' (monotone in j)
-                    double E = 0.0;
-                    bool feas = true;
+                if constexpr (REG) {
+                    // M <= 8: (A) budgets and the exact low-clamp test for every offloader, no
+                    // branches; (B) the rare literal divisions / feasibility checks; (C) the energies
+                    // in user order.  Keeping the branch out of the straight-line code lets the
+                    // users' dependency chains overlap.
+                    for (unsigned long long j = jlo; j < jhi; j++) {
+                        const double fe = grid_fe(fe_max, rho, (long long)j);
+                        const double inv = (j < (unsigned long long)kt) ? sInv[j] : 1.0 / fe;
+                        if (any && !(t_free + Smin * inv <= l_o)) break;  // D6' (monotone in j)
+                        double bud[MAXM], fv[MAXM];
+                        unsigned need = 0u;
 #pragma unroll
-                    for (int m = 0; m < MAXM; m++) {
-                        if (m >= M) break;
-                        double e;
-                        if ((offm >> m) & 1u) {
-                            double lom, zv, ku, up;
-                            if constexpr (REG) {
-                                lom = lo[m];
-                                zv = zvr[m];
-                                ku = kur[m];
-                                up = upr[m];
-                            } else {
-                                const int x = nv[m] * M + m;
-                                lom = l_o - sOR[x];
-                                zv = sZV[x];
-                                ku = sKU[x];
-                                up = sUP[x];
-                            }
-                            const double budget = lom - Sm[m] * inv;  // (l_o - O/R) - S_{n_m+1}/f_e
-                            double f = sFmin[m];
+                        for (int m = 0; m < MAXM; m++) {
+                            bud[m] = lo[m] - Sm[m] * inv;  // (l_o - O/R) - S_{n_m+1}/f_e
+                            fv[m] = sFmin[m];
                             // exact low clamp: fmin*budget > zv exactly => budget > 0 and
                             // RN(zv/budget) <= f_min <= f_max: feasible with f* = f_min (R9 when zv = 0)
-                            if (!(__fma_rn(f, budget, -zv) > 0.0)) {
-                                if (zv == 0.0) {
-                                    if (!(budget >= 0.0)) {
+                            if (((offm >> m) & 1u) && !(__fma_rn(fv[m], bud[m], -zvr[m]) > 0.0)) need |= 1u << m;
+                        }
+                        bool feas = true;
+                        if (need) {
+#pragma unroll
+                            for (int m = 0; m < MAXM; m++) {
+                                if ((need >> m) & 1u) {
+                                    if (zvr[m] == 0.0) {
+                                        if (!(bud[m] >= 0.0)) feas = false;
+                                    } else if (!(bud[m] > 0.0)) {
                                         feas = false;
-                                        break;
+                                    } else {
+                                        const double G = zvr[m] / bud[m];
+                                        if (G > sFmax[m]) feas = false;  // D7' with D13 (exact, R10)
+                                        fv[m] = (G < fv[m]) ? fv[m] : G;
                                     }
-                                } else {
-                                    if (!(budget > 0.0)) {
-                                        feas = false;
-                                        break;
-                                    }
-                                    const double G = zv / budget;
-                                    if (G > sFmax[m]) {  // D7' with D13 (exact, R10)
-                                        feas = false;
-                                        break;
-                                    }
-                                    f = (G < f) ? f : G;
                                 }
                             }
-                            e = ((ku * f) * f) + up;
-                        } else {
-                            e = sEl[m];
                         }
-                        E = E + e;
+                        if (!feas) break;  // D7' (monotone in j)
+                        double E = 0.0;
+#pragma unroll
+                        for (int m = 0; m < MAXM; m++) {
+                            if (m < M) {
+                                const double em = ((kur[m] * fv[m]) * fv[m]) + upr[m];
+                                E = E + (((offm >> m) & 1u) ? em : sEl[m]);
+                            }
+                        }
+                        E = E + (Psi * fe) * fe;
+                        if (E < bestE) {
+                            bestE = E;
+                            bestI = (long long)(vec * uk + j);
+                        }
                     }
-                    if (!feas) break;  // D7' (monotone in j)
-                    E = E + (Psi * fe) * fe;
-                    if (E < bestE) {
-                        bestE = E;
-                        bestI = (long long)(vec * uk + j);
-                    }
+                } else {
+                for (unsigned long long j = jlo; j < jhi; j++) {
+                        const double fe = grid_fe(fe_max, rho, (long long)j);
+                        const double inv = (j < (unsigned long long)kt) ? sInv[j] : 1.0 / fe;
+                        if (any && !(t_free + Smin * inv <= l_o)) break;  // D6' (monotone in j)
+                        double E = 0.0;
+                        bool feas = true;
+    #pragma unroll
+                        for (int m = 0; m < MAXM; m++) {
+                            if (m >= M) break;
+                            double e;
+                            if ((offm >> m) & 1u) {
+                                double lom, zv, ku, up;
+                                if constexpr (REG) {
+                                    lom = lo[m];
+                                    zv = zvr[m];
+                                    ku = kur[m];
+                                    up = upr[m];
+                                } else {
+                                    const int x = nv[m] * M + m;
+                                    lom = l_o - sOR[x];
+                                    zv = sZV[x];
+                                    ku = sKU[x];
+                                    up = sUP[x];
+                                }
+                                const double budget = lom - Sm[m] * inv;  // (l_o - O/R) - S_{n_m+1}/f_e
+                                double f = sFmin[m];
+                                // exact low clamp: fmin*budget > zv exactly => budget > 0 and
+                                // RN(zv/budget) <= f_min <= f_max: feasible with f* = f_min (R9 when zv = 0)
+                                if (!(__fma_rn(f, budget, -zv) > 0.0)) {
+                                    if (zv == 0.0) {
+                                        if (!(budget >= 0.0)) {
+                                            feas = false;
+                                            break;
+                                        }
+                                    } else {
+                                        if (!(budget > 0.0)) {
+                                            feas = false;
+                                            break;
+                                        }
+                                        const double G = zv / budget;
+                                        if (G > sFmax[m]) {  // D7' with D13 (exact, R10)
+                                            feas = false;
+                                            break;
+                                        }
+                                        f = (G < f) ? f : G;
+                                    }
+                                }
+                                e = ((ku * f) * f) + up;
+                            } else {
+                                e = sEl[m];
+                            }
+                            E = E + e;
+                        }
+                        if (!feas) break;  // D7' (monotone in j)
+                        E = E + (Psi * fe) * fe;
+                        if (E < bestE) {
+                            bestE = E;
+                            bestI = (long long)(vec * uk + j);
+                        }
+                }
                 }
             }
         }
