@@ -63,8 +63,8 @@ def _model(name, A_mmac, O_kelem, *, sigma=SIGMA, B_max=B_MAX, zeta=ZETA, kappa=
     return Model(name, N, B_max, A, O, g, q, d, c)
 
 
-def mobilenetv2():
-    return _model("mobilenetv2", MOBILENETV2_A, MOBILENETV2_O)
+def mobilenetv2(B_max=B_MAX):
+    return _model("mobilenetv2", MOBILENETV2_A, MOBILENETV2_O, B_max=B_max)
 
 
 def vgg16():

@@ -21,6 +21,7 @@ CFLAGS = ["-O2", "-std=gnu11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "
 ST_OK, ST_LOCAL_INFEASIBLE, ST_REQUIRE, ST_BADPARAM, ST_BADMODEL, ST_TOOBIG = range(6)
 STATS_FIELDS = 80
 MODE_FULL, MODE_LC, MODE_NO_EDGE_DVFS, MODE_BINARY = range(4)
+MAXM_LARGE = 1024
 
 _lock = threading.Lock()
 _lib = None
@@ -51,7 +52,7 @@ class OInst(C.Structure):
 class OResult(C.Structure):
     _fields_ = [("E", C.c_double), ("E_lc", C.c_double), ("t_free_next", C.c_double), ("f_e", C.c_double),
                 ("n_tilde", C.c_int), ("j", C.c_int), ("status", C.c_int), ("mask", C.c_uint),
-                ("f_user", C.c_double * 32),
+                ("f_user", C.c_double * MAXM_LARGE), ("part", C.c_int * MAXM_LARGE),
                 ("n_visit", C.c_longlong), ("n_eval", C.c_longlong), ("n_member", C.c_longlong)]
 
 
@@ -71,7 +72,7 @@ class OBatch(C.Structure):
 class OOut(C.Structure):
     _fields_ = [(f, C.POINTER(C.c_double)) for f in ("E", "E_lc", "t_free_next", "f_e", "f_user")] + \
                [(f, C.POINTER(C.c_int)) for f in ("n_tilde", "j", "status")] + \
-               [("mask", C.POINTER(C.c_uint)), ("counts", C.POINTER(C.c_longlong))]
+               [("mask", C.POINTER(C.c_uint)), ("counts", C.POINTER(C.c_longlong)), ("part", C.POINTER(C.c_int))]
 
 
 def lib():
@@ -206,7 +207,7 @@ def jdob(batch, i=0, mode=MODE_FULL) -> dict:
                       mode, C.byref(r))
     M = batch.M(i)
     return dict(E=r.E, E_lc=r.E_lc, t_free_next=r.t_free_next, f_e=r.f_e, n_tilde=r.n_tilde, j=r.j,
-                status=r.status, mask=r.mask, f_user=np.array(r.f_user[:M]),
+                status=r.status, mask=r.mask, f_user=np.array(r.f_user[:M]), part=np.array(r.part[:M]),
                 n_visit=r.n_visit, n_eval=r.n_eval, n_member=r.n_member)
 
 
@@ -215,7 +216,7 @@ def solve_batch(batch, mode=MODE_FULL, threads=1, counts=False) -> dict:
     n = batch.n_inst
     out = dict(E=np.zeros(n), E_lc=np.zeros(n), t_free_next=np.zeros(n), f_e=np.zeros(n),
                f_user=np.zeros(batch.n_users), n_tilde=np.zeros(n, np.int32), j=np.zeros(n, np.int32),
-               status=np.zeros(n, np.int32), mask=np.zeros(n, np.uint32))
+               status=np.zeros(n, np.int32), mask=np.zeros(n, np.uint32), part=np.zeros(batch.n_users, np.int32))
     if counts:
         out["counts"] = np.zeros((n, 3), np.int64)
     o = OOut()
@@ -225,6 +226,7 @@ def solve_batch(batch, mode=MODE_FULL, threads=1, counts=False) -> dict:
         setattr(o, f, _ip(out[f]))
     o.mask = out["mask"].ctypes.data_as(C.POINTER(C.c_uint))
     o.counts = out["counts"].ctypes.data_as(C.POINTER(C.c_longlong)) if counts else None
+    o.part = _ip(out["part"])
     b = _obatch(batch, keep)
     lib().oracle_solve_batch(C.byref(b), n, mode, C.byref(o), int(threads))
     return out

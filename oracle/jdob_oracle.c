@@ -35,7 +35,8 @@
 #define O_ST_BADMODEL 4
 #define O_ST_TOOBIG 5
 
-#define O_MAXM 32
+#define O_MAXM 32          /* brute force, grouping, offload mask */
+#define O_MAXM_LARGE 1024  /* J-DOB, LC, eval (NEXT-4: M > 32) */
 #define O_MAXN 63
 #define O_MAXK 65536
 
@@ -55,7 +56,8 @@ typedef struct {
     double E, E_lc, t_free_next, f_e;
     int n_tilde, j, status;
     unsigned mask;
-    double f_user[O_MAXM];
+    double f_user[O_MAXM_LARGE];
+    int part[O_MAXM_LARGE]; /* per user: partition point n~* if offloading, else N */
     /* algorithmic work counters: the literal Alg. 1/2 loop counts */
     long long n_visit;   /* (n~, j) pairs visited by the sweep (guard evaluated)            */
     long long n_eval;    /* (n~, j) pairs that passed the guard and were evaluated (D20-D22) */
@@ -123,7 +125,7 @@ static int o_finite(double x) { return isfinite(x); }
 /* Model validation: A_0 = 0, A_n > 0 (n >= 1), O, g, q >= 0,
  * d_n(b) > 0 and non-decreasing in b, c_n(b) >= 0 (Fig. 3 trend). */
 int oracle_check_model(const o_model *m) {
-    if (m->N < 1 || m->N > O_MAXN || m->B_max < 1 || m->B_max > O_MAXM) return O_ST_BADMODEL;
+    if (m->N < 1 || m->N > O_MAXN || m->B_max < 1 || m->B_max > O_MAXM_LARGE) return O_ST_BADMODEL;
     if (!(m->A[0] == 0.0)) return O_ST_BADMODEL;
     for (int n = 0; n <= m->N; n++) {
         if (!o_finite(m->A[n]) || !o_finite(m->O[n]) || !o_finite(m->g[n]) || !o_finite(m->q[n]))
@@ -145,7 +147,7 @@ int oracle_check_model(const o_model *m) {
  * Require of Alg. 1. */
 int oracle_check_inst(const o_model *m, const o_inst *in) {
     if (oracle_check_model(m) != O_ST_OK) return O_ST_BADMODEL;
-    if (in->M < 1 || in->M > O_MAXM || in->M > m->B_max) return O_ST_BADPARAM;
+    if (in->M < 1 || in->M > O_MAXM_LARGE || in->M > m->B_max) return O_ST_BADPARAM;
     for (int i = 0; i < in->M; i++) {
         double z = in->zeta[i], k = in->kappa[i], f0 = in->f_min[i], f1 = in->f_max[i];
         double R = in->R[i], p = in->p_u[i], T = in->T[i];
@@ -282,12 +284,13 @@ int oracle_jdob(const o_model *m, const o_inst *in, int mode, o_result *r) {
     int st = oracle_check_inst(m, in);
     r->status = st;
     int M = in->M;
-    double f_loc[O_MAXM], e_loc[O_MAXM];
+    double f_loc[O_MAXM_LARGE], e_loc[O_MAXM_LARGE];
     if (st == O_ST_BADPARAM || st == O_ST_BADMODEL) {
         r->E = r->E_lc = NAN;
         r->t_free_next = in->t_free;
         r->n_tilde = (m->N >= 1 && m->N <= O_MAXN) ? m->N : 0;
-        for (int i = 0; i < O_MAXM; i++) r->f_user[i] = NAN;
+        for (int i = 0; i < O_MAXM_LARGE; i++) r->f_user[i] = NAN;
+        for (int i = 0; i < O_MAXM_LARGE; i++) r->part[i] = r->n_tilde;
         return st;
     }
     double E_lc = oracle_lc(m, in, f_loc, e_loc);
@@ -299,14 +302,19 @@ int oracle_jdob(const o_model *m, const o_inst *in, int mode, o_result *r) {
     r->n_tilde = m->N;
     r->j = 0;
     r->mask = 0u;
-    for (int i = 0; i < M; i++) r->f_user[i] = f_loc[i];
+    for (int i = 0; i < M; i++) {
+        r->f_user[i] = f_loc[i];
+        r->part[i] = m->N;
+    }
     if (st != O_ST_OK || mode == 1) return st;
 
     long long k_full = o_grid_k(in);
     double E_star = O_INF;
     int best_nt = -1, best_j = 0;
     unsigned best_mask = 0u;
-    double best_fe = 0.0, best_tf = in->t_free, best_f[O_MAXM];
+    double best_fe = 0.0, best_tf = in->t_free, best_f[O_MAXM_LARGE];
+    static _Thread_local int best_mem[O_MAXM_LARGE], nt_mem[O_MAXM_LARGE];
+    int best_any = 0;
 
     for (int nt = 0; nt <= m->N; nt++) { /* Alg. 1 line 3: traverse partition points */
         if (mode == 3 && nt != 0 && nt != m->N) continue;
@@ -317,28 +325,30 @@ int oracle_jdob(const o_model *m, const o_inst *in, int mode, o_result *r) {
                 best_nt = nt;
                 best_j = 0;
                 best_mask = 0u;
+                best_any = 0;
                 best_fe = 0.0;
                 best_tf = in->t_free;
                 for (int i = 0; i < M; i++) best_f[i] = f_loc[i];
             }
             continue;
         }
-        double gamma[O_MAXM], th[O_MAXM];
-        int list[O_MAXM];
+        double gamma[O_MAXM_LARGE], th[O_MAXM_LARGE];
+        int list[O_MAXM_LARGE];
         oracle_thresholds(m, in, nt, gamma, list, th);
 
         /* ---- Alg. 2 ---- */
         double E_nt = O_INF;
         int have = 0, nt_j = 0;
         unsigned nt_mask = 0u;
-        double nt_fe = 0.0, nt_tf = in->t_free, nt_f[O_MAXM];
+        double nt_fe = 0.0, nt_tf = in->t_free, nt_f[O_MAXM_LARGE];
+        int nt_any = 0;
         int ihat = -1; /* -1 encodes "NAN" (R3) */
         for (int i = 0; i < M; i++)
             if (th[i] >= 0.0) {
                 ihat = i;
                 break;
             }
-        int member[O_MAXM];
+        int member[O_MAXM_LARGE];
         for (int i = 0; i < M; i++) member[i] = 0;
         if (ihat >= 0)
             for (int i = ihat; i < M; i++) member[list[i]] = 1;
@@ -369,7 +379,7 @@ int oracle_jdob(const o_model *m, const o_inst *in, int mode, o_result *r) {
             r->n_visit++;
             /* optimal device DVFS under the GPU-occupation guard */
             if (fe >= o_phi(m, nt, B_o) / (l_o - in->t_free)) {
-                double fstar[O_MAXM], tf;
+                double fstar[O_MAXM_LARGE], tf;
                 double E = o_eval_p1(m, in, nt, member, B_o, l_o, fe, f_loc, e_loc, fstar, &tf);
                 r->n_eval++;
                 r->n_member += B_o;
@@ -380,8 +390,11 @@ int oracle_jdob(const o_model *m, const o_inst *in, int mode, o_result *r) {
                     nt_fe = fe;
                     nt_tf = tf;
                     nt_mask = 0u;
+                    nt_any = 0;
                     for (int i = 0; i < M; i++) {
-                        if (member[i]) nt_mask |= (1u << i);
+                        if (member[i] && i < 32) nt_mask |= (1u << i);
+                        nt_mem[i] = member[i];
+                        nt_any |= member[i];
                         nt_f[i] = fstar[i];
                     }
                 }
@@ -395,19 +408,26 @@ int oracle_jdob(const o_model *m, const o_inst *in, int mode, o_result *r) {
             best_nt = nt;
             best_j = nt_j;
             best_mask = nt_mask;
+            best_any = nt_any;
             best_fe = nt_fe;
             best_tf = nt_tf;
-            for (int i = 0; i < M; i++) best_f[i] = nt_f[i];
+            for (int i = 0; i < M; i++) {
+                best_f[i] = nt_f[i];
+                best_mem[i] = nt_mem[i];
+            }
         }
     }
-    if (best_nt >= 0 && best_mask != 0u) {
+    if (best_nt >= 0 && best_any) {
         r->E = E_star;
         r->n_tilde = best_nt;
         r->j = best_j;
-        r->mask = best_mask;
+        r->mask = best_mask; /* users 0..31 only (M <= 32 instances) */
         r->f_e = best_fe;
         r->t_free_next = best_tf;
-        for (int i = 0; i < M; i++) r->f_user[i] = best_f[i];
+        for (int i = 0; i < M; i++) {
+            r->f_user[i] = best_f[i];
+            r->part[i] = best_mem[i] ? best_nt : m->N;
+        }
     }
     /* otherwise the winner is an all-local evaluation: keep the canonical answer (R8). */
     return st;
@@ -423,6 +443,7 @@ int oracle_jdob(const o_model *m, const o_inst *in, int mode, o_result *r) {
 /* batch starts s_n = l_o - S_n / f_e (R14), exact feasibility (R10).     */
 /* ------------------------------------------------------------------ */
 static int o_space_size(const o_model *m, const o_inst *in, int space, unsigned long long *size) {
+    if (in->M > O_MAXM) return O_ST_TOOBIG;
     long long k = o_grid_k(in);
     if (k <= 0) return O_ST_BADPARAM;
     unsigned long long lim = (1ull << 62);
@@ -579,7 +600,7 @@ int oracle_eval(const o_model *m, const o_inst *in, const int *nvec, double fe, 
         return st;
     }
     int M = in->M, N = m->N;
-    double f_loc[O_MAXM], e_loc[O_MAXM];
+    double f_loc[O_MAXM_LARGE], e_loc[O_MAXM_LARGE];
     oracle_lc(m, in, f_loc, e_loc);
     unsigned viol = 0u;
     double vN = o_v(m, N);
@@ -687,6 +708,7 @@ typedef struct {
     int *n_tilde, *j, *status;
     unsigned *mask;
     long long *counts; /* [n_inst*3] n_visit, n_eval, n_member, or NULL */
+    int *part;         /* [users] partition point per user, or NULL */
 } o_out;
 
 typedef struct {
@@ -705,7 +727,7 @@ static void *o_solve_range(void *arg) {
         o_make_inst(b, i, &in);
         o_result r;
         const o_model *m = &b->models[b->model_id[i]];
-        if (in.M < 1 || in.M > O_MAXM) {
+        if (in.M < 1 || in.M > O_MAXM_LARGE) {
             memset(&r, 0, sizeof(r));
             r.status = O_ST_BADPARAM;
             r.E = r.E_lc = NAN;
@@ -722,8 +744,10 @@ static void *o_solve_range(void *arg) {
         out->j[i] = r.j;
         out->status[i] = r.status;
         out->mask[i] = r.mask;
-        if (out->f_user && in.M >= 1 && in.M <= O_MAXM)
+        if (out->f_user && in.M >= 1 && in.M <= O_MAXM_LARGE)
             for (int u = 0; u < in.M; u++) out->f_user[b->user_off[i] + u] = r.f_user[u];
+        if (out->part && in.M >= 1 && in.M <= O_MAXM_LARGE)
+            for (int u = 0; u < in.M; u++) out->part[b->user_off[i] + u] = r.part[u];
         if (out->counts) {
             out->counts[3 * i + 0] = r.n_visit;
             out->counts[3 * i + 1] = r.n_eval;
@@ -807,14 +831,14 @@ int oracle_eval_batch(const o_batch *b, long long n_inst, const int *partition, 
         o_inst in;
         o_make_inst(b, i, &in);
         const o_model *m = &b->models[b->model_id[i]];
-        if (in.M < 1 || in.M > O_MAXM) {
+        if (in.M < 1 || in.M > O_MAXM_LARGE) {
             E[i] = NAN;
             tf[i] = NAN;
             viol[i] = 0u;
             status[i] = O_ST_BADPARAM;
             continue;
         }
-        double fs[O_MAXM];
+        double fs[O_MAXM_LARGE];
         status[i] = oracle_eval(m, &in, partition + b->user_off[i], fe[i], slack, &E[i], &tf[i], fs, &viol[i]);
         if (f_user)
             for (int u = 0; u < in.M; u++) f_user[b->user_off[i] + u] = fs[u];
@@ -916,10 +940,11 @@ int oracle_og(const o_model *m, const o_inst *in, int mode, o_og_result *r) {
     memset(r, 0, sizeof(*r));
     int st = oracle_check_inst(m, in);
     if (st == O_ST_REQUIRE) st = O_ST_OK; /* the DP costs a failed Require per group */
+    if (in->M > O_MAXM && st == O_ST_OK) st = O_ST_BADPARAM; /* grouping: M <= 32 */
     r->status = st;
     int M = in->M;
     if (st != O_ST_OK) {
-        o_result lr;
+        static _Thread_local o_result lr;
         oracle_jdob(m, in, 1, &lr); /* LC answer (or NaN for malformed input) */
         r->E = lr.E;
         r->t_free_next = in->t_free;
