@@ -41,7 +41,8 @@ extern "C" {
 #define JDOB_API
 #endif
 
-#define JDOB_MAX_M 32          /* users per instance (M' of Alg. 1)                 */
+#define JDOB_MAX_M 32          /* users per instance on the warp path; offload mask width */
+#define JDOB_MAX_M_LARGE 1024  /* users per instance (M' of Alg. 1), block path above 32 */
 #define JDOB_MAX_N 63          /* sub-tasks per DNN (N)                        */
 #define JDOB_MAX_K 65536       /* edge-frequency grid points per instance (k) */
 #define JDOB_STATS_FIELDS 80   /* doubles per statistics bucket (a12)               */
@@ -80,7 +81,7 @@ enum {
  *                d_n(b), c_n(b) of Eq. (5); rows n = 0 and columns b = 0 unused.
  */
 typedef struct {
-    int32_t N, B_max; /* 1 <= N <= 63, 1 <= B_max <= 32 */
+    int32_t N, B_max; /* 1 <= N <= 63, 1 <= B_max <= 1024 */
     const double *A, *O, *g, *q;
     const double *d, *c;
 } jdob_model;
@@ -90,7 +91,10 @@ typedef struct {
  * arrays; DESIGN.md §Data layout).  All array members are DEVICE pointers.
  *   model_id [n_inst]      : index into the models[] array of the call.
  *   user_off [n_inst+1]    : users of instance i are user_off[i] .. user_off[i+1]-1;
- *                            M_i = user_off[i+1] - user_off[i] must be in [1, 32].
+ *                            M_i = user_off[i+1] - user_off[i] must be in [1, min(1024, B_max)].
+ *                            jdob_solve_batch solves M_i <= 32 one warp per instance and
+ *                            M_i > 32 one thread block per instance; the other
+ *                            entry points take M_i <= 32.
  *   zeta, kappa, f_min, f_max, R, p_u, T [user_off[n_inst]] : per-user zeta_m
  *                            (cycles/workload), kappa_m (switched capacitance),
  *                            f_m,min/max (Hz), R_m (bit/s), p_m^u (W), T_m^(d) (s)
@@ -120,7 +124,8 @@ typedef struct {
  *   n_tilde [n_inst]     : identical partition point n~*; N when all-local (R4, R8).
  *   j [n_inst]           : grid index of f_e (f_e = fe_max - j*rho); 0 when all-local.
  *   status [n_inst]      : JDOB_ST_*.
- *   mask [n_inst]        : offloading set M'_o, bit m = user m of the instance.
+ *   mask [n_inst]        : offloading set M'_o, bit m = user m of the instance (M_i <= 32;
+ *                          0 for M_i > 32 -- use `partition`).
  *   f_user [user_off[n_inst]] : optional (NULL = skip) device frequencies f_m* (D20).
  *   counts [3*n_inst]    : optional (NULL = skip) literal Alg. 2 work counters per
  *                          instance: (n~, j) pairs visited, pairs evaluated (guard
@@ -131,7 +136,8 @@ typedef struct {
  *                          [4] min r, [5] sum E/M, [6] sum E_lc/M, [7] #offloading,
  *                          [8] #status != OK, [9+n] #instances with n~* = n (n <= 63);
  *                          r = 100 (E_lc - E) / E_lc.  Deterministic for a given
- *                          n_inst (fixed reduction tree).
+ *                          n_inst (fixed reduction tree).  Default buckets (bucket == NULL)
+ *                          cover M_i <= n_buckets.
  */
 typedef struct {
     double *E, *E_lc, *t_free_next, *f_e;
@@ -140,7 +146,8 @@ typedef struct {
     double *f_user;
     int64_t *counts;
     double *stats;
-    int32_t n_buckets; /* 1 .. JDOB_MAX_BUCKETS when stats != NULL */
+    int32_t n_buckets;  /* 1 .. JDOB_MAX_BUCKETS when stats != NULL */
+    int32_t *partition; /* optional [user_off[n_inst]]: n~* for offloaders, N for local users */
 } jdob_result;
 
 /*

@@ -164,19 +164,25 @@ class Batch:
 
 
 def concat(batches: Sequence[Batch]) -> Batch:
-    """Concatenate batches that share one model list object."""
+    """Concatenate batches; model lists are shared when identical, else appended (model_id shifted)."""
     models = batches[0].models
+    shared = all(b.models is models for b in batches)
+    if not shared:
+        models = [m for b in batches for m in b.models]
     offs = [np.zeros(1, np.int64)]
+    mids = []
     base = 0
+    mbase = 0
     for b in batches:
-        assert b.models is models
         offs.append(b.user_off[1:] + base)
         base += b.n_users
+        mids.append(b.model_id + (0 if shared else mbase))
+        mbase += len(b.models)
     kw = {f: np.concatenate([getattr(b, f) for b in batches]) for f in Batch.USER_FIELDS + Batch.INST_FIELDS}
     bucket = None
     if all(b.bucket is not None for b in batches):
         bucket = np.concatenate([b.bucket for b in batches])
-    return Batch(models=models, model_id=np.concatenate([b.model_id for b in batches]),
+    return Batch(models=models, model_id=np.concatenate(mids).astype(np.int32),
                  user_off=np.concatenate(offs), bucket=bucket, **kw)
 
 

@@ -38,7 +38,8 @@ class JBatch(C.Structure):
 
 class JResult(C.Structure):
     _fields_ = [(f, C.c_void_p) for f in ("E", "E_lc", "t_free_next", "f_e", "n_tilde", "j", "status", "mask",
-                                          "f_user", "counts", "stats")] + [("n_buckets", C.c_int32)]
+                                          "f_user", "counts", "stats")] + [("n_buckets", C.c_int32),
+                                                                           ("partition", C.c_void_p)]
 
 
 class JGrouped(C.Structure):
@@ -168,7 +169,8 @@ class DeviceBatch:
 
 
 def solve_batch(db: DeviceBatch, mode: int = MODE_FULL, f_user: bool = True, counts: bool = False,
-                stats: bool = False, n_buckets: Optional[int] = None, stream=None, out: Optional[dict] = None) -> dict:
+                stats: bool = False, n_buckets: Optional[int] = None, stream=None, out: Optional[dict] = None,
+                partition: bool = False) -> dict:
     """jdob_solve_batch: J-DOB (Alg. 1/2) over every instance of `db`; outputs are device tensors."""
     torch = _torch()
     dev = db.device
@@ -189,9 +191,11 @@ def solve_batch(db: DeviceBatch, mode: int = MODE_FULL, f_user: bool = True, cou
         if stats:
             nb = n_buckets if n_buckets is not None else db.n_buckets
             out["stats"] = torch.empty((nb, STATS_FIELDS), dtype=torch.float64, device=dev)
+        if partition:
+            out["partition"] = torch.empty(nu, dtype=torch.int32, device=dev)
     r = JResult(*[_ptr(out.get(f)) for f in ("E", "E_lc", "t_free_next", "f_e", "n_tilde", "j", "status", "mask",
                                              "f_user", "counts", "stats")],
-                int(out["stats"].shape[0]) if out.get("stats") is not None else 0)
+                int(out["stats"].shape[0]) if out.get("stats") is not None else 0, _ptr(out.get("partition")))
     ws = db.workspace(0)
     _check(lib().jdob_solve_batch(db.jmodels, db.n_models, C.byref(db.jbatch), int(mode), C.byref(r),
                                   ws.data_ptr(), ws.numel(), _stream_handle(stream)))
@@ -306,7 +310,7 @@ def solve_batch_host(hb: HostBuffers, mode: int = MODE_FULL, stream=None):
     Returns (h2d_bytes, d2h_bytes)."""
     o = hb.out
     r = JResult(*[_ptr(o.get(f)) for f in ("E", "E_lc", "t_free_next", "f_e", "n_tilde", "j", "status", "mask",
-                                           "f_user", "counts", "stats")], hb.n_buckets)
+                                           "f_user", "counts", "stats")], hb.n_buckets, _ptr(o.get("partition")))
     h2d = C.c_int64()
     d2h = C.c_int64()
     _check(lib().jdob_solve_batch_host(hb.jmodels, hb.n_models, C.byref(hb.jbatch), int(mode), C.byref(r),

@@ -53,8 +53,8 @@ static int check_models(const jdob_model *models, int32_t n_models) {
     for (int i = 0; i < n_models; i++) {
         const jdob_model &m = models[i];
         if (m.N < 1 || m.N > JDOB_MAX_N) return fail(JDOB_EINVAL, "model %d: N = %d outside [1, %d]", i, m.N, JDOB_MAX_N);
-        if (m.B_max < 1 || m.B_max > JDOB_MAX_M)
-            return fail(JDOB_EINVAL, "model %d: B_max = %d outside [1, %d]", i, m.B_max, JDOB_MAX_M);
+        if (m.B_max < 1 || m.B_max > JDOB_MAX_M_LARGE)
+            return fail(JDOB_EINVAL, "model %d: B_max = %d outside [1, %d]", i, m.B_max, JDOB_MAX_M_LARGE);
         if (!m.A || !m.O || !m.g || !m.q || !m.d || !m.c) return fail(JDOB_EINVAL, "model %d: NULL table", i);
     }
     return JDOB_OK;
@@ -175,7 +175,8 @@ const char *jdob_version(void) { return "jdob-b200 0.1 (sm_100a)"; }
 size_t jdob_workspace_bytes(const jdob_model *models, int32_t n_models, int32_t which) {
     if (!models || n_models < 1) return 0;
     for (int i = 0; i < n_models; i++)
-        if (models[i].N < 1 || models[i].N > JDOB_MAX_N || models[i].B_max < 1 || models[i].B_max > JDOB_MAX_M)
+        if (models[i].N < 1 || models[i].N > JDOB_MAX_N || models[i].B_max < 1 ||
+            models[i].B_max > JDOB_MAX_M_LARGE)
             return 0;
     size_t s = models_bytes(models, n_models);
     if (which == 0) return s + stats_partial_bytes();
@@ -232,7 +233,13 @@ int jdob_solve_batch(const jdob_model *models, int32_t n_models, const jdob_batc
     dr.mask = out->mask;
     dr.f_user = out->f_user;
     dr.counts = (long long *)out->counts;
+    dr.partition = out->partition;
     launch_solve(dm, db, dr, mode, s, num_sms());
+    // instances with 32 < M <= B_max (block per instance); M > B_max is BADPARAM, so the launch is
+    // needed only when some model admits batches wider than a warp
+    bool wide = false;
+    for (int i = 0; i < n_models; i++) wide |= models[i].B_max > JDOB_MAX_M;
+    if (wide) launch_solve_large(dm, db, dr, mode, s, num_sms());
     if ((rc = cuda_check("solve"))) return rc;
     if (out->stats) {
         double *partials = (double *)((char *)ws + models_bytes(models, n_models));
@@ -381,7 +388,8 @@ int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob
     g_err.clear();
     if (!models || n_models < 1) return fail(JDOB_EINVAL, "models");
     for (int i = 0; i < n_models; i++) {
-        if (models[i].N < 1 || models[i].N > JDOB_MAX_N || models[i].B_max < 1 || models[i].B_max > JDOB_MAX_M)
+        if (models[i].N < 1 || models[i].N > JDOB_MAX_N || models[i].B_max < 1 ||
+            models[i].B_max > JDOB_MAX_M_LARGE)
             return fail(JDOB_EINVAL, "model %d: N/B_max out of range", i);
         if (!models[i].A || !models[i].O || !models[i].g || !models[i].q || !models[i].d || !models[i].c)
             return fail(JDOB_EINVAL, "model %d: NULL table", i);
@@ -408,6 +416,7 @@ int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob
     const size_t in_inst = al(n * 4) + al((n + 1) * 8) + 4 * al(n * 8) + (b->bucket ? al(n * 4) : 0);
     const size_t in_user = 7 * al(nu * 8);
     const size_t outb = 4 * al(n * 8) + 4 * al(n * 4) + (out->f_user ? al(nu * 8) : 0) +
+                        (out->partition ? al(nu * 4) : 0) +
                         (out->counts ? al(n * 3 * 8) : 0) +
                         (out->stats ? al((size_t)out->n_buckets * JDOB_STATS_FIELDS * 8) : 0);
     const size_t wsb = jdob_workspace_bytes(models, n_models, 0);
@@ -466,6 +475,7 @@ int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob
     dr.f_user = out->f_user ? (double *)take(nu * 8) : nullptr;
     dr.counts = out->counts ? (int64_t *)take(n * 3 * 8) : nullptr;
     dr.stats = out->stats ? (double *)take((size_t)out->n_buckets * JDOB_STATS_FIELDS * 8) : nullptr;
+    dr.partition = out->partition ? (int32_t *)take(nu * 4) : nullptr;
     void *ws[NS];
     for (int k = 0; k < NS; k++) ws[k] = take(wsb);
 
@@ -534,6 +544,7 @@ int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob
         d2(out->status + i0, cr.status, (i1 - i0) * 4);
         d2(out->mask + i0, cr.mask, (i1 - i0) * 4);
         if (out->f_user) d2(out->f_user + u0, dr.f_user + u0, (u1 - u0) * 8);
+        if (out->partition) d2(out->partition + u0, dr.partition + u0, (u1 - u0) * 4);
         if (out->counts) d2(out->counts + 3 * i0, cr.counts, (i1 - i0) * 3 * 8);
     }
     for (int k = 0; k < NS; k++) {
@@ -552,6 +563,7 @@ int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob
         r2.mask = dr.mask;
         r2.f_user = dr.f_user;
         r2.counts = (long long *)dr.counts;
+        r2.partition = dr.partition;
         double *partials = (double *)((char *)ws[0] + models_bytes(models, n_models));
         launch_stats(to_dev(&db), r2, partials, dr.stats, out->n_buckets, s);
         cudaMemcpyAsync(out->stats, dr.stats, (size_t)out->n_buckets * JDOB_STATS_FIELDS * 8,

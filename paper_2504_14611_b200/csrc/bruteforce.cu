@@ -33,6 +33,10 @@ __global__ void k_bf_setup(const DevModel *models, DevBatch b, int space, BfHead
     const DevModel *mdp;
     InstRegs x;
     int st = warp_validate(models, b, 0, lane, x, M, k, mdp, off);
+    if (st == kStDefer) {  // more than 32 users: outside the brute-force index encoding
+        st = JDOB_ST_TOOBIG;
+        M = 0;
+    }
     if (lane == 0) {
         hdr->status = st;
         hdr->M = M;

@@ -29,6 +29,7 @@ __global__ void k_og_prep(const DevModel *models, DevBatch b, OgWork w) {
     const DevModel *mdp;
     InstRegs x;
     int st = warp_validate(models, b, i, lane, x, M, k, mdp, off);
+    if (st == kStDefer) st = JDOB_ST_BADPARAM;   // grouping takes M <= 32
     if (st == JDOB_ST_REQUIRE) st = JDOB_ST_OK;  // the DP costs a failed Require per group
     const long long M64 = b.user_off[i + 1] - off;
     if (st != JDOB_ST_OK) {
@@ -222,6 +223,7 @@ static DevResult stage_result(const OgWork &w, double *f_user) {
     r.mask = w.r_mask;
     r.f_user = f_user;
     r.counts = nullptr;
+    r.partition = nullptr;
     return r;
 }
 

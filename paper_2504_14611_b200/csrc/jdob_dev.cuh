@@ -15,6 +15,8 @@
 namespace jdob {
 
 constexpr int kMaxM = JDOB_MAX_M;
+constexpr int kMaxMLarge = JDOB_MAX_M_LARGE;
+constexpr int kStDefer = -1;  // internal status: M > 32, handled by k_solve_large
 constexpr int kMaxN = JDOB_MAX_N;
 constexpr int kMaxK = JDOB_MAX_K;
 constexpr int kStatsF = JDOB_STATS_FIELDS;
@@ -47,6 +49,7 @@ struct DevResult {
     unsigned *mask;
     double *f_user;
     long long *counts;
+    int *partition;   // per user n~* or N, or NULL
 };
 
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
@@ -102,7 +105,8 @@ __device__ __forceinline__ int warp_validate(const DevModel *models, const DevBa
     }
     mdp = &models[mid];
     if (*mdp->valid == 0) return JDOB_ST_BADMODEL;
-    if (M64 < 1 || M64 > kMaxM || M64 > mdp->B1 - 1) return JDOB_ST_BADPARAM;
+    if (M64 < 1 || M64 > kMaxMLarge || M64 > mdp->B1 - 1) return JDOB_ST_BADPARAM;
+    if (M64 > kMaxM) return kStDefer;  // more users than lanes: the block-per-instance path
     bool ok = true;
     if (lane < M) {
         const long long u = off + lane;

@@ -51,6 +51,8 @@ int launch_grouped(const DevModel *models, const DevBatch &b, int mode, const Og
                    cudaStream_t s, int num_sms);
 void launch_solve(const DevModel *models, const DevBatch &b, const DevResult &r, int mode, cudaStream_t s,
                   int num_sms);
+void launch_solve_large(const DevModel *models, const DevBatch &b, const DevResult &r, int mode, cudaStream_t s,
+                        int num_sms);
 void launch_stats(const DevBatch &b, const DevResult &r, double *partials, double *stats, int n_buckets,
                   cudaStream_t s);
 void launch_eval(const DevModel *models, const DevBatch &b, const int *partition, const int *plan_nt,

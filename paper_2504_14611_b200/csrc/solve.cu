@@ -131,6 +131,7 @@ __device__ __forceinline__ void write_bad(const DevResult &r, long long i, long 
         }
     }
     if (r.f_user && M >= 1 && M <= kMaxM && lane < M) r.f_user[off + lane] = dnan();
+    if (r.partition && M >= 1 && M <= kMaxM && lane < M) r.partition[off + lane] = N;
 }
 
 __device__ __forceinline__ void write_local(const DevResult &r, long long i, long long off, int M, int N,
@@ -152,6 +153,7 @@ __device__ __forceinline__ void write_local(const DevResult &r, long long i, lon
         }
     }
     if (r.f_user && lane < M) r.f_user[off + lane] = floc;
+    if (r.partition && lane < M) r.partition[off + lane] = N;
 }
 
 template <bool COUNTS>
@@ -163,6 +165,7 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
     const DevModel *mdp;
     InstRegs x;
     const int st = warp_validate(models, b, i, lane, x, M, k, mdp, off);
+    if (st == kStDefer) return;  // M > 32: solved by k_solve_large (solve_large.cu)
     const double t_free = b.t_free[i], fe_max = b.fe_max[i], rho = b.rho[i];
     if (st == JDOB_ST_BADPARAM || st == JDOB_ST_BADMODEL) {
         write_bad(r, i, off, M, mdp ? mdp->N : 0, t_free, st, lane);
@@ -399,6 +402,7 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
         r.mask[i] = mask;
     }
     if (r.f_user && lane < M) r.f_user[off + lane] = f;
+    if (r.partition && lane < M) r.partition[off + lane] = member ? bN : N;
 }
 
 #ifndef JDOB_SOLVE_MINB

@@ -342,3 +342,63 @@ def test_og_statuses(J):
     b = g.toy_instance("toy-1"); b.f_min[1] = 3e9; parts.append(b)     # BADPARAM
     for b in parts:
         _og_parity(J, b)
+
+
+# ------------------------------- M > 32 (NEXT-4) -----------------------------------
+def _large_batch(Ms, seed, hetero=False, tfree=False):
+    from tests.test_oracle_large import large_instance
+    b = g.concat([large_instance(M, seed + q, hetero=hetero) for q, M in enumerate(Ms)])
+    if tfree:
+        for i in range(b.n_inst):
+            b.t_free[i] = 0.5 * b.T[b.user_off[i]:b.user_off[i + 1]].min()
+    return b
+
+
+def _large_parity(J, b, mode=0):
+    db = J.DeviceBatch(b)
+    res = J.solve_batch(db, mode=mode, counts=True, partition=True)
+    import torch
+    torch.cuda.synchronize()
+    gpu = to_np(res)
+    orc = O.solve_batch(b, mode=mode, counts=True)
+    for f in ("E", "E_lc", "t_free_next", "f_e", "n_tilde", "j", "status", "counts", "f_user"):
+        assert_bits_equal(gpu[f].reshape(-1), orc[f].reshape(-1), "large " + f)
+    assert_bits_equal(gpu["partition"], orc["part"], "large partition")
+
+
+@pytest.mark.parametrize("hetero,tfree", [(False, False), (True, True)])
+def test_large_m_parity(J, hetero, tfree):
+    _large_parity(J, _large_batch([33, 48, 64, 100, 257], seed=3, hetero=hetero, tfree=tfree))
+
+
+def test_large_m_mixed_batch_and_modes(J):
+    # M <= 32 (warp path) and M > 32 (block path) in one batch
+    small = g.random_batch(seed=191, n_inst=40, M_lo=1, M_hi=32, N_lo=1, N_hi=8, k_max=40)
+    mix = g.concat([small, _large_batch([40, 77], seed=9)])
+    for mode in (0, 2, 3):
+        _large_parity(J, mix, mode=mode)
+    # statuses on the block path: local infeasibility and Require
+    bb = _large_batch([50, 60], seed=11)
+    bb.T[3] = 1e-6
+    bb.t_free[1] = 10.0
+    _large_parity(J, bb)
+
+
+def test_large_m_complexity_smoke(J):
+    # M = 1000, N = 19, k ~ 64 well under 10 s, bit-exact vs the oracle
+    import time
+    import torch
+    b = _large_batch([1000], seed=7)
+    db = J.DeviceBatch(b)
+    J.solve_batch(db)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = J.solve_batch(db, partition=True)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    assert dt < 10.0
+    orc = O.solve_batch(b)
+    gpu = to_np(res)
+    for f in ("E", "n_tilde", "j", "t_free_next"):
+        assert_bits_equal(gpu[f], orc[f], f)
+    assert_bits_equal(gpu["partition"], orc["part"], "partition")
