@@ -12,8 +12,9 @@ Extra legs in the same line: "bruteforce" (C4 exhaustive search, 2.75e10
 candidates, index space sharded over the ranks, NCCL MIN-allreduce of (E, idx)),
 "e2e" (jdob_solve_batch_host from pinned host buffers, copies inside the timed
 region), "cpu_baseline" (the C oracle on a bounded sample on the host cores),
-"roofline" (FP64-pipe work of K1 from the literal Alg. 2 counters / its live
-CUDA-event duration, against the FP64 peak of DESIGN.md §Roofline).
+"roofline" (FP64 work K1 executed -- from its executed-work counters -- / its
+live CUDA-event duration, against the FP64 peak of DESIGN.md §Roofline; the
+literal Alg. 1/2 work of the same launch is reported beside it).
 
 --impl reference times the CPU oracle (the reference arm of this tier).
 """
@@ -115,16 +116,20 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def fp64_work(batch, counts):
-    """Algorithmic FP64 operations of K1 per launch: the literal Alg. 1/2 evaluation,
-    each +, -, x, / or comparison = 1 op, from the per-instance counters (n_visit, n_eval, n_member):
-      member evaluation 9, non-member term 1, evaluated pair 6, visited pair 4,
-      per n~ setup 6M + M(M-1)/2 + 3M, LC 8M."""
+def fp64_work(batch, counts, setups=None, lower_bound=False):
+    """FP64 operations of K1 per launch, each +, -, x, / or comparison = 1 op, from
+    per-instance counters (n_visit, n_eval, n_member): member evaluation 9, non-member term 1,
+    evaluated pair 6, visited pair 4, per n~ set-up 6M + M(M-1)/2 + 3M, LC 8M.  Literal Alg. 1/2:
+    every n~ is set up (setups = N).  Executed (pruned sweep): setups and pairs from the executed-work
+    counters, plus the n~ lower bounds (8 ops per (n~, user) and one RD reciprocal per user)."""
     M = np.diff(batch.user_off).astype(np.float64)
     N = np.array([batch.models[m].N for m in batch.model_id], np.float64)
     visit, ev, mem = (counts[:, 0].astype(np.float64), counts[:, 1].astype(np.float64),
                       counts[:, 2].astype(np.float64))
-    ops = 9 * mem + (ev * M - mem) + 6 * ev + 4 * visit + N * (6 * M + M * (M - 1) / 2 + 3 * M) + 8 * M
+    S = N if setups is None else setups.astype(np.float64)
+    ops = 9 * mem + (ev * M - mem) + 6 * ev + 4 * visit + S * (6 * M + M * (M - 1) / 2 + 3 * M) + 8 * M
+    if lower_bound:
+        ops = ops + (8 * N * M + M) * (S > 0)
     return float(np.sum(ops)), float(np.sum(mem))
 
 
@@ -209,10 +214,14 @@ def run_mine(args):
     db = J.DeviceBatch(batch)
     torch.cuda.synchronize()
 
-    # untimed: algorithmic work counters (literal Alg. 2 counts, checked against the oracle in tests)
+    # untimed: algorithmic work counters -- literal Alg. 2 counts (checked against the oracle in tests)
+    # and the work the pruned product sweep executes (same decisions as the timed launches)
     res_c = J.solve_batch(db, counts=True, f_user=False)
     counts = res_c["counts"].cpu().numpy()
-    work, n_member = fp64_work(batch, counts)
+    literal_work, n_member = fp64_work(batch, counts)
+    wk = J.solve_batch(db, work=True, f_user=False)["work"].cpu().numpy()
+    work, n_member_exec = fp64_work(batch, wk[:, 1:], setups=wk[:, 0], lower_bound=True)
+    setup_frac = float(wk[:, 0].sum()) / float(sum(batch.models[m].N for m in batch.model_id))
     # parity spot check against the oracle on 64 sampled instances (rank 0)
     parity = None
     if rank == 0:
@@ -272,8 +281,9 @@ def run_mine(args):
         t = torch.tensor([total_ms, solve_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms, solve_ms = float(t[0]), float(t[1])
-        w = torch.tensor([work], device="cuda", dtype=torch.float64)
+        w = torch.tensor([work, literal_work], device="cuda", dtype=torch.float64)
         dist.all_reduce(w, op=dist.ReduceOp.MAX)   # per-GPU work of the slowest rank's kind
+        work, literal_work = float(w[0]), float(w[1])
     value = world * n * K / (total_ms / 1e3)
 
     # end-to-end through the public host-buffer API (copies inside the timed region)
@@ -334,10 +344,14 @@ def run_mine(args):
                          "unit": "G FP64 op/s", "frac": achieved / peak,
                          "traffic": ncu_traffic("k_solve") if args.workload == "c2" else None,
                          "algorithmic_bytes": int(batch.nbytes()),
-                         "work_per_launch": work, "member_evals_per_launch": n_member,
+                         "work_per_launch": work, "member_evals_per_launch": n_member_exec,
+                         "literal_work_per_launch": literal_work, "literal_member_evals_per_launch": n_member,
+                         "literal_equivalent": literal_work / (solve_ms / 1e3) / 1e9,
+                         "n_tilde_setups_frac": setup_frac,
                          "launch_ms": solve_ms,
-                         "peak_note": "148 SMs x 64 FP64 lanes/clk x max SM clock (DESIGN.md §7); "
-                                      "work = literal Alg. 1/2 FP64 ops, division = 1 op"},
+                         "peak_note": "148 SMs x 64 FP64 lanes/clk x max SM clock (DESIGN.md §7); work = FP64 "
+                                      "ops K1 executed (exact n~ pruning), division = 1 op; literal_equivalent "
+                                      "= the unpruned Alg. 1/2 work of the same launch / its time"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": 6 * K,

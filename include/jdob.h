@@ -129,7 +129,9 @@ typedef struct {
  *   f_user [user_off[n_inst]] : optional (NULL = skip) device frequencies f_m* (D20).
  *   counts [3*n_inst]    : optional (NULL = skip) literal Alg. 2 work counters per
  *                          instance: (n~, j) pairs visited, pairs evaluated (guard
- *                          passed), sum of B_o over evaluated pairs.
+ *                          passed), sum of B_o over evaluated pairs.  Requesting them
+ *                          turns off the exact n~ pruning (every n~ is swept literally);
+ *                          results are identical either way.
  *   stats [n_buckets * JDOB_STATS_FIELDS] : optional (NULL = skip) energy-saving
  *                          statistics (a12, R16), fields per bucket:
  *                          [0] #OK instances, [1] sum r, [2] sum r^2, [3] max r,
@@ -148,6 +150,9 @@ typedef struct {
     double *stats;
     int32_t n_buckets;  /* 1 .. JDOB_MAX_BUCKETS when stats != NULL */
     int32_t *partition; /* optional [user_off[n_inst]]: n~* for offloaders, N for local users */
+    int64_t *work;      /* optional [4*n_inst], ignored when counts != NULL and by the host API:
+                           work the pruned sweep executed per instance -- n~ set-ups, visited
+                           pairs, evaluated pairs, member evaluations */
 } jdob_result;
 
 /*

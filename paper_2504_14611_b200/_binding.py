@@ -39,7 +39,8 @@ class JBatch(C.Structure):
 class JResult(C.Structure):
     _fields_ = [(f, C.c_void_p) for f in ("E", "E_lc", "t_free_next", "f_e", "n_tilde", "j", "status", "mask",
                                           "f_user", "counts", "stats")] + [("n_buckets", C.c_int32),
-                                                                           ("partition", C.c_void_p)]
+                                                                           ("partition", C.c_void_p),
+                                                                           ("work", C.c_void_p)]
 
 
 class JGrouped(C.Structure):
@@ -170,7 +171,7 @@ class DeviceBatch:
 
 def solve_batch(db: DeviceBatch, mode: int = MODE_FULL, f_user: bool = True, counts: bool = False,
                 stats: bool = False, n_buckets: Optional[int] = None, stream=None, out: Optional[dict] = None,
-                partition: bool = False) -> dict:
+                partition: bool = False, work: bool = False) -> dict:
     """jdob_solve_batch: J-DOB (Alg. 1/2) over every instance of `db`; outputs are device tensors."""
     torch = _torch()
     dev = db.device
@@ -193,9 +194,12 @@ def solve_batch(db: DeviceBatch, mode: int = MODE_FULL, f_user: bool = True, cou
             out["stats"] = torch.empty((nb, STATS_FIELDS), dtype=torch.float64, device=dev)
         if partition:
             out["partition"] = torch.empty(nu, dtype=torch.int32, device=dev)
+        if work:
+            out["work"] = torch.empty((n, 4), dtype=torch.int64, device=dev)
     r = JResult(*[_ptr(out.get(f)) for f in ("E", "E_lc", "t_free_next", "f_e", "n_tilde", "j", "status", "mask",
                                              "f_user", "counts", "stats")],
-                int(out["stats"].shape[0]) if out.get("stats") is not None else 0, _ptr(out.get("partition")))
+                int(out["stats"].shape[0]) if out.get("stats") is not None else 0, _ptr(out.get("partition")),
+                _ptr(out.get("work")))
     ws = db.workspace(0)
     _check(lib().jdob_solve_batch(db.jmodels, db.n_models, C.byref(db.jbatch), int(mode), C.byref(r),
                                   ws.data_ptr(), ws.numel(), _stream_handle(stream)))
@@ -310,7 +314,7 @@ def solve_batch_host(hb: HostBuffers, mode: int = MODE_FULL, stream=None):
     Returns (h2d_bytes, d2h_bytes)."""
     o = hb.out
     r = JResult(*[_ptr(o.get(f)) for f in ("E", "E_lc", "t_free_next", "f_e", "n_tilde", "j", "status", "mask",
-                                           "f_user", "counts", "stats")], hb.n_buckets, _ptr(o.get("partition")))
+                                           "f_user", "counts", "stats")], hb.n_buckets, _ptr(o.get("partition")), None)
     h2d = C.c_int64()
     d2h = C.c_int64()
     _check(lib().jdob_solve_batch_host(hb.jmodels, hb.n_models, C.byref(hb.jbatch), int(mode), C.byref(r),

@@ -234,6 +234,7 @@ int jdob_solve_batch(const jdob_model *models, int32_t n_models, const jdob_batc
     dr.f_user = out->f_user;
     dr.counts = (long long *)out->counts;
     dr.partition = out->partition;
+    dr.work = (long long *)out->work;
     launch_solve(dm, db, dr, mode, s, num_sms());
     // instances with 32 < M <= B_max (block per instance); M > B_max is BADPARAM, so the launch is
     // needed only when some model admits batches wider than a warp
@@ -476,6 +477,7 @@ int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob
     dr.counts = out->counts ? (int64_t *)take(n * 3 * 8) : nullptr;
     dr.stats = out->stats ? (double *)take((size_t)out->n_buckets * JDOB_STATS_FIELDS * 8) : nullptr;
     dr.partition = out->partition ? (int32_t *)take(nu * 4) : nullptr;
+    dr.work = nullptr;  // device-API diagnostic only
     void *ws[NS];
     for (int k = 0; k < NS; k++) ws[k] = take(wsb);
 

@@ -49,7 +49,8 @@ struct DevResult {
     unsigned *mask;
     double *f_user;
     long long *counts;
-    int *partition;   // per user n~* or N, or NULL
+    int *partition = nullptr;   // per user n~* or N, or NULL
+    long long *work = nullptr;  // [4 n_inst] executed-work counters of the pruned sweep, or NULL
 };
 
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }

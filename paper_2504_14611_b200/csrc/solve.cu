@@ -49,6 +49,8 @@ struct SolveSmem {
     double2 pp[kMaxM];                   // per sorted position p: {phi_n~(M - p), psi_n~(M - p)}
     int rank[kMaxM], order[kMaxM];
     double inv[kInvCache];
+    double rinv[kMaxM];                  // RD(1 / R_m): lower-bound upload term
+    double lb[64];                       // per n~: lower bound of every configuration's energy
 };
 
 // Ranks under the key (gamma desc, T asc, index asc) (R2), then order[] and the
@@ -129,6 +131,7 @@ __device__ __forceinline__ void write_bad(const DevResult &r, long long i, long 
             r.counts[3 * i + 1] = 0;
             r.counts[3 * i + 2] = 0;
         }
+        if (r.work) r.work[4 * i] = r.work[4 * i + 1] = r.work[4 * i + 2] = r.work[4 * i + 3] = 0;
     }
     if (r.f_user && M >= 1 && M <= kMaxM && lane < M) r.f_user[off + lane] = dnan();
     if (r.partition && M >= 1 && M <= kMaxM && lane < M) r.partition[off + lane] = N;
@@ -151,12 +154,17 @@ __device__ __forceinline__ void write_local(const DevResult &r, long long i, lon
             r.counts[3 * i + 1] = 0;
             r.counts[3 * i + 2] = 0;
         }
+        if (r.work && zero_counts) r.work[4 * i] = r.work[4 * i + 1] = r.work[4 * i + 2] = r.work[4 * i + 3] = 0;
     }
     if (r.f_user && lane < M) r.f_user[off + lane] = floc;
     if (r.partition && lane < M) r.partition[off + lane] = N;
 }
 
-template <bool COUNTS>
+// COUNTS: per-instance work counters.  PRUNE: skip every n~ whose energy lower bound is not below
+// the best energy found so far (exact, DESIGN.md §4 "n~ pruning").  <true, false> = literal Alg. 2
+// counters (r.counts), <true, true> = executed-work counters of the pruned sweep (r.work),
+// <false, true> = the product path.
+template <bool COUNTS, bool PRUNE>
 __device__ __forceinline__ void solve_instance(long long i, const DevModel *models, const DevBatch &b,
                                                const DevResult &r, int mode, SolveSmem &s, int lane) {
     __syncwarp();
@@ -206,149 +214,223 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
     const double f00 = __shfl_sync(0xffffffffu, x.f0, 0), k0 = __shfl_sync(0xffffffffu, x.k, 0);
     const double p0 = __shfl_sync(0xffffffffu, x.p, 0);
     const bool uni = homog && __all_sync(0xffffffffu, lane >= M || (x.f0 == f00 && x.k == k0 && x.p == p0));
-    if (homog) sort_users(M, 0.0, x.T, s, lane);  // equal gamma: key (T asc, index asc)
+    const double T0 = __shfl_sync(0xffffffffu, x.T, 0);
+    if (homog && __all_sync(0xffffffffu, lane >= M || x.T == T0)) {
+        // equal gamma and equal deadlines (Table I identical-deadline setting): the key (T asc,
+        // index asc) is the index order and every suffix minimum is T
+        if (lane < M) {
+            s.rank[lane] = lane;
+            s.order[lane] = lane;
+            s.Lg[lane].x = x.T;
+        }
+    } else if (homog) {
+        sort_users(M, 0.0, x.T, s, lane);  // equal gamma: key (T asc, index asc)
+    }
     __syncwarp();
 
     const int B1 = md.B1;
-    double bE = dinf();
-    int bN = 0x7fffffff, bP = 0, bJ = 0;
-    int aN = N;  // first all-local evaluation key (R8); n~ = N at j = 0 by default (R4)
-    int aJ = 0;
-    long long c_visit = 0, c_eval = 0, c_member = 0;
-
-    for (int nt = 0; nt < N; nt++) {
-        if (mode == JDOB_MODE_BINARY && nt != 0) break;
-        const int ihat = setup_nt(md, nt, M, homog, uni, t_free, s, lane);
-        // two grid points per lane (j0 + lane and j0 + 32 + lane): the two energy chains are
-        // independent, which doubles the instruction-level parallelism of the sweep and lets both
-        // share each user's shared-memory loads
-        for (long long j0 = 0; j0 < kk; j0 += 64) {
-            const long long jA = j0 + lane, jB = jA + 32;
-            const bool vA = jA < kk, vB = jB < kk;
-            const double feA = grid_fe(fe_max, rho, jA), feB = grid_fe(fe_max, rho, jB);
-            // p(j): first sorted position >= i^ with !(f_e < th_i)  (M if the set is empty)
-            int loA = ihat, hiA = M, loB = ihat, hiB = M;
-            while (loA < hiA) {
-                const int mm = (loA + hiA) >> 1;
-                if (feA < s.th[mm]) loA = mm + 1;
-                else hiA = mm;
+    const bool use_lb = PRUNE && mode != JDOB_MODE_BINARY;
+    if (use_lb) {
+        // Lower bound of E over every configuration at n~: a member's term
+        // ((kappa u) f*) f* + (O/R) p >= ((kappa u) f_min) f_min + RN(RD(O RD(1/R)) p) (f* >= f_min, RN
+        // monotone), a non-member's term is e_loc, so each term >= the min of the two; the user-order
+        // RN sum of the minima is <= the sum of the terms, and the edge term (psi f_e) f_e >= 0.
+        if (lane < M) s.rinv[lane] = __ddiv_rd(1.0, x.R);
+        __syncwarp();
+        for (int nt = lane; nt < N; nt += 32) {
+            const double u_nt = md.u[nt], O_nt = md.O[nt];
+            double S = 0.0;
+            for (int m = 0; m < M; m++) {
+                const double ku = s.kap[m] * u_nt;
+                const double up = __dmul_rd(O_nt, s.rinv[m]) * s.pu[m];
+                const double fm = s.fmm[m].x;
+                const double em = ((ku * fm) * fm) + up;
+                const double el = s.et[m].x;
+                S = S + ((em < el) ? em : el);
             }
-            while (loB < hiB) {
-                const int mm = (loB + hiB) >> 1;
-                if (feB < s.th[mm]) loB = mm + 1;
-                else hiB = mm;
-            }
-            const int pA = loA, pB = loB;
-            // Alg. 2's break: the first j with an empty set ends this n~'s sweep
-            const unsigned empA = __ballot_sync(0xffffffffu, vA && pA == M);
-            const unsigned empB = __ballot_sync(0xffffffffu, vB && pB == M);
-            const long long jb = empA ? j0 + (__ffs(empA) - 1) : (empB ? j0 + 32 + (__ffs(empB) - 1) : kk);
-            const bool emp = (empA | empB) != 0u;
-            if (emp && aN == N) {
-                aN = nt;
-                aJ = (int)jb;
-            }
-            if (COUNTS && emp && lane == 0) {  // the all-local evaluation at jb (guard passes: 0 / inf = 0)
-                c_visit += 1;
-                c_eval += 1;
-            }
-            const bool actA = vA && jA < jb, actB = vB && jB < jb;
-            const int qA = actA ? pA : 0, qB = actB ? pB : 0;  // p < M for active grid points
-            const double2 lgA = s.Lg[qA], lgB = s.Lg[qB];     // l_o, phi / (l_o - t_free)
-            const double2 pqA = s.pp[qA], pqB = s.pp[qB];     // phi_n~(B_o), psi_n~(B_o)
-            // D6 guard: f_e >= phi / (l_o - t_free); the quotient depends only on p
-            const bool passA = actA && feA >= lgA.y, passB = actB && feB >= lgB.y;
-            if (COUNTS) {
-                c_visit += (actA ? 1 : 0) + (actB ? 1 : 0);
-                c_eval += (passA ? 1 : 0) + (passB ? 1 : 0);
-                c_member += (passA ? M - pA : 0) + (passB ? M - pB : 0);
-            }
-            if (!(passA || passB)) {
-                if (emp) break;
-                continue;
-            }
-            const double invA = (jA < kInvCache) ? s.inv[jA] : 1.0 / feA;
-            const double invB = (jB < kInvCache) ? s.inv[jB] : 1.0 / feB;
-            const double teA = pqA.x * invA, teB = pqB.x * invB;
-            double EA = 0.0, EB = 0.0;
-            if (uni) {
-                // Uniform users (same R, zeta, f_min, f_max, kappa, p_u; Table I): every member
-                // has the same budget, f* and offloader term, so D20/D21 are formed once and
-                // only the user-order sum runs over M.  Same operations, same bits.
-                const double2 a0 = s.orzv[0], c0 = s.kuup[0], t0 = s.fmm[0];
-                const double budA = (lgA.x - a0.x) - teA, budB = (lgB.x - a0.x) - teB;
-                double fA = t0.x, fB = t0.x;
-                if (passA && !(__fma_rn(t0.x, budA, -a0.y) > 0.0) && a0.y != 0.0)
-                    fA = clampf(a0.y / budA, t0.x, t0.y);  // D20 (R9 when zv = 0)
-                if (passB && !(__fma_rn(t0.x, budB, -a0.y) > 0.0) && a0.y != 0.0)
-                    fB = clampf(a0.y / budB, t0.x, t0.y);
-                const double emA = ((c0.x * fA) * fA) + c0.y;  // D21 offloader term
-                const double emB = ((c0.x * fB) * fB) + c0.y;
-#pragma unroll 4
-                for (int m = 0; m < M; m++) {
-                    const double2 et = s.et[m];  // eloc, thu
-                    EA = EA + ((!(feA < et.y)) ? emA : et.x);
-                    EB = EB + ((!(feB < et.y)) ? emB : et.x);
-                }
-            } else {
-                const long long fbA = __double_as_longlong(feA), fbB = __double_as_longlong(feB);
-#pragma unroll 2
-                for (int m = 0; m < M; m++) {
-                    const double2 a = s.orzv[m];  // OR, zv
-                    const double2 c = s.kuup[m];  // ku, up
-                    const double2 d = s.et[m];    // eloc, thu
-                    const double2 t = s.fmm[m];   // fmin, fmax
-                    // f_e, th >= 0 (or +inf): IEEE order = integer order of the bit patterns
-                    const long long thb = __double_as_longlong(d.y);
-                    const bool memA = fbA >= thb, memB = fbB >= thb;
-                    const double budA = (lgA.x - a.x) - teA, budB = (lgB.x - a.x) - teB;
-                    double fA = t.x, fB = t.x;  // f_min unless f_min budget > zv fails exactly
-                    const bool needA = passA && memA && !(__fma_rn(t.x, budA, -a.y) > 0.0);
-                    const bool needB = passB && memB && !(__fma_rn(t.x, budB, -a.y) > 0.0);
-                    if (needA || needB) {
-                        // R9 (zv = 0 -> f_min) tested on the bits, inside the rare branch
-                        const bool nz = (__double_as_longlong(a.y) << 1) != 0;
-                        if (needA && nz) fA = clampf(a.y / budA, t.x, t.y);  // D20
-                        if (needB && nz) fB = clampf(a.y / budB, t.x, t.y);
-                    }
-                    const double emA = ((c.x * fA) * fA) + c.y;  // D21 offloader term
-                    const double emB = ((c.x * fB) * fB) + c.y;
-                    EA = EA + (memA ? emA : d.x);
-                    EB = EB + (memB ? emB : d.x);
-                }
-            }
-            EA = EA + (pqA.y * feA) * feA;
-            EB = EB + (pqB.y * feB) * feB;
-            if (passA && EA < bE) {  // strict: lane keys ascend in (n~, j)
-                bE = EA;
-                bN = nt;
-                bJ = (int)jA;
-                bP = pA;
-            }
-            if (passB && EB < bE) {
-                bE = EB;
-                bN = nt;
-                bJ = (int)jB;
-                bP = pB;
-            }
-            if (emp) break;
+            s.lb[nt] = S;
         }
         __syncwarp();
     }
-    // warp argmin over (E, n~, j)
+    double bE;
+    int bN, bP, bJ, aN, aJ;
+    long long c_setup = 0, c_visit = 0, c_eval = 0, c_member = 0;
+    int last_nt = -1;  // the n~ whose set-up is in shared memory
+    for (int pass = 0;; pass++) {
+        // pass 1 (rare): an exact tie with E_LC after pruning -- the all-local key (aN, aJ) of the
+        // skipped n~ may matter (R8), so the instance is swept again without pruning
+        const bool prune = use_lb && pass == 0;
+        bool pruned = false;
+        double bEw = dinf();  // warp-uniform best energy so far
+        bE = dinf();
+        bN = 0x7fffffff;
+        bP = 0;
+        bJ = 0;
+        aN = N;  // first all-local evaluation key (R8); n~ = N at j = 0 by default (R4)
+        aJ = 0;
+
+        for (int nt = -1;;) {
+            if (!prune) {
+                if (++nt >= N || (mode == JDOB_MODE_BINARY && nt != 0)) break;
+            } else {
+                // next n~ whose lower bound is below the best so far (every configuration at a skipped
+                // n~ has E >= lb >= bEw, so none of them can win)
+                unsigned long long cand = __ballot_sync(0xffffffffu, lane < N && s.lb[lane] < bEw);
+                if (N > 32) cand |= (unsigned long long)__ballot_sync(0xffffffffu, lane + 32 < N &&
+                                                                                s.lb[lane + 32] < bEw) << 32;
+                cand &= ~0ull << (nt + 1);
+                if (cand == 0ull) {
+                    pruned |= nt + 1 < N;
+                    break;
+                }
+                const int nx = __ffsll((long long)cand) - 1;
+                pruned |= nx > nt + 1;
+                nt = nx;
+            }
+            if (COUNTS) c_setup += 1;
+            last_nt = nt;
+            const int ihat = setup_nt(md, nt, M, homog, uni, t_free, s, lane);
+            // two grid points per lane (j0 + lane and j0 + 32 + lane): the two energy chains are
+            // independent, which doubles the instruction-level parallelism of the sweep and lets both
+            // share each user's shared-memory loads
+            for (long long j0 = 0; j0 < kk; j0 += 64) {
+                const long long jA = j0 + lane, jB = jA + 32;
+                const bool vA = jA < kk, vB = jB < kk;
+                const double feA = grid_fe(fe_max, rho, jA), feB = grid_fe(fe_max, rho, jB);
+                // p(j): first sorted position >= i^ with !(f_e < th_i)  (M if the set is empty)
+                int loA = ihat, hiA = M, loB = ihat, hiB = M;
+                while (loA < hiA) {
+                    const int mm = (loA + hiA) >> 1;
+                    if (feA < s.th[mm]) loA = mm + 1;
+                    else hiA = mm;
+                }
+                while (loB < hiB) {
+                    const int mm = (loB + hiB) >> 1;
+                    if (feB < s.th[mm]) loB = mm + 1;
+                    else hiB = mm;
+                }
+                const int pA = loA, pB = loB;
+                // Alg. 2's break: the first j with an empty set ends this n~'s sweep
+                const unsigned empA = __ballot_sync(0xffffffffu, vA && pA == M);
+                const unsigned empB = __ballot_sync(0xffffffffu, vB && pB == M);
+                const long long jb = empA ? j0 + (__ffs(empA) - 1) : (empB ? j0 + 32 + (__ffs(empB) - 1) : kk);
+                const bool emp = (empA | empB) != 0u;
+                if (emp && aN == N) {
+                    aN = nt;
+                    aJ = (int)jb;
+                }
+                if (COUNTS && emp && lane == 0) {  // the all-local evaluation at jb (guard passes: 0 / inf = 0)
+                    c_visit += 1;
+                    c_eval += 1;
+                }
+                const bool actA = vA && jA < jb, actB = vB && jB < jb;
+                const int qA = actA ? pA : 0, qB = actB ? pB : 0;  // p < M for active grid points
+                const double2 lgA = s.Lg[qA], lgB = s.Lg[qB];     // l_o, phi / (l_o - t_free)
+                const double2 pqA = s.pp[qA], pqB = s.pp[qB];     // phi_n~(B_o), psi_n~(B_o)
+                // D6 guard: f_e >= phi / (l_o - t_free); the quotient depends only on p
+                const bool passA = actA && feA >= lgA.y, passB = actB && feB >= lgB.y;
+                if (COUNTS) {
+                    c_visit += (actA ? 1 : 0) + (actB ? 1 : 0);
+                    c_eval += (passA ? 1 : 0) + (passB ? 1 : 0);
+                    c_member += (passA ? M - pA : 0) + (passB ? M - pB : 0);
+                }
+                if (!(passA || passB)) {
+                    if (emp) break;
+                    continue;
+                }
+                const double invA = (jA < kInvCache) ? s.inv[jA] : 1.0 / feA;
+                const double invB = (jB < kInvCache) ? s.inv[jB] : 1.0 / feB;
+                const double teA = pqA.x * invA, teB = pqB.x * invB;
+                double EA = 0.0, EB = 0.0;
+                if (uni) {
+                    // Uniform users (same R, zeta, f_min, f_max, kappa, p_u; Table I): every member
+                    // has the same budget, f* and offloader term, so D20/D21 are formed once and
+                    // only the user-order sum runs over M.  Same operations, same bits.
+                    const double2 a0 = s.orzv[0], c0 = s.kuup[0], t0 = s.fmm[0];
+                    const double budA = (lgA.x - a0.x) - teA, budB = (lgB.x - a0.x) - teB;
+                    double fA = t0.x, fB = t0.x;
+                    if (passA && !(__fma_rn(t0.x, budA, -a0.y) > 0.0) && a0.y != 0.0)
+                        fA = clampf(a0.y / budA, t0.x, t0.y);  // D20 (R9 when zv = 0)
+                    if (passB && !(__fma_rn(t0.x, budB, -a0.y) > 0.0) && a0.y != 0.0)
+                        fB = clampf(a0.y / budB, t0.x, t0.y);
+                    const double emA = ((c0.x * fA) * fA) + c0.y;  // D21 offloader term
+                    const double emB = ((c0.x * fB) * fB) + c0.y;
+#pragma unroll 4
+                    for (int m = 0; m < M; m++) {
+                        const double2 et = s.et[m];  // eloc, thu
+                        EA = EA + ((!(feA < et.y)) ? emA : et.x);
+                        EB = EB + ((!(feB < et.y)) ? emB : et.x);
+                    }
+                } else {
+                    const long long fbA = __double_as_longlong(feA), fbB = __double_as_longlong(feB);
+#pragma unroll 2
+                    for (int m = 0; m < M; m++) {
+                        const double2 a = s.orzv[m];  // OR, zv
+                        const double2 c = s.kuup[m];  // ku, up
+                        const double2 d = s.et[m];    // eloc, thu
+                        const double2 t = s.fmm[m];   // fmin, fmax
+                        // f_e, th >= 0 (or +inf): IEEE order = integer order of the bit patterns
+                        const long long thb = __double_as_longlong(d.y);
+                        const bool memA = fbA >= thb, memB = fbB >= thb;
+                        const double budA = (lgA.x - a.x) - teA, budB = (lgB.x - a.x) - teB;
+                        double fA = t.x, fB = t.x;  // f_min unless f_min budget > zv fails exactly
+                        const bool needA = passA && memA && !(__fma_rn(t.x, budA, -a.y) > 0.0);
+                        const bool needB = passB && memB && !(__fma_rn(t.x, budB, -a.y) > 0.0);
+                        if (needA || needB) {
+                            // R9 (zv = 0 -> f_min) tested on the bits, inside the rare branch
+                            const bool nz = (__double_as_longlong(a.y) << 1) != 0;
+                            if (needA && nz) fA = clampf(a.y / budA, t.x, t.y);  // D20
+                            if (needB && nz) fB = clampf(a.y / budB, t.x, t.y);
+                        }
+                        const double emA = ((c.x * fA) * fA) + c.y;  // D21 offloader term
+                        const double emB = ((c.x * fB) * fB) + c.y;
+                        EA = EA + (memA ? emA : d.x);
+                        EB = EB + (memB ? emB : d.x);
+                    }
+                }
+                EA = EA + (pqA.y * feA) * feA;
+                EB = EB + (pqB.y * feB) * feB;
+                if (passA && EA < bE) {  // strict: lane keys ascend in (n~, j)
+                    bE = EA;
+                    bN = nt;
+                    bJ = (int)jA;
+                    bP = pA;
+                }
+                if (passB && EB < bE) {
+                    bE = EB;
+                    bN = nt;
+                    bJ = (int)jB;
+                    bP = pB;
+                }
+                if (emp) break;
+            }
+            if (prune) {  // warp minimum of the lane bests (identical in every lane)
+                double w = bE;
 #pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) {
-        const double oE = __shfl_xor_sync(0xffffffffu, bE, d);
-        const int oN = __shfl_xor_sync(0xffffffffu, bN, d);
-        const int oJ = __shfl_xor_sync(0xffffffffu, bJ, d);
-        const int oP = __shfl_xor_sync(0xffffffffu, bP, d);
-        const bool take = (oE < bE) || (oE == bE && (oN < bN || (oN == bN && oJ < bJ)));
-        if (take) {
-            bE = oE;
-            bN = oN;
-            bJ = oJ;
-            bP = oP;
+                for (int d = 16; d >= 1; d >>= 1) {
+                    const double o = __shfl_xor_sync(0xffffffffu, w, d);
+                    w = (o < w) ? o : w;
+                }
+                bEw = (w < bEw) ? w : bEw;
+            }
+            __syncwarp();
         }
+        // warp argmin over (E, n~, j)
+#pragma unroll
+        for (int d = 16; d >= 1; d >>= 1) {
+            const double oE = __shfl_xor_sync(0xffffffffu, bE, d);
+            const int oN = __shfl_xor_sync(0xffffffffu, bN, d);
+            const int oJ = __shfl_xor_sync(0xffffffffu, bJ, d);
+            const int oP = __shfl_xor_sync(0xffffffffu, bP, d);
+            const bool take = (oE < bE) || (oE == bE && (oN < bN || (oN == bN && oJ < bJ)));
+            if (take) {
+                bE = oE;
+                bN = oN;
+                bJ = oJ;
+                bP = oP;
+            }
+        }
+        if (!(pruned && bE == E_lc)) break;
     }
     if (COUNTS) {
 #pragma unroll
@@ -357,10 +439,16 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
             c_eval += __shfl_xor_sync(0xffffffffu, c_eval, d);
             c_member += __shfl_xor_sync(0xffffffffu, c_member, d);
         }
-        if (lane == 0) {
+        if (lane == 0 && !PRUNE) {
             r.counts[3 * i] = c_visit;
             r.counts[3 * i + 1] = c_eval;
             r.counts[3 * i + 2] = c_member;
+        }
+        if (lane == 0 && PRUNE) {
+            r.work[4 * i] = c_setup;
+            r.work[4 * i + 1] = c_visit;
+            r.work[4 * i + 2] = c_eval;
+            r.work[4 * i + 3] = c_member;
         }
     }
     const bool offload_wins = (bE < E_lc) || (bE == E_lc && (bN < aN || (bN == aN && bJ < aJ)));
@@ -369,7 +457,7 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
         return;
     }
     // winner: recompute D20 and D22 lane = user (same arithmetic as the sweep)
-    setup_nt(md, bN, M, homog, false, t_free, s, lane);  // per-user copies for the winner
+    if (bN != last_nt) setup_nt(md, bN, M, homog, uni, t_free, s, lane);
     const int Bo = M - bP;
     const double lo_ = s.Lg[bP].x;
     const double fe = grid_fe(fe_max, rho, bJ);
@@ -378,7 +466,7 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
     const bool member = (lane < M) && (s.rank[lane] >= bP);
     double f = floc, arr = t_free;
     if (member) {
-        const double2 a = s.orzv[lane], t = s.fmm[lane];  // (O/R, zv), (f_min, f_max)
+        const double2 a = s.orzv[uni ? 0 : lane], t = s.fmm[lane];  // (O/R, zv), (f_min, f_max)
         const double budget = (lo_ - a.x) - te;
         const bool low = (a.y == 0.0) || (__fma_rn(t.x, budget, -a.y) > 0.0);
         f = low ? t.x : clampf(a.y / budget, t.x, t.y);
@@ -409,7 +497,7 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
 #define JDOB_SOLVE_MINB 5
 #endif
 
-template <bool COUNTS>
+template <bool COUNTS, bool PRUNE>
 __global__ void __launch_bounds__(kSolveWarps * 32, JDOB_SOLVE_MINB)
     k_solve(const DevModel *models, DevBatch b, DevResult r, int mode) {
     __shared__ SolveSmem smem[kSolveWarps];
@@ -417,21 +505,27 @@ __global__ void __launch_bounds__(kSolveWarps * 32, JDOB_SOLVE_MINB)
     SolveSmem &s = smem[threadIdx.x >> 5];
     const long long gw = (long long)blockIdx.x * kSolveWarps + (threadIdx.x >> 5);
     const long long nw = (long long)gridDim.x * kSolveWarps;
-    for (long long i = gw; i < b.n_inst; i += nw) solve_instance<COUNTS>(i, models, b, r, mode, s, lane);
+    for (long long i = gw; i < b.n_inst; i += nw) solve_instance<COUNTS, PRUNE>(i, models, b, r, mode, s, lane);
+}
+
+template <bool COUNTS, bool PRUNE>
+static void launch_solve_t(const DevModel *models, const DevBatch &b, const DevResult &r, int mode, cudaStream_t s,
+                           int num_sms) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve<COUNTS, PRUNE>, kSolveWarps * 32, 0);
+    if (per_sm < 1) per_sm = 1;
+    const long long want = (b.n_inst + kSolveWarps - 1) / kSolveWarps;
+    long long grid = (long long)num_sms * per_sm;
+    if (want < grid) grid = want;
+    k_solve<COUNTS, PRUNE><<<(unsigned)grid, kSolveWarps * 32, 0, s>>>(models, b, r, mode);
 }
 
 void launch_solve(const DevModel *models, const DevBatch &b, const DevResult &r, int mode, cudaStream_t s,
                   int num_sms) {
     if (b.n_inst <= 0) return;
-    int per_sm = 0;
-    if (r.counts) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve<true>, kSolveWarps * 32, 0);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve<false>, kSolveWarps * 32, 0);
-    if (per_sm < 1) per_sm = 1;
-    const long long want = (b.n_inst + kSolveWarps - 1) / kSolveWarps;
-    long long grid = (long long)num_sms * per_sm;
-    if (want < grid) grid = want;
-    if (r.counts) k_solve<true><<<(unsigned)grid, kSolveWarps * 32, 0, s>>>(models, b, r, mode);
-    else k_solve<false><<<(unsigned)grid, kSolveWarps * 32, 0, s>>>(models, b, r, mode);
+    if (r.counts) launch_solve_t<true, false>(models, b, r, mode, s, num_sms);      // literal counters
+    else if (r.work) launch_solve_t<true, true>(models, b, r, mode, s, num_sms);    // executed counters
+    else launch_solve_t<false, true>(models, b, r, mode, s, num_sms);
 }
 
 }  // namespace jdob

@@ -180,6 +180,7 @@ __device__ void large_instance(long long i, const DevModel *models, const DevBat
             r.status[i] = st;
             r.mask[i] = 0u;
             if (r.counts) r.counts[3 * i] = r.counts[3 * i + 1] = r.counts[3 * i + 2] = 0;
+            if (r.work) r.work[4 * i] = r.work[4 * i + 1] = r.work[4 * i + 2] = r.work[4 * i + 3] = 0;
         }
         for (int m = tid; m < M; m += kLT) {
             if (r.f_user) r.f_user[off + m] = dnan();
@@ -215,6 +216,7 @@ __device__ void large_instance(long long i, const DevModel *models, const DevBat
             r.status[i] = st;
             r.mask[i] = 0u;
             if (r.counts && zero_counts) r.counts[3 * i] = r.counts[3 * i + 1] = r.counts[3 * i + 2] = 0;
+            if (r.work && zero_counts) r.work[4 * i] = r.work[4 * i + 1] = r.work[4 * i + 2] = r.work[4 * i + 3] = 0;
         }
         for (int m = tid; m < M; m += kLT) {
             const long long u = off + m;
@@ -355,10 +357,16 @@ __device__ void large_instance(long long i, const DevModel *models, const DevBat
         }
     }
     __syncthreads();
-    if (COUNTS && tid == 0) {
+    if (COUNTS && tid == 0 && r.counts) {
         r.counts[3 * i] = cscr[0];
         r.counts[3 * i + 1] = cscr[1];
         r.counts[3 * i + 2] = cscr[2];
+    }
+    if (COUNTS && tid == 0 && r.work) {  // no pruning on this path: executed = literal
+        r.work[4 * i] = (mode == JDOB_MODE_BINARY) ? 1 : N;
+        r.work[4 * i + 1] = cscr[0];
+        r.work[4 * i + 2] = cscr[1];
+        r.work[4 * i + 3] = cscr[2];
     }
     const bool offload_wins = (bE < E_lc) || (bE == E_lc && (bN < aN || (bN == aN && bJ < aJ)));
     if (!offload_wins) {
@@ -440,7 +448,7 @@ void launch_solve_large(const DevModel *models, const DevBatch &b, const DevResu
     const size_t smem = large_smem_bytes();
     long long grid = 2LL * num_sms;
     if (b.n_inst < grid) grid = b.n_inst;
-    if (r.counts) {
+    if (r.counts || r.work) {
         cudaFuncSetAttribute(k_solve_large<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         k_solve_large<true><<<(unsigned)grid, kLT, smem, s>>>(models, b, r, mode);
     } else {

@@ -19,12 +19,33 @@ def J():
     return J
 
 
+PRODUCT_FIELDS = ("E", "E_lc", "t_free_next", "f_e", "n_tilde", "j", "status", "mask", "f_user")
+
+
 def run(J, batch, mode=0, counts=True, stats=False, n_buckets=None):
+    """Solve on the GPU.  With counts, the literal (unpruned) sweep runs; the pruned product path
+    (no counters) and its executed-work variant run as well and must give the same bits."""
     db = J.DeviceBatch(batch)
     res = J.solve_batch(db, mode=mode, counts=counts, stats=stats, n_buckets=n_buckets)
     import torch
     torch.cuda.synchronize()
-    return db, to_np(res)
+    out = to_np(res)
+    if counts:
+        for kw in (dict(), dict(work=True)):
+            alt = to_np(J.solve_batch(db, mode=mode, stats=stats, n_buckets=n_buckets, **kw))
+            for f in PRODUCT_FIELDS + (("stats",) if stats else ()):
+                assert_bits_equal(alt[f], out[f], f"pruned vs literal {f} {kw}")
+            if kw:
+                check_work(batch, alt["work"], out["counts"], mode)
+    return db, out
+
+
+def check_work(batch, work, counts, mode):
+    """Executed work of the pruned sweep: at most the literal work (twice in the rare E = E_LC re-sweep)."""
+    N = np.array([batch.models[m].N for m in batch.model_id])
+    assert (work[:, 0] <= 2 * N).all()
+    assert (work[:, 1:] <= 2 * counts).all()
+    assert (work >= 0).all()
 
 
 @pytest.mark.parametrize("toy", ["toy-1", "toy-2", "toy-2-m1", "toy-2-tfree", "toy-4"])
@@ -364,6 +385,9 @@ def _large_parity(J, b, mode=0):
     for f in ("E", "E_lc", "t_free_next", "f_e", "n_tilde", "j", "status", "counts", "f_user"):
         assert_bits_equal(gpu[f].reshape(-1), orc[f].reshape(-1), "large " + f)
     assert_bits_equal(gpu["partition"], orc["part"], "large partition")
+    prod = to_np(J.solve_batch(db, mode=mode, partition=True))
+    for f in PRODUCT_FIELDS + ("partition",):
+        assert_bits_equal(prod[f], gpu[f], "large pruned " + f)
 
 
 @pytest.mark.parametrize("hetero,tfree", [(False, False), (True, True)])
