@@ -68,18 +68,18 @@ __device__ __forceinline__ double grid_fe(double fe_max, double rho, long long j
     return __dsub_rn(fe_max, __dmul_rn((double)j, rho));
 }
 
-// k = #{j >= 0 : f_e(j) >= f_e,min}; the predicate is monotone in j, so a binary
-// search over [0, kMaxK + 1] finds the first failing j exactly (equals the oracle's
-// literal walk).  Returns kMaxK + 1 when the grid is longer than kMaxK.
+// k = #{j >= 0 : f_e(j) >= f_e,min}; the predicate is monotone in j (RN(j rho) is
+// non-decreasing, so is the subtraction's complement), so k is its first failing j in
+// [0, kMaxK + 1].  Start from the estimate (f_e,max - f_e,min)/rho + 1 and step until
+// pred(k - 1) holds and pred(k) fails -- the same k as the oracle's literal walk.
+// Returns kMaxK + 1 when the grid is longer than kMaxK.
 __device__ __forceinline__ long long grid_k(double fe_min, double fe_max, double rho) {
-    long long lo = 0, hi = kMaxK + 1;  // answer in [lo, hi]
-    if (grid_fe(fe_max, rho, hi) >= fe_min) return kMaxK + 1;
-    while (lo < hi) {
-        long long mid = (lo + hi) >> 1;
-        if (grid_fe(fe_max, rho, mid) >= fe_min) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
+    if (grid_fe(fe_max, rho, kMaxK + 1) >= fe_min) return kMaxK + 1;
+    const double est = (fe_max - fe_min) / rho;
+    long long j = (est < 0.0) ? 0 : (est < (double)kMaxK ? (long long)est + 1 : kMaxK + 1);
+    while (j <= kMaxK && grid_fe(fe_max, rho, j) >= fe_min) j++;
+    while (j > 0 && !(grid_fe(fe_max, rho, j - 1) >= fe_min)) j--;
+    return j;
 }
 
 struct InstRegs {  // lane-resident user parameters (lane = user)
@@ -131,7 +131,10 @@ __device__ __forceinline__ int warp_validate(const DevModel *models, const DevBa
     k = grid_k(fe_min, fe_max, rho);
     if (k > kMaxK) return JDOB_ST_BADPARAM;
     const double vN = mdp->v[mdp->N];
-    const bool infeas = (lane < M) && ((x.z * vN) / x.f1 > x.T);
+    // P:127 literally RN(zeta v_N / f_max) > T; when T f_max - zeta v_N > 0 exactly (the fma's sign)
+    // the quotient is < T, so RN(.) <= T and the test fails without the division
+    const double zvN = x.z * vN;
+    const bool infeas = (lane < M) && !(__fma_rn(x.T, x.f1, -zvN) > 0.0) && (zvN / x.f1 > x.T);
     if (__any_sync(0xffffffffu, infeas)) return JDOB_ST_LOCAL_INFEASIBLE;
     double Tmin = x.T;
 #pragma unroll

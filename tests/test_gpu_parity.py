@@ -91,6 +91,24 @@ def test_random_uniform_users(J, seed, M_hi, N_hi, k_max):
     assert_solve_parity(gpu, orc, counts=True)
 
 
+@pytest.mark.parametrize("uniform", [False, True])
+def test_zero_energy_ties(J, uniform):
+    """kappa = p_u = 0 and c = 0: every configuration costs exactly E_LC = 0, so the answer is decided
+    by the (E, n~, j) tie rule against the first all-local evaluation (R8).  The pruned sweep skips
+    every n~ after the first (lb = 0 >= best = 0) and must fall back to the literal re-sweep."""
+    b = g.random_batch(seed=181, n_inst=800, M_lo=1, M_hi=32, N_lo=1, N_hi=12, k_max=50)
+    if uniform:
+        b = uniformise(b, 181)
+    b.kappa[:] = 0.0
+    b.p_u[:] = 0.0
+    for m in b.models:
+        m.c[:] = 0.0
+    _, gpu = run(J, b)
+    orc = O.solve_batch(b, counts=True)
+    assert_solve_parity(gpu, orc, counts=True)
+    assert (orc["E"][orc["status"] == 0] == 0.0).all()
+
+
 @pytest.mark.parametrize("mode", [1, 2, 3])
 def test_random_modes(J, mode):
     b = g.random_batch(seed=110 + mode, n_inst=800, M_lo=1, M_hi=16, N_lo=1, N_hi=8, k_max=64)

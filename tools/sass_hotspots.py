@@ -39,7 +39,8 @@ for l in lines[fn_start + 1:]:
         break
     m = re.search(r'line (\d+)', l)
     if "//##" in l and m:
-        cur_line = int(m.group(1))
+        mf = re.search(r'File "([^"]+)"', l)
+        cur_line = (os.path.basename(mf.group(1)) if mf else "?", int(m.group(1)))
     m2 = re.search(r'/\*([0-9a-f]{4,})\*/', l)
     if m2 and cur_line is not None:
         off2line[int(m2.group(1), 16)] = cur_line
@@ -47,13 +48,23 @@ ex = defaultdict(int)
 st = defaultdict(int)
 for r in data:
     off = int(r[iadr], 16) - base
-    ln = off2line.get(off, -1)
+    ln = off2line.get(off, ("?", -1))
     ex[ln] += int(r[iex] or 0)
     st[ln] += int(r[ist] or 0)
 te, ts = sum(ex.values()), sum(st.values())
-src = open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_2504_14611_b200", "csrc",
-                        sys.argv[5] if len(sys.argv) > 5 else "solve.cu")).read().splitlines()
+csrc = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_2504_14611_b200", "csrc")
+srcs = {}
+
+
+def code_of(f, n):
+    if f not in srcs:
+        pth = os.path.join(csrc, f)
+        srcs[f] = open(pth).read().splitlines() if os.path.exists(pth) else []
+    L = srcs[f]
+    return L[n - 1].strip()[:64] if 0 < n <= len(L) else "?"
+
+
 print(f"total warp instructions {te:.4e}, stall samples {ts}")
 for ln, s in sorted(st.items(), key=lambda x: -x[1])[:top]:
-    code = src[ln - 1].strip()[:70] if 0 < ln <= len(src) else "?"
-    print(f"line {ln:4d}  stall {100*s/ts:5.1f}%  instr {100*ex[ln]/te:5.1f}%  {code}")
+    f, n = ln
+    print(f"{f[:16]:>16}:{n:<5d} stall {100*s/ts:5.1f}%  instr {100*ex[ln]/te:5.1f}%  {code_of(f, n)}")
