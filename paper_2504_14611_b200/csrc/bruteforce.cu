@@ -16,6 +16,11 @@
 namespace jdob {
 
 constexpr int kInvTab = 2048;  // 1/f_e(j) cached in shared memory for j < kInvTab
+constexpr int kBfThreads = kBfWarps * 32;
+
+#ifndef JDOB_BF_PRUNE
+#define JDOB_BF_PRUNE 1
+#endif
 
 // setup output, in the workspace
 struct BfHeader {
@@ -23,6 +28,7 @@ struct BfHeader {
     long long k;
     unsigned long long size;   // index-space size (0 when too big)
     double t_free, fe_max, rho;
+    unsigned long long best_bits;  // incumbent energy (bits of a double >= 0), shared by every block
 };
 
 __global__ void k_bf_setup(const DevModel *models, DevBatch b, int space, BfHeader *hdr, double *tab /*[4][N+1][M]*/,
@@ -47,6 +53,7 @@ __global__ void k_bf_setup(const DevModel *models, DevBatch b, int space, BfHead
         hdr->t_free = b.t_free[0];
         hdr->fe_max = b.fe_max[0];
         hdr->rho = b.rho[0];
+        hdr->best_bits = (unsigned long long)__double_as_longlong(dinf());
     }
     if (st != JDOB_ST_OK && st != JDOB_ST_REQUIRE) return;
     const DevModel &md = *mdp;
@@ -100,7 +107,7 @@ template <int MAXM>
 #endif
 __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const DevModel *models, int model_id, int space,
                                                            unsigned long long idx_begin, unsigned long long idx_end,
-                                                           const BfHeader *hdr, const double *tab,
+                                                           BfHeader *hdr, const double *tab,
                                                            const double *user, const double *invtab,
                                                            double *part_E, long long *part_idx) {
     extern __shared__ double sm[];
@@ -120,6 +127,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
         double *sOR = sm, *sZV = sm + NM, *sKU = sm + 2 * NM, *sUP = sm + 3 * NM;
         double *sEl = sm + 4 * NM, *sFmin = sEl + 32, *sFmax = sEl + 64, *sT = sEl + 96;
         double *sInv = sEl + 128;
+        double *sSuf = sInv + kInvTab;  // [17][kBfThreads] per-lane suffix sums (N <= 15 path)
         const long long kt = k < kInvTab ? k : kInvTab;
         for (int x = threadIdx.x; x < 4 * NM; x += blockDim.x) sm[x] = tab[x];
         for (int x = threadIdx.x; x < 128; x += blockDim.x) sEl[x] = user[x];
@@ -134,22 +142,44 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
             const unsigned long long gw = (unsigned long long)blockIdx.x * kBfWarps + w;
             const unsigned long long nw = (unsigned long long)gridDim.x * kBfWarps;
             const double *dA = md.dA, *cA = md.cA;
-            const unsigned long long radix = (unsigned long long)(N + 1);
-            for (unsigned long long c = gw; c < nchunks; c += nw) {
+            const int radix = N + 1;
+            // General space: the lane's vector advances by 32 nw per step, so its digits are kept and
+            // advanced by a mixed-radix add of the stride's digits (64-bit division only twice, here)
+            int dig[MAXM], sdig[MAXM];
+            {
+                unsigned long long t = vb + gw * 32 + lane, u = 32ull * nw;
+#pragma unroll
+                for (int m = MAXM - 1; m >= 0; m--) {
+                    dig[m] = 0;
+                    sdig[m] = 0;
+                    if (m < M && space == 0) {
+                        dig[m] = (int)(t % (unsigned long long)radix);
+                        t /= (unsigned long long)radix;
+                        sdig[m] = (int)(u % (unsigned long long)radix);
+                        u /= (unsigned long long)radix;
+                    }
+                }
+            }
+            auto advance = [&]() {  // dig += sdig (mod radix^M)
+                if (space != 0) return;
+                int carry = 0;
+#pragma unroll
+                for (int m = MAXM - 1; m >= 0; m--) {
+                    if (m < M) {
+                        const int d = dig[m] + sdig[m] + carry;
+                        carry = d >= radix ? 1 : 0;
+                        dig[m] = carry ? d - radix : d;
+                    }
+                }
+            };
+            for (unsigned long long c = gw; c < nchunks; c += nw, advance()) {
                 const unsigned long long vec = vb + c * 32 + lane;
                 if (vec >= ve) continue;
-                // decode the partition vector
+                // the partition vector
                 int nv[MAXM];
                 if (space == 0) {
-                    unsigned long long t = vec;
 #pragma unroll
-                    for (int m = MAXM - 1; m >= 0; m--) {
-                        if (m < M) {
-                            nv[m] = (int)(t % radix);
-                            t /= radix;
-                        }
-                    }
-                    // (the loop walks m = M-1 .. 0 because m >= M entries are skipped)
+                    for (int m = 0; m < MAXM; m++) nv[m] = dig[m];
                 } else {
                     const unsigned long long mask = vec & ((1ull << M) - 1ull);
                     const int nt = (int)(vec >> M);
@@ -171,21 +201,44 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                         if (T < l_o) l_o = T;
                     }
                 }
-                for (int n = N; n >= 1; n--) {
-                    int bn = 0;
+                if (M <= 15 && N <= 15) {
+                    // digit histogram in 4-bit fields: b_n = M - #{m : n_m >= n}, accumulated while n
+                    // descends; S_n kept per lane in shared memory and read back at n_m + 1
+                    unsigned long long hist = 0ull;
 #pragma unroll
-                    for (int m = 0; m < MAXM; m++) bn += (m < M && nv[m] < n) ? 1 : 0;
-                    if (bn > 0) {
-                        S = S + dA[n * B1 + bn];
-                        Psi = Psi + cA[n * B1 + bn];
-                    } else {
-                        S = S + 0.0;
-                        Psi = Psi + 0.0;
+                    for (int m = 0; m < MAXM; m++)
+                        if (m < M) hist += 1ull << (4 * nv[m]);
+                    double *Sa = sSuf + threadIdx.x;
+                    Sa[(N + 1) * kBfThreads] = 0.0;
+                    int ge = 0;
+                    for (int n = N; n >= 1; n--) {
+                        ge += (int)((hist >> (4 * n)) & 0xfull);
+                        const int bn = M - ge;
+                        S = S + ((bn > 0) ? dA[n * B1 + bn] : 0.0);
+                        Psi = Psi + ((bn > 0) ? cA[n * B1 + bn] : 0.0);
+                        Sa[n * kBfThreads] = S;
                     }
 #pragma unroll
                     for (int m = 0; m < MAXM; m++)
-                        if (m < M && nv[m] + 1 == n) Sm[m] = S;
-                    if (nmin + 1 == n) Smin = S;
+                        if (m < M) Sm[m] = Sa[(nv[m] + 1) * kBfThreads];
+                    Smin = Sa[(nmin + 1) * kBfThreads];
+                } else {
+                    for (int n = N; n >= 1; n--) {
+                        int bn = 0;
+#pragma unroll
+                        for (int m = 0; m < MAXM; m++) bn += (m < M && nv[m] < n) ? 1 : 0;
+                        if (bn > 0) {
+                            S = S + dA[n * B1 + bn];
+                            Psi = Psi + cA[n * B1 + bn];
+                        } else {
+                            S = S + 0.0;
+                            Psi = Psi + 0.0;
+                        }
+#pragma unroll
+                        for (int m = 0; m < MAXM; m++)
+                            if (m < M && nv[m] + 1 == n) Sm[m] = S;
+                        if (nmin + 1 == n) Smin = S;
+                    }
                 }
                 const bool any = nmin < N;
                 // per-vector hoists: REG (M <= 8) keeps l_o - O/R, zeta v, kappa u, (O/R) p per user in
@@ -208,6 +261,54 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                 }
                 const unsigned long long jlo = (vec == vb) ? idx_begin - vb * uk : 0ull;
                 const unsigned long long jhi = (vec == ve - 1) ? idx_end - (ve - 1) * uk : uk;
+#if JDOB_BF_PRUNE
+                // Vector bound (exact, DESIGN.md §4 "brute-force bound").  Every candidate the literal
+                // scan evaluates passes D6': RN(t_free + RN(Smin RN(1/f_e))) <= l_o, which implies
+                // f_e >= Smin / ((l_o (1 + u) - t_free)(1 + u)(1 + 2u)) (u = 2^-53) >= fl, computed
+                // below with directed rounding; f_e >= f_e(jhi - 1) as well.  Each offloader term is
+                // >= its f_min value, a local term is e_loc, and RN is monotone, so
+                //   E(j) >= RN(RN-sum_m(term lower bounds) + (Psi fl) fl) = LB.
+                // The vector is skipped when LB >= this lane's best (its candidates have larger
+                // indices, so an equal E cannot win) or LB > the incumbent shared by all blocks.
+                {
+                    double fel = grid_fe(fe_max, rho, (long long)(jhi - 1));
+                    if (any) {
+                        const double fe0 = grid_fe(fe_max, rho, (long long)jlo);
+                        const double inv0 = (jlo < (unsigned long long)kt) ? sInv[jlo] : 1.0 / fe0;
+                        if (!(t_free + Smin * inv0 <= l_o)) continue;  // D6' fails at once: no candidate
+                        const double X = __dmul_ru(__dadd_ru(__dmul_ru(l_o, 0x1.0000000000001p+0), -t_free),
+                                                   0x1.0000000000004p+0);
+                        const double fd = __ddiv_rd(Smin, X);
+                        fel = (fd > fel) ? fd : fel;
+                    }
+                    double lbu = 0.0;
+#pragma unroll
+                    for (int m = 0; m < MAXM; m++) {
+                        if (m < M) {
+                            double t;
+                            if ((offm >> m) & 1u) {
+                                double ku, up;
+                                if constexpr (REG) {
+                                    ku = kur[m];
+                                    up = upr[m];
+                                } else {
+                                    const int x = nv[m] * M + m;
+                                    ku = sKU[x];
+                                    up = sUP[x];
+                                }
+                                t = ((ku * sFmin[m]) * sFmin[m]) + up;
+                            } else {
+                                t = sEl[m];
+                            }
+                            lbu = lbu + t;
+                        }
+                    }
+                    const double LB = lbu + (Psi * fel) * fel;
+                    const double inc = __longlong_as_double(*(volatile long long *)&hdr->best_bits);
+                    if (LB >= bestE || LB > inc) continue;
+                }
+                const double best_before = bestE;
+#endif
                 if constexpr (REG) {
                     // M <= 8: (A) budgets and the exact low-clamp test for every offloader, no
                     // branches; (B) the rare literal divisions / feasibility checks; (C) the energies
@@ -321,6 +422,10 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                         }
                 }
                 }
+#if JDOB_BF_PRUNE
+                if (bestE < best_before)  // publish the lane's new best as the shared incumbent
+                    atomicMin(&hdr->best_bits, (unsigned long long)__double_as_longlong(bestE));
+#endif
             }
         }
     }
@@ -377,7 +482,7 @@ size_t bf_workspace_bytes() {
 
 template <int MAXM>
 static void launch_main(const DevModel *models, int model_id, int space, unsigned long long ib, unsigned long long ie,
-                        const BfHeader *hdr, const double *tab, const double *user, const double *inv,
+                        BfHeader *hdr, const double *tab, const double *user, const double *inv,
                         double *part_E, long long *part_idx, size_t smem, cudaStream_t s) {
     cudaFuncSetAttribute(k_bf_main<MAXM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_bf_main<MAXM><<<kBfBlocks, kBfWarps * 32, smem, s>>>(models, model_id, space, ib, ie, hdr, tab, user, inv,
@@ -401,7 +506,7 @@ void launch_bruteforce_impl(const DevModel *models, const DevBatch &b, int model
     long long *part_idx = (long long *)p;
     k_bf_setup<<<1, 32, 0, s>>>(models, b, space, hdr, tab, user, inv);
     const int Mc = (M >= 1 && M <= kMaxM) ? M : 1;
-    const size_t smem = sizeof(double) * (4 * (size_t)(N + 1) * Mc + 128 + kInvTab);
+    const size_t smem = sizeof(double) * (4 * (size_t)(N + 1) * Mc + 128 + kInvTab + 17 * kBfThreads);
     if (Mc <= 8)
         launch_main<8>(models, model_id, space, idx_begin, idx_end, hdr, tab, user, inv, part_E, part_idx, smem, s);
     else if (Mc <= 16)

@@ -294,6 +294,29 @@ def test_bf_random_full_and_ranges(J):
                 assert int(I.item()) == Io
 
 
+def test_bf_zero_energy_ties(J):
+    """kappa = p_u = c = 0: every feasible candidate has E = 0, so the answer is the lowest feasible
+    index -- the vector bound (LB = 0 >= best = 0) must never drop a lower-index tie."""
+    b = g.random_batch(seed=151, n_inst=30, M_lo=1, M_hi=6, N_lo=1, N_hi=5, k_max=24, tfree_frac=0.4)
+    b.kappa[:] = 0.0
+    b.p_u[:] = 0.0
+    for m in b.models:
+        m.c[:] = 0.0
+    rng = np.random.default_rng(1)
+    for i in range(b.n_inst):
+        bi = b.subset(i, i + 1)
+        db = J.DeviceBatch(bi)
+        for space in (0, 1):
+            size = O.bf_space_size(bi, space)
+            lo = int(rng.integers(0, max(size // 2, 1)))
+            for a, c in ((0, size), (lo, size)):
+                E, I, S = J.bruteforce(db, space, a, c)
+                Eo, Io, So = O.bf(bi, space, a, c)
+                assert int(S.item()) == So
+                assert_bits_equal(E.cpu().numpy(), np.array([Eo]), f"E {i} {space} {a}")
+                assert int(I.item()) == Io
+
+
 def test_bf_larger_M(J):
     # M in 9..16 and 17..32 exercise the other kernel specialisations (small N keeps spaces small)
     for seed, M_lo, M_hi, N_hi in ((151, 9, 12, 1), (152, 17, 20, 1)):
