@@ -166,9 +166,13 @@ __device__ __forceinline__ void write_local(const DevResult &r, long long i, lon
 // the best energy found so far (exact, DESIGN.md §4 "n~ pruning").  <true, false> = literal Alg. 2
 // counters (r.counts), <true, true> = executed-work counters of the pruned sweep (r.work),
 // <false, true> = the product path.
-template <bool COUNTS, bool PRUNE>
+// UNI: the instance class this kernel solves.  true = uniform users (Table I; the other instances
+// are marked kStDefer), false = the rest (only instances marked kStDefer by the first kernel).
+// Two specialised kernels keep each one's code, and so its instruction-cache footprint, small.
+template <bool COUNTS, bool PRUNE, bool UNI>
 __device__ __forceinline__ void solve_instance(long long i, const DevModel *models, const DevBatch &b,
                                                const DevResult &r, int mode, SolveSmem &s, int lane) {
+    if (!UNI && r.status[i] != kStDefer) return;  // solved by the uniform-users kernel
     __syncwarp();
     long long off, k;
     int M;
@@ -222,10 +226,15 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
     const double R0 = __shfl_sync(0xffffffffu, x.R, 0), z0 = __shfl_sync(0xffffffffu, x.z, 0);
     const double f10 = __shfl_sync(0xffffffffu, x.f1, 0);
     auto sb = [](double a, double c) { return __double_as_longlong(a) == __double_as_longlong(c); };
-    const bool homog = __all_sync(0xffffffffu, lane >= M || (sb(x.R, R0) && sb(x.z, z0) && sb(x.f1, f10)));
+    const bool homog_ = __all_sync(0xffffffffu, lane >= M || (sb(x.R, R0) && sb(x.z, z0) && sb(x.f1, f10)));
     const double f00 = __shfl_sync(0xffffffffu, x.f0, 0), k0 = __shfl_sync(0xffffffffu, x.k, 0);
     const double p0 = __shfl_sync(0xffffffffu, x.p, 0);
-    const bool uni = homog && __all_sync(0xffffffffu, lane >= M || (sb(x.f0, f00) && sb(x.k, k0) && sb(x.p, p0)));
+    const bool uni_ = homog_ && __all_sync(0xffffffffu, lane >= M || (sb(x.f0, f00) && sb(x.k, k0) && sb(x.p, p0)));
+    if (UNI && !uni_) {  // left to the general kernel
+        if (lane == 0) r.status[i] = kStDefer;
+        return;
+    }
+    const bool homog = UNI ? true : homog_, uni = UNI ? true : uni_;
     const double T0 = __shfl_sync(0xffffffffu, x.T, 0);
     if (homog && __all_sync(0xffffffffu, lane >= M || x.T == T0)) {
         // equal gamma and equal deadlines (Table I identical-deadline setting): the key (T asc,
@@ -509,7 +518,7 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
 #define JDOB_SOLVE_MINB 5
 #endif
 
-template <bool COUNTS, bool PRUNE>
+template <bool COUNTS, bool PRUNE, bool UNI>
 __global__ void __launch_bounds__(kSolveWarps * 32, JDOB_SOLVE_MINB)
     k_solve(const DevModel *models, DevBatch b, DevResult r, int mode) {
     __shared__ SolveSmem smem[kSolveWarps];
@@ -522,27 +531,34 @@ __global__ void __launch_bounds__(kSolveWarps * 32, JDOB_SOLVE_MINB)
     __syncwarp();
     const long long gw = (long long)blockIdx.x * kSolveWarps + (threadIdx.x >> 5);
     const long long nw = (long long)gridDim.x * kSolveWarps;
-    for (long long i = gw; i < b.n_inst; i += nw) solve_instance<COUNTS, PRUNE>(i, models, b, r, mode, s, lane);
+    for (long long i = gw; i < b.n_inst; i += nw) solve_instance<COUNTS, PRUNE, UNI>(i, models, b, r, mode, s, lane);
 }
 
-template <bool COUNTS, bool PRUNE>
+template <bool COUNTS, bool PRUNE, bool UNI>
 static void launch_solve_t(const DevModel *models, const DevBatch &b, const DevResult &r, int mode, cudaStream_t s,
                            int num_sms) {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve<COUNTS, PRUNE>, kSolveWarps * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve<COUNTS, PRUNE, UNI>, kSolveWarps * 32, 0);
     if (per_sm < 1) per_sm = 1;
     const long long want = (b.n_inst + kSolveWarps - 1) / kSolveWarps;
     long long grid = (long long)num_sms * per_sm;
     if (want < grid) grid = want;
-    k_solve<COUNTS, PRUNE><<<(unsigned)grid, kSolveWarps * 32, 0, s>>>(models, b, r, mode);
+    k_solve<COUNTS, PRUNE, UNI><<<(unsigned)grid, kSolveWarps * 32, 0, s>>>(models, b, r, mode);
+}
+
+template <bool COUNTS, bool PRUNE>
+static void launch_pair(const DevModel *models, const DevBatch &b, const DevResult &r, int mode, cudaStream_t s,
+                        int num_sms) {
+    launch_solve_t<COUNTS, PRUNE, true>(models, b, r, mode, s, num_sms);   // uniform users; marks the rest
+    launch_solve_t<COUNTS, PRUNE, false>(models, b, r, mode, s, num_sms);  // the rest
 }
 
 void launch_solve(const DevModel *models, const DevBatch &b, const DevResult &r, int mode, cudaStream_t s,
                   int num_sms) {
     if (b.n_inst <= 0) return;
-    if (r.counts) launch_solve_t<true, false>(models, b, r, mode, s, num_sms);      // literal counters
-    else if (r.work) launch_solve_t<true, true>(models, b, r, mode, s, num_sms);    // executed counters
-    else launch_solve_t<false, true>(models, b, r, mode, s, num_sms);
+    if (r.counts) launch_pair<true, false>(models, b, r, mode, s, num_sms);      // literal counters
+    else if (r.work) launch_pair<true, true>(models, b, r, mode, s, num_sms);    // executed counters
+    else launch_pair<false, true>(models, b, r, mode, s, num_sms);
 }
 
 }  // namespace jdob
