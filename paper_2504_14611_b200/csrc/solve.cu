@@ -172,7 +172,6 @@ __device__ __forceinline__ void write_local(const DevResult &r, long long i, lon
 template <bool COUNTS, bool PRUNE, bool UNI>
 __device__ __forceinline__ void solve_instance(long long i, const DevModel *models, const DevBatch &b,
                                                const DevResult &r, int mode, SolveSmem &s, int lane) {
-    if (!UNI && r.status[i] != kStDefer) return;  // solved by the uniform-users kernel
     __syncwarp();
     long long off, k;
     int M;
@@ -518,8 +517,12 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
 #define JDOB_SOLVE_MINB 5
 #endif
 
+#ifndef JDOB_SOLVE_MINB_U
+#define JDOB_SOLVE_MINB_U 6
+#endif
+
 template <bool COUNTS, bool PRUNE, bool UNI>
-__global__ void __launch_bounds__(kSolveWarps * 32, JDOB_SOLVE_MINB)
+__global__ void __launch_bounds__(kSolveWarps * 32, UNI ? JDOB_SOLVE_MINB_U : JDOB_SOLVE_MINB)
     k_solve(const DevModel *models, DevBatch b, DevResult r, int mode) {
     __shared__ SolveSmem smem[kSolveWarps];
     const int lane = threadIdx.x & 31;
@@ -531,7 +534,20 @@ __global__ void __launch_bounds__(kSolveWarps * 32, JDOB_SOLVE_MINB)
     __syncwarp();
     const long long gw = (long long)blockIdx.x * kSolveWarps + (threadIdx.x >> 5);
     const long long nw = (long long)gridDim.x * kSolveWarps;
-    for (long long i = gw; i < b.n_inst; i += nw) solve_instance<COUNTS, PRUNE, UNI>(i, models, b, r, mode, s, lane);
+    if (UNI) {
+        for (long long i = gw; i < b.n_inst; i += nw) solve_instance<COUNTS, PRUNE, UNI>(i, models, b, r, mode, s, lane);
+    } else {
+        // only the instances the uniform-users kernel left (kStDefer): 32 statuses per coalesced read
+        for (long long base = gw * 32; base < b.n_inst; base += nw * 32) {
+            const long long ii = base + lane;
+            unsigned def = __ballot_sync(0xffffffffu, ii < b.n_inst && r.status[ii] == kStDefer);
+            while (def) {
+                const int q = __ffs(def) - 1;
+                def &= def - 1u;
+                solve_instance<COUNTS, PRUNE, UNI>(base + q, models, b, r, mode, s, lane);
+            }
+        }
+    }
 }
 
 template <bool COUNTS, bool PRUNE, bool UNI>
