@@ -255,20 +255,35 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
         // ((kappa u) f*) f* + (O/R) p >= ((kappa u) f_min) f_min + RN(RD(O RD(1/R)) p) (f* >= f_min, RN
         // monotone), a non-member's term is e_loc, so each term >= the min of the two; the user-order
         // RN sum of the minima is <= the sum of the terms, and the edge term (psi f_e) f_e >= 0.
-        if (lane < M) s.rinv[lane] = __ddiv_rd(1.0, x.R);
-        __syncwarp();
-        for (int nt = lane; nt < N; nt += 32) {
-            const double u_nt = md.u[nt], O_nt = md.O[nt];
-            double S = 0.0;
-            for (int m = 0; m < M; m++) {
-                const double ku = s.kap[m] * u_nt;
-                const double up = __dmul_rd(O_nt, s.rinv[m]) * s.pu[m];
-                const double fm = s.fmm[m].x;
-                const double em = ((ku * fm) * fm) + up;
-                const double el = s.et[m].x;
-                S = S + ((em < el) ? em : el);
+        if (UNI) {  // every user has user 0's kappa, f_min, p_u and R: one bound term per n~
+            const double rinv0 = __ddiv_rd(1.0, x.R), k0_ = x.k, fm0 = x.f0, pu0 = x.p;  // lane 0's values
+            const double rv = __shfl_sync(0xffffffffu, rinv0, 0), kv = __shfl_sync(0xffffffffu, k0_, 0);
+            const double fv = __shfl_sync(0xffffffffu, fm0, 0), pv = __shfl_sync(0xffffffffu, pu0, 0);
+            for (int nt = lane; nt < N; nt += 32) {
+                const double em = (((kv * md.u[nt]) * fv) * fv) + __dmul_rd(md.O[nt], rv) * pv;
+                double S = 0.0;
+                for (int m = 0; m < M; m++) {
+                    const double el = s.et[m].x;
+                    S = S + ((em < el) ? em : el);
+                }
+                s.lb[nt] = S;
             }
-            s.lb[nt] = S;
+        } else {
+            if (lane < M) s.rinv[lane] = __ddiv_rd(1.0, x.R);
+            __syncwarp();
+            for (int nt = lane; nt < N; nt += 32) {
+                const double u_nt = md.u[nt], O_nt = md.O[nt];
+                double S = 0.0;
+                for (int m = 0; m < M; m++) {
+                    const double ku = s.kap[m] * u_nt;
+                    const double up = __dmul_rd(O_nt, s.rinv[m]) * s.pu[m];
+                    const double fm = s.fmm[m].x;
+                    const double em = ((ku * fm) * fm) + up;
+                    const double el = s.et[m].x;
+                    S = S + ((em < el) ? em : el);
+                }
+                s.lb[nt] = S;
+            }
         }
         __syncwarp();
     }
