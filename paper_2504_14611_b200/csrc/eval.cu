@@ -61,7 +61,9 @@ __global__ void k_eval(const DevModel *models, DevBatch b, const int *partition,
     double Tmin = dinf();
     for (int m = 0; m < M; m++) {
         double T = b.T[off + m];
-        if ((b.zeta[off + m] * vN) / b.f_max[off + m] > T && st == JDOB_ST_OK) st = JDOB_ST_LOCAL_INFEASIBLE;
+        // P:127 RN(zeta v_N / f_max) > T; the fma sign proves "no" without the division
+        const double zvN = b.zeta[off + m] * vN, f1 = b.f_max[off + m];
+        if (st == JDOB_ST_OK && !(__fma_rn(T, f1, -zvN) > 0.0) && zvN / f1 > T) st = JDOB_ST_LOCAL_INFEASIBLE;
         if (T < Tmin) Tmin = T;
     }
     if (st == JDOB_ST_OK && Tmin < t_free) st = JDOB_ST_REQUIRE;
@@ -133,11 +135,14 @@ __global__ void k_eval(const DevModel *models, DevBatch b, const int *partition,
             double zv = b.zeta[u] * md.v[nm];
             const double Sn = partition ? S[nm + 1] : S_plan;
             double budget = (l_o - OR) - Sn * inv;
+            const double f0 = b.f_min[u];
             if (zv == 0.0) {
                 if (budget < 0.0) viol |= 8u;
-                f = b.f_min[u];
+                f = f0;
+            } else if (__fma_rn(f0, budget, -zv) > 0.0) {
+                f = f0;  // f_min budget - zv > 0 exactly: budget > 0 and RN(zv / budget) <= f_min
             } else if (budget > 0.0) {
-                f = clampf(zv / budget, b.f_min[u], b.f_max[u]);
+                f = clampf(zv / budget, f0, b.f_max[u]);
             } else {
                 viol |= 8u;
                 f = b.f_max[u];
@@ -149,7 +154,8 @@ __global__ void k_eval(const DevModel *models, DevBatch b, const int *partition,
             if (fin > tf) tf = fin;
         } else {
             double T = b.T[u];
-            f = clampf((b.zeta[u] * vN) / T, b.f_min[u], b.f_max[u]);
+            const double zvN = b.zeta[u] * vN, f0 = b.f_min[u];
+            f = (__fma_rn(f0, T, -zvN) > 0.0) ? f0 : clampf(zvN / T, f0, b.f_max[u]);
             e = ((b.kappa[u] * uN) * f) * f;
             if ((b.zeta[u] * vN) / f > T + slack * fabs(T)) viol |= 4u;
         }

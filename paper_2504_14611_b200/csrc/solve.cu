@@ -213,7 +213,10 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
 
     const long long kk = (mode == JDOB_MODE_NO_EDGE_DVFS) ? 1 : k;
     const long long kc = kk < kInvCache ? kk : kInvCache;
-    if (!(fe_max == s.inv_key.x && rho == s.inv_key.y && kc <= s.inv_n)) {  // 1/f_e(j) cache per warp
+    // 1/f_e(j) cache per warp: the hit test is read by every lane before any lane rewrites it
+    const bool inv_hit = __all_sync(0xffffffffu, fe_max == s.inv_key.x && rho == s.inv_key.y && kc <= s.inv_n);
+    if (!inv_hit) {  // warp-uniform
+        __syncwarp();
         for (long long j = lane; j < kc; j += 32) s.inv[j] = 1.0 / grid_fe(fe_max, rho, j);
         if (lane == 0) {
             s.inv_key = make_double2(fe_max, rho);

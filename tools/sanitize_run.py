@@ -11,6 +11,8 @@ import paper_2504_14611_b200 as J  # noqa: E402
 b = G.random_batch(seed=5, n_inst=64, M_lo=1, M_hi=32, N_lo=1, N_hi=12, k_max=70, tfree_frac=0.4)
 db = J.DeviceBatch(b)
 res = J.solve_batch(db, counts=True, stats=True, n_buckets=32)
+J.solve_batch(db, stats=True, n_buckets=32)          # pruned product path
+J.solve_batch(db, work=True, partition=True)         # executed-work counters
 J.eval_plans(db, plans=res)
 J.eval_plans(db, J.plan_partition(db, res), res["f_e"])
 J.solve_grouped(J.DeviceBatch(b.subset(0, 16)))
@@ -22,6 +24,14 @@ J.bruteforce(dt, 0)
 J.bruteforce(dt, 1)
 small = G.random_batch(seed=9, n_inst=1, M_lo=9, M_hi=9, N_lo=1, N_hi=1, k_max=3)
 J.bruteforce(J.DeviceBatch(small), 0)
+J.solve_batch(J.DeviceBatch(c), work=True)
+big = G.concat([G.random_batch(seed=3, n_inst=8, M_lo=1, M_hi=32, N_lo=1, N_hi=8, k_max=40)])
+from tests.test_oracle_large import large_instance  # noqa: E402
+lb = G.concat([large_instance(40, 1), large_instance(70, 2, hetero=True)])
+J.solve_batch(J.DeviceBatch(lb), partition=True)
+J.solve_batch(J.DeviceBatch(lb), counts=True, partition=True)
+r5 = G.random_batch(seed=21, n_inst=1, M_lo=5, M_hi=5, N_lo=3, N_hi=3, k_max=20)
+J.bruteforce(J.DeviceBatch(r5), 0)
 hb = J.HostBuffers(c, stats=True, n_buckets=3)
 J.solve_batch_host(hb)
 torch.cuda.synchronize()
