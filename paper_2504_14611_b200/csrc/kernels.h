@@ -18,7 +18,6 @@ struct ModelChunk {
 // Launch geometry of the solve kernel (one warp per instance, persistent grid).
 constexpr int kSolveWarps = 4;
 constexpr int kStatsBlocks = 1184;   // fixed => deterministic statistics tree
-constexpr int kStatsWarps = 2;
 constexpr int kBfBlocks = 148 * 8;   // persistent brute-force grid
 constexpr int kBfWarps = 4;
 

@@ -1,9 +1,9 @@
 // K4: energy-saving statistics (row a12; "average energy consumption per user",
 // P:407; reduction vs LC; R16), bucketed, with a FIXED reduction tree:
-// warp w of the fixed grid owns the contiguous instance range [w n / W, (w+1) n / W),
-// accumulates it sequentially into warp-private shared memory (lane f owns fields
-// f, f+32, f+64 -> no atomics), warps of a block are combined in warp order, and a
-// final one-block kernel folds the per-block partials in block order.  Results are
+// block w of the fixed grid (one warp) owns the contiguous instance range
+// [w n / W, (w+1) n / W); each lane accumulates its fixed subsequence of it into
+// lane-private shared memory, the lanes are folded in lane order, and a final kernel
+// folds the per-block partials in a fixed tree.  Counts are exact integers.  Results are
 // therefore identical run to run for a given n_inst.
 #include "jdob_dev.cuh"
 #include "kernels.h"
@@ -23,79 +23,66 @@ __device__ __forceinline__ double combine(int f, double a, double b) {
     return a + b;
 }
 
-__global__ void __launch_bounds__(kStatsWarps * 32) k_stats_partial(DevBatch b, DevResult r, double *partials,
-                                                                      int n_buckets) {
-    extern __shared__ double acc[];  // [kStatsWarps][n_buckets][kStatsF]
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    double *my = acc + (size_t)w * n_buckets * kStatsF;
-    for (int x = lane; x < n_buckets * kStatsF; x += 32) my[x] = field_init(x % kStatsF);
-    __syncwarp();
-    const long long W = (long long)gridDim.x * kStatsWarps;
-    const long long gw = (long long)blockIdx.x * kStatsWarps + w;
-    const long long i0 = b.n_inst * gw / W, i1 = b.n_inst * (gw + 1) / W;
-    for (long long base = i0; base < i1; base += 32) {
-        const long long i = base + lane;
-        bool valid = i < i1;
-        int bk = -1, ok = 0, nt = 0, offl = 0;
-        double rr = 0.0, eM = 0.0, elM = 0.0;
-        if (valid) {
-            const int M = (int)(b.user_off[i + 1] - b.user_off[i]);
-            bk = b.bucket ? b.bucket[i] : ((M >= 1 && M <= kMaxM) ? M - 1 : 0);
-            if (bk < 0 || bk >= n_buckets) bk = -1;
-            ok = (r.status[i] == JDOB_ST_OK);
-            if (ok) {
-                const double E = r.E[i], El = r.E_lc[i];
-                rr = 100.0 * (El - E) / El;
-                eM = E / (double)M;
-                elM = El / (double)M;
-                nt = r.n_tilde[i];
-                offl = r.mask[i] != 0u;
-            }
-        }
-        const int cnt = (int)((i1 - base) < 32 ? (i1 - base) : 32);
-        for (int t = 0; t < cnt; t++) {
-            const int tb = __shfl_sync(0xffffffffu, bk, t);
-            const int tok = __shfl_sync(0xffffffffu, ok, t);
-            const double tr = __shfl_sync(0xffffffffu, rr, t);
-            const double te = __shfl_sync(0xffffffffu, eM, t);
-            const double tl = __shfl_sync(0xffffffffu, elM, t);
-            const int tn = __shfl_sync(0xffffffffu, nt, t);
-            const int to = __shfl_sync(0xffffffffu, offl, t);
-            if (tb < 0) continue;
-            double *a = my + (size_t)tb * kStatsF;
-            if (!tok) {
-                if (lane == 8) a[8] = a[8] + 1.0;
-                continue;
-            }
-#pragma unroll
-            for (int q = 0; q < 3; q++) {
-                const int f = lane + 32 * q;
-                if (f >= kStatsF) break;
-                double v;
-                switch (f) {
-                    case 0: v = 1.0; break;
-                    case 1: v = tr; break;
-                    case 2: v = tr * tr; break;
-                    case 3: v = tr; break;
-                    case 4: v = tr; break;
-                    case 5: v = te; break;
-                    case 6: v = tl; break;
-                    case 7: v = to ? 1.0 : 0.0; break;
-                    case 8: v = 0.0; break;
-                    default: v = (f - 9 == tn) ? 1.0 : 0.0; break;
-                }
-                if (f == 8 || (f >= 9 + 64)) continue;
-                a[f] = combine(f, a[f], v);
-            }
-        }
+// Field slots kept per lane in floating point: sum r, sum r^2, max r, min r, sum E/M, sum E_lc/M.
+constexpr int kLaneF = 6;
+__device__ __forceinline__ int lane_slot(int f) {  // field -> per-lane slot, -1 = integer counter
+    return (f == 1) ? 0 : (f == 2) ? 1 : (f == 3) ? 2 : (f == 4) ? 3 : (f == 5) ? 4 : (f == 6) ? 5 : -1;
+}
+
+// One warp per block.  Lane l of warp w owns the instances i0 + l, i0 + l + 32, ... of the warp's fixed
+// range and accumulates them IN THAT ORDER into its own shared-memory slots (no shuffles, no atomics on
+// floating point); integer counters use shared-memory integer atomics (exact, order-free).  The lanes
+// are then folded in lane order, so the result is identical run to run.
+__global__ void __launch_bounds__(32) k_stats_partial(DevBatch b, DevResult r, double *partials, int n_buckets) {
+    extern __shared__ double sh[];
+    double *fs = sh;                                                        // [n_buckets][kLaneF][32]
+    int *cnt = (int *)(sh + (size_t)n_buckets * kLaneF * 32);               // [n_buckets][kStatsF]
+    const int lane = threadIdx.x;
+    for (int x = lane; x < n_buckets * kLaneF * 32; x += 32) {
+        const int slot = (x / 32) % kLaneF;
+        fs[x] = (slot == 2) ? -dinf() : (slot == 3) ? dinf() : 0.0;
     }
-    __syncthreads();
-    // combine warps in order, write this block's partial
+    for (int x = lane; x < n_buckets * kStatsF; x += 32) cnt[x] = 0;
+    __syncwarp();
+    const long long W = gridDim.x;
+    const long long gw = blockIdx.x;
+    const long long i0 = b.n_inst * gw / W, i1 = b.n_inst * (gw + 1) / W;
+    for (long long i = i0 + lane; i < i1; i += 32) {
+        const int M = (int)(b.user_off[i + 1] - b.user_off[i]);
+        int bk = b.bucket ? b.bucket[i] : ((M >= 1 && M <= kMaxM) ? M - 1 : 0);
+        if (bk < 0 || bk >= n_buckets) continue;
+        int *c = cnt + bk * kStatsF;
+        if (r.status[i] != JDOB_ST_OK) {
+            atomicAdd(c + 8, 1);
+            continue;
+        }
+        const double E = r.E[i], El = r.E_lc[i];
+        const double rr = 100.0 * (El - E) / El;
+        double *a = fs + (size_t)bk * kLaneF * 32 + lane;
+        a[0 * 32] = a[0 * 32] + rr;
+        a[1 * 32] = a[1 * 32] + rr * rr;
+        a[2 * 32] = (rr > a[2 * 32]) ? rr : a[2 * 32];
+        a[3 * 32] = (rr < a[3 * 32]) ? rr : a[3 * 32];
+        a[4 * 32] = a[4 * 32] + E / (double)M;
+        a[5 * 32] = a[5 * 32] + El / (double)M;
+        atomicAdd(c + 0, 1);
+        if (r.mask[i] != 0u) atomicAdd(c + 7, 1);
+        const int nt = r.n_tilde[i];
+        if (nt >= 0 && nt < 64) atomicAdd(c + 9 + nt, 1);
+    }
+    __syncwarp();
     double *dst = partials + (size_t)blockIdx.x * n_buckets * kStatsF;
-    for (int x = threadIdx.x; x < n_buckets * kStatsF; x += blockDim.x) {
-        const int f = x % kStatsF;
-        double v = acc[x];
-        for (int ww = 1; ww < kStatsWarps; ww++) v = combine(f, v, acc[(size_t)ww * n_buckets * kStatsF + x]);
+    for (int x = lane; x < n_buckets * kStatsF; x += 32) {
+        const int f = x % kStatsF, bk = x / kStatsF;
+        const int slot = lane_slot(f);
+        double v;
+        if (slot < 0) {
+            v = (f == 0 || f == 7 || f == 8 || (f >= 9 && f < 9 + 64)) ? (double)cnt[x] : field_init(f);
+        } else {
+            const double *q = fs + ((size_t)bk * kLaneF + slot) * 32;
+            v = field_init(f);
+            for (int l = 0; l < 32; l++) v = combine(f, v, q[l]);
+        }
         dst[x] = v;
     }
 }
@@ -116,10 +103,10 @@ __global__ void k_stats_final(const double *partials, int n_blocks, int n_bucket
 
 void launch_stats(const DevBatch &b, const DevResult &r, double *partials, double *stats, int n_buckets,
                   cudaStream_t s) {
-    size_t smem = (size_t)kStatsWarps * n_buckets * kStatsF * sizeof(double);
+    const size_t smem = (size_t)n_buckets * kLaneF * 32 * sizeof(double) + (size_t)n_buckets * kStatsF * sizeof(int);
     cudaFuncSetAttribute(k_stats_partial, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kStatsWarps * JDOB_MAX_BUCKETS * kStatsF * (int)sizeof(double));
-    k_stats_partial<<<kStatsBlocks, kStatsWarps * 32, smem, s>>>(b, r, partials, n_buckets);
+                         (int)((size_t)JDOB_MAX_BUCKETS * (kLaneF * 32 * sizeof(double) + kStatsF * sizeof(int))));
+    k_stats_partial<<<kStatsBlocks, 32, smem, s>>>(b, r, partials, n_buckets);
     const int warps = n_buckets * kStatsF;
     k_stats_final<<<(warps * 32 + 255) / 256, 256, 0, s>>>(partials, kStatsBlocks, n_buckets, stats);
 }
