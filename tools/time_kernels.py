@@ -28,6 +28,24 @@ def t_solve(cfg, n):
     return {"cfg": cfg, "n": n, "ms": ms, "inst_per_s": n / ms * 1e3, "E_sum": float(res["E"].sum().item())}
 
 
+def t_eval(cfg, n):
+    b = G.config_batch(cfg, n_inst=n)
+    db = J.DeviceBatch(b)
+    res = J.solve_batch(db, f_user=False)
+    ev = J.eval_plans(db, plans=res, f_user=False)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(5):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        J.eval_plans(db, plans=res, f_user=False, out=ev)
+        e.record()
+        torch.cuda.synchronize()
+        ts.append(s.elapsed_time(e))
+    ms = float(np.median(ts))
+    return {"cfg": cfg + "_eval", "n": n, "ms": ms, "inst_per_s": n / ms * 1e3}
+
+
 def t_bf(frac):
     b = G.config_batch("c4")
     db = J.DeviceBatch(b)
@@ -64,7 +82,7 @@ if __name__ == "__main__":
     which = sys.argv[1:] or ["c2", "c3", "c5", "bf"]
     todo = {"c2": lambda: t_solve("c2", 1 << 20), "c3": lambda: t_solve("c3", 100_000),
             "c5": lambda: t_solve("c5", 1_000_000), "bf": lambda: t_bf(0.25),
-            "og": lambda: t_grouped("c3", 100_000)}
+            "og": lambda: t_grouped("c3", 100_000), "eval": lambda: t_eval("c2", 1 << 20)}
     for r in (todo[w]() for w in which):
         r["lib"] = os.path.basename(lib)
         print(json.dumps(r), flush=True)
