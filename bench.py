@@ -201,10 +201,17 @@ def run_mine(args):
     import torch
     world, rank, local = dist_env()
     dist = None
-    torch.cuda.set_device(local)
+    # JDOB_BENCH_BACKEND=gloo (test only): several ranks sharing the visible GPUs, to exercise the
+    # multi-rank path on a one-GPU box; the driver's runs use NCCL with one GPU per rank
+    backend = os.environ.get("JDOB_BENCH_BACKEND", "nccl")
+    dev_index = local % torch.cuda.device_count() if backend != "nccl" else local
+    torch.cuda.set_device(dev_index)
     if world > 1 or "TORCHELASTIC_RUN_ID" in os.environ:   # launched by torchrun (also at N = 1)
         import torch.distributed as D
-        D.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            D.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            D.init_process_group(backend)
         dist = D
     import paper_2504_14611_b200 as J
     label, n_default = WORKLOADS[args.workload]
@@ -253,7 +260,7 @@ def run_mine(args):
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks = Clocks(local)
+    clocks = Clocks(dev_index)
     clocks.start()
     time.sleep(0.3)
     K = args.steps
@@ -342,7 +349,9 @@ def run_mine(args):
                        "parallelism": f"dp{world}"},
             "roofline": {"bound": "alu", "kernel": "k_solve (K1)", "achieved": achieved, "peak": peak,
                          "unit": "G FP64 op/s", "frac": achieved / peak,
-                         "traffic": ncu_traffic("k_solve") if args.workload == "c2" else None,
+                         # committed ncu capture of the default C2 launch (2^20 instances), else none
+                         "traffic": ncu_traffic("k_solve") if (args.workload == "c2" and n == 1 << 20) else None,
+                         "ncu_hw": ncu_traffic("k_solve_hw") if (args.workload == "c2" and n == 1 << 20) else None,
                          "algorithmic_bytes": int(batch.nbytes()),
                          "work_per_launch": work, "member_evals_per_launch": n_member_exec,
                          "literal_work_per_launch": literal_work, "literal_member_evals_per_launch": n_member,
