@@ -101,7 +101,8 @@ __global__ void k_bf_setup(const DevModel *models, DevBatch b, int space, BfHead
     for (long long j = lane; j < kt; j += 32) invtab[j] = 1.0 / grid_fe(b.fe_max[0], b.rho[0], j);
 }
 
-template <int MAXM>
+// EXACT: M == MAXM, so every per-user guard folds at compile time (the C4 case, M = 8)
+template <int MAXM, bool EXACT>
 #ifndef JDOB_BF_MINB
 #define JDOB_BF_MINB 4
 #endif
@@ -118,7 +119,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
     double bestE = dinf();
     long long bestI = -1;
     if (st == JDOB_ST_OK || st == JDOB_ST_REQUIRE) {
-        const int M = hdr->M, N = hdr->N, B1 = hdr->B1;
+        const int M = EXACT ? MAXM : hdr->M, N = hdr->N, B1 = hdr->B1;
         const long long k = hdr->k;
         const unsigned long long size = hdr->size;
         const double t_free = hdr->t_free, fe_max = hdr->fe_max, rho = hdr->rho;
@@ -480,12 +481,12 @@ size_t bf_workspace_bytes() {
            1024;
 }
 
-template <int MAXM>
+template <int MAXM, bool EXACT = false>
 static void launch_main(const DevModel *models, int model_id, int space, unsigned long long ib, unsigned long long ie,
                         BfHeader *hdr, const double *tab, const double *user, const double *inv,
                         double *part_E, long long *part_idx, size_t smem, cudaStream_t s) {
-    cudaFuncSetAttribute(k_bf_main<MAXM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_bf_main<MAXM><<<kBfBlocks, kBfWarps * 32, smem, s>>>(models, model_id, space, ib, ie, hdr, tab, user, inv,
+    cudaFuncSetAttribute(k_bf_main<MAXM, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_bf_main<MAXM, EXACT><<<kBfBlocks, kBfWarps * 32, smem, s>>>(models, model_id, space, ib, ie, hdr, tab, user, inv,
                                                          part_E, part_idx);
 }
 
@@ -507,7 +508,10 @@ void launch_bruteforce_impl(const DevModel *models, const DevBatch &b, int model
     k_bf_setup<<<1, 32, 0, s>>>(models, b, space, hdr, tab, user, inv);
     const int Mc = (M >= 1 && M <= kMaxM) ? M : 1;
     const size_t smem = sizeof(double) * (4 * (size_t)(N + 1) * Mc + 128 + kInvTab + 17 * kBfThreads);
-    if (Mc <= 8)
+    if (Mc == 8)
+        launch_main<8, true>(models, model_id, space, idx_begin, idx_end, hdr, tab, user, inv, part_E, part_idx, smem,
+                             s);
+    else if (Mc <= 8)
         launch_main<8>(models, model_id, space, idx_begin, idx_end, hdr, tab, user, inv, part_E, part_idx, smem, s);
     else if (Mc <= 16)
         launch_main<16>(models, model_id, space, idx_begin, idx_end, hdr, tab, user, inv, part_E, part_idx, smem, s);
