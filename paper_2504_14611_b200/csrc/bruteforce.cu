@@ -95,6 +95,10 @@ __global__ void k_bf_setup(const DevModel *models, DevBatch b, int space, BfHead
             tab[1 * NM + n * M + lane] = x.z * md.v[n];       // zeta_m v_n
             tab[2 * NM + n * M + lane] = x.k * md.u[n];       // kappa_m u_n
             tab[3 * NM + n * M + lane] = OR * x.p;            // (O_n / R_m) p_m
+            // energy lower bound of user m at partition point n: the f_min offloader
+            // term for n < N, e_loc for n = N -- the same expressions as the kernel's bound
+            tab[4 * NM + n * M + lane] = (n < N) ? (((x.k * md.u[n]) * x.f0) * x.f0) + OR * x.p
+                                                 : user[0 * 32 + lane];
         }
     }
     const long long kt = k < kInvTab ? k : kInvTab;
@@ -126,11 +130,12 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
         const DevModel &md = models[model_id];
         const int NM = (N + 1) * M;
         double *sOR = sm, *sZV = sm + NM, *sKU = sm + 2 * NM, *sUP = sm + 3 * NM;
-        double *sEl = sm + 4 * NM, *sFmin = sEl + 32, *sFmax = sEl + 64, *sT = sEl + 96;
+        double *sLB = sm + 4 * NM;  // [N+1][M] per-user bound terms
+        double *sEl = sm + 5 * NM, *sFmin = sEl + 32, *sFmax = sEl + 64, *sT = sEl + 96;
         double *sInv = sEl + 128;
         double *sSuf = sInv + kInvTab;  // [17][kBfThreads] per-lane suffix sums (N <= 15 path)
         const long long kt = k < kInvTab ? k : kInvTab;
-        for (int x = threadIdx.x; x < 4 * NM; x += blockDim.x) sm[x] = tab[x];
+        for (int x = threadIdx.x; x < 5 * NM; x += blockDim.x) sm[x] = tab[x];
         for (int x = threadIdx.x; x < 128; x += blockDim.x) sEl[x] = user[x];
         for (long long x = threadIdx.x; x < kt; x += blockDim.x) sInv[x] = invtab[x];
         __syncthreads();
@@ -187,6 +192,15 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
 #pragma unroll
                     for (int m = 0; m < MAXM; m++) nv[m] = (nt < N && ((mask >> m) & 1ull)) ? nt : N;
                 }
+#if JDOB_BF_PRUNE
+                // user terms of the vector bound first (table lookups): most vectors stop here
+                double lbu = 0.0;
+#pragma unroll
+                for (int m = 0; m < MAXM; m++)
+                    if (m < M) lbu = lbu + sLB[nv[m] * M + m];
+                const double inc = __longlong_as_double(*(volatile long long *)&hdr->best_bits);
+                if (lbu >= bestE || lbu > inc) continue;  // the edge term only adds (>= 0)
+#endif
                 // batch sizes, suffix sums S_n and Psi (descending n), per-user S_{n_m + 1}
                 double Sm[MAXM];
 #pragma unroll
@@ -282,30 +296,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                         const double fd = __ddiv_rd(Smin, X);
                         fel = (fd > fel) ? fd : fel;
                     }
-                    double lbu = 0.0;
-#pragma unroll
-                    for (int m = 0; m < MAXM; m++) {
-                        if (m < M) {
-                            double t;
-                            if ((offm >> m) & 1u) {
-                                double ku, up;
-                                if constexpr (REG) {
-                                    ku = kur[m];
-                                    up = upr[m];
-                                } else {
-                                    const int x = nv[m] * M + m;
-                                    ku = sKU[x];
-                                    up = sUP[x];
-                                }
-                                t = ((ku * sFmin[m]) * sFmin[m]) + up;
-                            } else {
-                                t = sEl[m];
-                            }
-                            lbu = lbu + t;
-                        }
-                    }
                     const double LB = lbu + (Psi * fel) * fel;
-                    const double inc = __longlong_as_double(*(volatile long long *)&hdr->best_bits);
                     if (LB >= bestE || LB > inc) continue;
                 }
                 const double best_before = bestE;
@@ -477,7 +468,7 @@ __global__ void k_bf_final(const BfHeader *hdr, const double *part_E, const long
 }
 
 size_t bf_workspace_bytes() {
-    return 256 + sizeof(double) * (4 * 64 * 32 + 4 * 32 + kInvTab) + (sizeof(double) + sizeof(long long)) * kBfBlocks +
+    return 256 + sizeof(double) * (5 * 64 * 32 + 4 * 32 + kInvTab) + (sizeof(double) + sizeof(long long)) * kBfBlocks +
            1024;
 }
 
@@ -497,7 +488,7 @@ void launch_bruteforce_impl(const DevModel *models, const DevBatch &b, int model
     BfHeader *hdr = (BfHeader *)p;
     p += 256;
     double *tab = (double *)p;
-    p += sizeof(double) * 4 * 64 * 32;
+    p += sizeof(double) * 5 * 64 * 32;
     double *user = (double *)p;
     p += sizeof(double) * 4 * 32;
     double *inv = (double *)p;
@@ -507,7 +498,7 @@ void launch_bruteforce_impl(const DevModel *models, const DevBatch &b, int model
     long long *part_idx = (long long *)p;
     k_bf_setup<<<1, 32, 0, s>>>(models, b, space, hdr, tab, user, inv);
     const int Mc = (M >= 1 && M <= kMaxM) ? M : 1;
-    const size_t smem = sizeof(double) * (4 * (size_t)(N + 1) * Mc + 128 + kInvTab + 17 * kBfThreads);
+    const size_t smem = sizeof(double) * (5 * (size_t)(N + 1) * Mc + 128 + kInvTab + 17 * kBfThreads);
     if (Mc == 8)
         launch_main<8, true>(models, model_id, space, idx_begin, idx_end, hdr, tab, user, inv, part_E, part_idx, smem,
                              s);
