@@ -83,3 +83,38 @@ def test_oracle_header_independent():
     src = open(os.path.join(ROOT, "oracle", "jdob_oracle.c")).read()
     assert "#include \"" not in src
     assert "jdob.h" not in src
+
+
+def test_struct_layouts_match_header(tmp_path):
+    """The ctypes mirrors of jdob_model / jdob_batch / jdob_result / jdob_grouped_result have the
+    header's field offsets and sizes (compiled with the system C compiler against include/jdob.h)."""
+    import shutil
+    import subprocess
+
+    from paper_2504_14611_b200 import _binding as B
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    structs = {"jdob_model": B.JModel, "jdob_batch": B.JBatch, "jdob_result": B.JResult,
+               "jdob_grouped_result": B.JGrouped}
+    lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "jdob.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            lines.append(f'printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    lines += ["return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    inc = os.path.join(ROOT, "include")
+    subprocess.run([cc, "-I", inc, str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    got = {}
+    for ln in out:
+        if ln.strip():
+            c, f, v = ln.split()
+            got[(c, f)] = int(v)
+    for cname, py in structs.items():
+        assert got[(cname, "size")] == C.sizeof(py), cname
+        for f, _ in py._fields_:
+            assert got[(cname, f)] == getattr(py, f).offset, (cname, f)
