@@ -54,6 +54,24 @@ struct DevResult {
 };
 
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
+
+// Warp min / max of NON-NEGATIVE doubles (+0 .. +inf): their IEEE order is the integer order of the
+// bit patterns, so two 32-bit redux.sync steps (high word, then low word among the lanes holding the
+// extreme high word) give the exact extreme value.
+__device__ __forceinline__ double warp_min_nonneg(double x) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    const unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
+    const unsigned mh = __reduce_min_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_min_sync(0xffffffffu, (hi == mh) ? lo : 0xffffffffu);
+    return __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
+}
+__device__ __forceinline__ double warp_max_nonneg(double x) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    const unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
+    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_max_sync(0xffffffffu, (hi == mh) ? lo : 0u);
+    return __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
+}
 __device__ __forceinline__ double dnan() { return __longlong_as_double(0x7ff8000000000000LL); }
 __device__ __forceinline__ bool dfinite(double x) { return isfinite(x); }
 
@@ -136,12 +154,7 @@ __device__ __forceinline__ int warp_validate(const DevModel *models, const DevBa
     const double zvN = x.z * vN;
     const bool infeas = (lane < M) && !(__fma_rn(x.T, x.f1, -zvN) > 0.0) && (zvN / x.f1 > x.T);
     if (__any_sync(0xffffffffu, infeas)) return JDOB_ST_LOCAL_INFEASIBLE;
-    double Tmin = x.T;
-#pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) {
-        double o = __shfl_xor_sync(0xffffffffu, Tmin, d);
-        Tmin = (o < Tmin) ? o : Tmin;
-    }
+    const double Tmin = warp_min_nonneg(x.T);  // T > 0 (checked above), +inf beyond M
     if (Tmin < t_free) return JDOB_ST_REQUIRE;
     return JDOB_ST_OK;
 }

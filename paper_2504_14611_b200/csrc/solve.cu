@@ -204,8 +204,9 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
         s.pu[lane] = x.p;
     }
     s.T[lane] = x.T;  // +inf beyond M
+    __syncwarp();
     double E_lc = 0.0;
-    for (int t = 0; t < M; t++) E_lc = E_lc + __shfl_sync(0xffffffffu, eloc, t);  // user-index order
+    for (int t = 0; t < M; t++) E_lc = E_lc + s.et[t].x;  // user-index order
     if (st != JDOB_ST_OK || mode == JDOB_MODE_LC) {
         write_local(r, i, off, M, N, E_lc, t_free, floc, st, lane, true);
         return;
@@ -225,19 +226,17 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
         __syncwarp();
     }
     // instance-level flags (warp-uniform)
-    const double R0 = __shfl_sync(0xffffffffu, x.R, 0), z0 = __shfl_sync(0xffffffffu, x.z, 0);
-    const double f10 = __shfl_sync(0xffffffffu, x.f1, 0);
+    const double R0 = s.R[0], z0 = s.z[0], f10 = s.f1[0];  // user 0's values
     auto sb = [](double a, double c) { return __double_as_longlong(a) == __double_as_longlong(c); };
     const bool homog_ = __all_sync(0xffffffffu, lane >= M || (sb(x.R, R0) && sb(x.z, z0) && sb(x.f1, f10)));
-    const double f00 = __shfl_sync(0xffffffffu, x.f0, 0), k0 = __shfl_sync(0xffffffffu, x.k, 0);
-    const double p0 = __shfl_sync(0xffffffffu, x.p, 0);
+    const double f00 = s.fmm[0].x, k0 = s.kap[0], p0 = s.pu[0];
     const bool uni_ = homog_ && __all_sync(0xffffffffu, lane >= M || (sb(x.f0, f00) && sb(x.k, k0) && sb(x.p, p0)));
     if (UNI && !uni_) {  // left to the general kernel
         if (lane == 0) r.status[i] = kStDefer;
         return;
     }
     const bool homog = UNI ? true : homog_, uni = UNI ? true : uni_;
-    const double T0 = __shfl_sync(0xffffffffu, x.T, 0);
+    const double T0 = s.T[0];
     if (homog && __all_sync(0xffffffffu, lane >= M || x.T == T0)) {
         // equal gamma and equal deadlines (Table I identical-deadline setting): the key (T asc,
         // index asc) is the index order and every suffix minimum is T
@@ -442,30 +441,30 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
                 }
                 if (emp) break;
             }
-            if (prune) {  // warp minimum of the lane bests (identical in every lane)
-                double w = bE;
-#pragma unroll
-                for (int d = 16; d >= 1; d >>= 1) {
-                    const double o = __shfl_xor_sync(0xffffffffu, w, d);
-                    w = (o < w) ? o : w;
-                }
+            if (prune) {  // warp minimum of the lane bests (energies are >= 0)
+                const double w = warp_min_nonneg(bE);
                 bEw = (w < bEw) ? w : bEw;
             }
             __syncwarp();
         }
-        // warp argmin over (E, n~, j)
-#pragma unroll
-        for (int d = 16; d >= 1; d >>= 1) {
-            const double oE = __shfl_xor_sync(0xffffffffu, bE, d);
-            const int oN = __shfl_xor_sync(0xffffffffu, bN, d);
-            const int oJ = __shfl_xor_sync(0xffffffffu, bJ, d);
-            const int oP = __shfl_xor_sync(0xffffffffu, bP, d);
-            const bool take = (oE < bE) || (oE == bE && (oN < bN || (oN == bN && oJ < bJ)));
-            if (take) {
-                bE = oE;
-                bN = oN;
-                bJ = oJ;
-                bP = oP;
+        // warp argmin over (E, n~, j): E >= 0, so the minimum energy comes from two integer
+        // reductions of its bits; among the lanes holding it, the smallest packed key
+        // n~ << 22 | j << 5 | p (n~ < 64, j < 2^16, p < 32) is the smallest (n~, j)
+        {
+            const double Emin = warp_min_nonneg(bE);
+            const unsigned key = (bE == Emin && bE < dinf())
+                                     ? (((unsigned)bN << 22) | ((unsigned)bJ << 5) | (unsigned)bP)
+                                     : 0xffffffffu;
+            const unsigned mk = __reduce_min_sync(0xffffffffu, key);
+            bE = Emin;
+            if (mk != 0xffffffffu) {
+                bN = (int)(mk >> 22);
+                bJ = (int)((mk >> 5) & 0xffffu);
+                bP = (int)(mk & 31u);
+            } else {  // no candidate in any lane (bE = +inf)
+                bN = 0x7fffffff;
+                bJ = 0;
+                bP = 0;
             }
         }
         if (!(pruned && bE == E_lc)) break;
@@ -511,11 +510,7 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
         arr = a.y / f + a.x;
         if (arr < t_free) arr = t_free;
     }
-#pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) {
-        const double o = __shfl_xor_sync(0xffffffffu, arr, d);
-        arr = (o > arr) ? o : arr;
-    }
+    arr = warp_max_nonneg(arr);  // arrivals >= t_free >= 0
     const unsigned mask = __ballot_sync(0xffffffffu, member);
     if (lane == 0) {
         r.E[i] = bE;
