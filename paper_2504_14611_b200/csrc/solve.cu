@@ -258,9 +258,7 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
         // monotone), a non-member's term is e_loc, so each term >= the min of the two; the user-order
         // RN sum of the minima is <= the sum of the terms, and the edge term (psi f_e) f_e >= 0.
         if (UNI) {  // every user has user 0's kappa, f_min, p_u and R: one bound term per n~
-            const double rinv0 = __ddiv_rd(1.0, x.R), k0_ = x.k, fm0 = x.f0, pu0 = x.p;  // lane 0's values
-            const double rv = __shfl_sync(0xffffffffu, rinv0, 0), kv = __shfl_sync(0xffffffffu, k0_, 0);
-            const double fv = __shfl_sync(0xffffffffu, fm0, 0), pv = __shfl_sync(0xffffffffu, pu0, 0);
+            const double rv = __ddiv_rd(1.0, R0), kv = k0, fv = f00, pv = p0;  // user 0's values
             for (int nt = lane; nt < N; nt += 32) {
                 const double em = (((kv * md.u[nt]) * fv) * fv) + __dmul_rd(md.O[nt], rv) * pv;
                 double S = 0.0;
