@@ -80,6 +80,22 @@ __device__ __forceinline__ void sort_users(int M, double gam, double T, SolveSme
     __syncwarp();
 }
 
+// Homogeneous users (equal gamma): ranks under the key (T asc, index asc) from the deadlines in
+// shared memory (broadcast reads, no shuffles), then order[] and the suffix minima (= sorted T).
+__device__ __noinline__ void sort_users_T(int M, double T, SolveSmem &s, int lane) {
+    int r = 0;
+    for (int t = 0; t < M; t++) {
+        const double Tt = s.T[t];
+        r += (Tt < T || (Tt == T && t < lane)) ? 1 : 0;
+    }
+    if (lane < M) {
+        s.rank[lane] = r;
+        s.order[r] = lane;
+        s.Lg[r].x = T;  // ascending deadlines: the suffix minimum at position r is T itself
+    }
+    __syncwarp();
+}
+
 // Alg. 1 lines 4-6 for partition point nt.  Returns i^ (M if none).
 __device__ __forceinline__ int setup_nt(const DevModel &md, int nt, int M, bool homog, bool uni, double t_free,
                                         SolveSmem &s, int lane) {
@@ -246,7 +262,7 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
             s.Lg[lane].x = x.T;
         }
     } else if (homog) {
-        sort_users(M, 0.0, x.T, s, lane);  // equal gamma: key (T asc, index asc)
+        sort_users_T(M, x.T, s, lane);  // equal gamma: key (T asc, index asc)
     }
     __syncwarp();
 
