@@ -92,6 +92,18 @@ def test_random_uniform_users(J, seed, M_hi, N_hi, k_max):
 
 
 @pytest.mark.parametrize("uniform", [False, True])
+def test_deep_models_and_long_grids(J, uniform):
+    """N > 32 (two n~ bounds per lane, two-word candidate ballots), grids longer than the 1/f_e cache
+    (k up to 300 > 192), M up to 32: literal, pruned and executed-work sweeps against the oracle."""
+    b = g.random_batch(seed=300, n_inst=300, M_lo=1, M_hi=32, N_lo=33, N_hi=63, k_max=300)
+    if uniform:
+        b = uniformise(b, 300)
+    _, gpu = run(J, b)
+    orc = O.solve_batch(b, counts=True)
+    assert_solve_parity(gpu, orc, counts=True)
+
+
+@pytest.mark.parametrize("uniform", [False, True])
 def test_zero_energy_ties(J, uniform):
     """kappa = p_u = 0 and c = 0: every configuration costs exactly E_LC = 0, so the answer is decided
     by the (E, n~, j) tie rule against the first all-local evaluation (R8).  The pruned sweep skips
