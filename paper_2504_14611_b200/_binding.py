@@ -275,7 +275,7 @@ def bruteforce(db: DeviceBatch, space: int, idx_begin: int = 0, idx_end: Optiona
 class HostBuffers:
     """Pinned host copies of a batch and its outputs for the end-to-end call."""
 
-    def __init__(self, batch, f_user=False, stats=False, n_buckets=None):
+    def __init__(self, batch, f_user=False, stats=False, n_buckets=None, partition=False):
         torch = _torch()
 
         def pin(a, dtype):
@@ -304,6 +304,7 @@ class HostBuffers:
                         f_e=z(n, torch.float64), n_tilde=z(n, torch.int32), j=z(n, torch.int32),
                         status=z(n, torch.int32), mask=z(n, torch.int32),
                         f_user=z(nu, torch.float64) if f_user else None, counts=None,
+                        partition=z(nu, torch.int32) if partition else None,
                         stats=z((n_buckets or MAX_M) * STATS_FIELDS, torch.float64) if stats else None)
         self.n_buckets = (n_buckets or MAX_M) if stats else 0
 

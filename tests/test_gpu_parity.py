@@ -258,6 +258,22 @@ def test_host_api_matches_device(J):
         assert_bits_equal(host[f], gpu[f], f)
 
 
+def test_host_api_large_m_and_partition(J):
+    """Host API on a batch mixing M <= 32 and M > 32 (block path), per-user partition copied back."""
+    small = g.random_batch(seed=141, n_inst=200, M_lo=1, M_hi=32, N_lo=1, N_hi=8, k_max=40)
+    mix = g.concat([small, _large_batch([40, 90, 33], seed=5)])
+    db = J.DeviceBatch(mix)
+    dev = to_np(J.solve_batch(db, partition=True))
+    hb = J.HostBuffers(mix, f_user=True, partition=True)
+    J.solve_batch_host(hb)
+    host = {k: v.numpy() for k, v in hb.out.items() if v is not None}
+    host["mask"] = host["mask"].view(np.uint32)
+    for f in ("E", "E_lc", "t_free_next", "f_e", "n_tilde", "j", "status", "mask", "f_user", "partition"):
+        assert_bits_equal(host[f], dev[f], f)
+    orc = O.solve_batch(mix)
+    assert_bits_equal(host["partition"], orc["part"], "partition vs oracle")
+
+
 def test_host_api_chunked_pipeline(J):
     # > 131072 instances: several copy/compute pipeline chunks on two internal streams
     b = g.config_batch("c3", n_inst=300_000)
