@@ -29,6 +29,14 @@
 // f_min, kappa and p_u agree ("uniform users": all of Table I's experiments, where
 // only deadlines differ), every member of a configuration has the same budget, f*
 // and offloader energy, which are then formed once per (n~, j) instead of per user.
+// Uniform-user instances are solved by their own kernel (UNI = true), whose smaller
+// code keeps instruction-cache stalls down; the general kernel takes the rest.
+//
+// Branch and bound over n~ (DESIGN.md §4 "n~ pruning"): a lower bound of every
+// configuration's energy is formed per n~ (lane = n~); n~ are visited in ascending
+// order and one whose bound is not below the best energy so far is skipped.  An
+// exact tie of the best offloading energy with E_LC after pruning re-sweeps the
+// instance literally (the all-local key of a skipped n~ could matter, R8).
 #include "jdob_dev.cuh"
 #include "kernels.h"
 
