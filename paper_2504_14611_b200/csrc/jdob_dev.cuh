@@ -85,6 +85,9 @@ __device__ __forceinline__ double clampf(double G, double fmin, double fmax) {
 __device__ __forceinline__ double grid_fe(double fe_max, double rho, long long j) {
     return __dsub_rn(fe_max, __dmul_rn((double)j, rho));
 }
+__device__ __forceinline__ double grid_fe(double fe_max, double rho, int j) {  // same value: j < 2^31
+    return __dsub_rn(fe_max, __dmul_rn((double)j, rho));
+}
 
 // k = #{j >= 0 : f_e(j) >= f_e,min}; the predicate is monotone in j (RN(j rho) is
 // non-decreasing, so is the subtraction's complement), so k is its first failing j in

@@ -236,13 +236,13 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
         return;
     }
 
-    const long long kk = (mode == JDOB_MODE_NO_EDGE_DVFS) ? 1 : k;
-    const long long kc = kk < kInvCache ? kk : kInvCache;
+    const int kk = (mode == JDOB_MODE_NO_EDGE_DVFS) ? 1 : (int)k;  // k <= kMaxK (validated)
+    const int kc = kk < kInvCache ? kk : kInvCache;
     // 1/f_e(j) cache per warp: the hit test is read by every lane before any lane rewrites it
     const bool inv_hit = __all_sync(0xffffffffu, fe_max == s.inv_key.x && rho == s.inv_key.y && kc <= s.inv_n);
     if (!inv_hit) {  // warp-uniform
         __syncwarp();
-        for (long long j = lane; j < kc; j += 32) s.inv[j] = 1.0 / grid_fe(fe_max, rho, j);
+        for (int j = lane; j < kc; j += 32) s.inv[j] = 1.0 / grid_fe(fe_max, rho, (long long)j);
         if (lane == 0) {
             s.inv_key = make_double2(fe_max, rho);
             s.inv_n = (int)kc;
@@ -352,8 +352,8 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
             // two grid points per lane (j0 + lane and j0 + 32 + lane): the two energy chains are
             // independent, which doubles the instruction-level parallelism of the sweep and lets both
             // share each user's shared-memory loads
-            for (long long j0 = 0; j0 < kk; j0 += 64) {
-                const long long jA = j0 + lane, jB = jA + 32;
+            for (int j0 = 0; j0 < kk; j0 += 64) {
+                const int jA = j0 + lane, jB = jA + 32;
                 const bool vA = jA < kk, vB = jB < kk;
                 const double feA = grid_fe(fe_max, rho, jA), feB = grid_fe(fe_max, rho, jB);
                 // p(j): first sorted position >= i^ with !(f_e < th_i)  (M if the set is empty)
@@ -372,7 +372,7 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
                 // Alg. 2's break: the first j with an empty set ends this n~'s sweep
                 const unsigned empA = __ballot_sync(0xffffffffu, vA && pA == M);
                 const unsigned empB = __ballot_sync(0xffffffffu, vB && pB == M);
-                const long long jb = empA ? j0 + (__ffs(empA) - 1) : (empB ? j0 + 32 + (__ffs(empB) - 1) : kk);
+                const int jb = empA ? j0 + (__ffs(empA) - 1) : (empB ? j0 + 32 + (__ffs(empB) - 1) : kk);
                 const bool emp = (empA | empB) != 0u;
                 if (emp && aN == N) {
                     aN = nt;
