@@ -133,6 +133,17 @@ def fp64_work(batch, counts, setups=None, lower_bound=False):
     return float(np.sum(ops)), float(np.sum(mem))
 
 
+def hbm_context(nbytes, ms):
+    """HBM side of K1 for context: algorithmic bytes per launch over the launch time, against the
+    measured copy bandwidth (MEASURED_PEAKS.json, driver-written) -- K1 is not memory-bound."""
+    try:
+        peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        peak = None
+    gbs = nbytes / (ms / 1e3) / 1e9
+    return {"achieved_gbs": gbs, "peak_gbs": peak, "frac": (gbs / peak) if peak else None}
+
+
 def ncu_traffic(kernel):
     """dram read+write bytes per launch of `kernel` from the committed ncu --set full capture."""
     try:
@@ -353,6 +364,7 @@ def run_mine(args):
                          "traffic": ncu_traffic("k_solve") if (args.workload == "c2" and n == 1 << 20) else None,
                          "ncu_hw": ncu_traffic("k_solve_hw") if (args.workload == "c2" and n == 1 << 20) else None,
                          "algorithmic_bytes": int(batch.nbytes()),
+                         "hbm": hbm_context(int(batch.nbytes()), solve_ms),
                          "work_per_launch": work, "member_evals_per_launch": n_member_exec,
                          "literal_work_per_launch": literal_work, "literal_member_evals_per_launch": n_member,
                          "literal_equivalent": literal_work / (solve_ms / 1e3) / 1e9,
