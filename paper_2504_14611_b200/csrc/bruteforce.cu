@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                         if (!(t_free + Smin * inv0 <= l_o)) continue;  // D6' fails at once: no candidate
                         const double X = __dmul_ru(__dadd_ru(__dmul_ru(l_o, 0x1.0000000000001p+0), -t_free),
                                                    0x1.0000000000004p+0);
-                        const double fd = __ddiv_rd(Smin, X);
+                        const double fd = div_lb(Smin, X);  // <= Smin / X
                         fel = (fd > fel) ? fd : fel;
                     }
                     const double LB = lbu + (Psi * fel) * fel;

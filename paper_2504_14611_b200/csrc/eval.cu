@@ -148,7 +148,7 @@ __global__ void k_eval(const DevModel *models, DevBatch b, const int *partition,
                 f = b.f_max[u];
             }
             e = ((b.kappa[u] * md.u[nm]) * f) * f + OR * b.p_u[u];
-            double arr = zv / f + OR;
+            double arr = div_z(zv, f) + OR;
             double fin = arr + Sn * inv;
             if (fin > l_o + tol) viol |= 2u;
             if (fin > tf) tf = fin;

@@ -81,6 +81,29 @@ __device__ __forceinline__ double clampf(double G, double fmin, double fmax) {
     return (x > fmax) ? fmax : x;
 }
 
+// a / b for b > 0 finite.  A zero numerator sends the correctly rounded division to its slow
+// path (~140 instructions: the fast path's exponent test fails for a zero quotient), and
+// 0 / b = 0 with a's sign, i.e. a itself: same bits, no division.  zeta v_0 = 0 at n~ = 0.
+__device__ __forceinline__ double div_z(double a, double b) { return (a == 0.0) ? a : a / b; }
+
+// RD(1 / x) for x > 0 (the bound of DESIGN.md §4 "n~ pruning"), without the div_rd subroutine:
+// q = RN(1 / x); if q x - 1 > 0 exactly (the sign of the fma) then q > 1/x and RD(1/x) is q's
+// predecessor (no representable number lies strictly between RD and RN when they differ),
+// otherwise q <= 1/x and q = RD(1/x).  q = +inf (x subnormal) gives DBL_MAX = RD; q = +0 gives
+// +0 = RD (1/x below half the smallest subnormal).
+__device__ __forceinline__ double recip_rd(double x) {
+    const double q = 1.0 / x;
+    return (__fma_rn(q, x, -1.0) > 0.0) ? __longlong_as_double(__double_as_longlong(q) - 1) : q;
+}
+
+// A lower bound of a / b for a >= 0, b > 0, at most RD(a / b)'s predecessor below it, without the
+// div_rd subroutine: q = RN(a / b) and the sign of a - q b (exact in the fma) tells whether q
+// exceeds the quotient; if it may (<= 0), q's predecessor is returned.  Only bounds use it.
+__device__ __forceinline__ double div_lb(double a, double b) {
+    const double q = a / b;
+    return (q > 0.0 && !(__fma_rn(-q, b, a) > 0.0)) ? __longlong_as_double(__double_as_longlong(q) - 1) : q;
+}
+
 // Edge grid (R7): f_e(j) = f_e,max - j*rho, one multiply then one subtract.
 __device__ __forceinline__ double grid_fe(double fe_max, double rho, long long j) {
     return __dsub_rn(fe_max, __dmul_rn((double)j, rho));

@@ -112,7 +112,7 @@ __device__ __forceinline__ int setup_nt(const DevModel &md, int nt, int M, bool 
     if (lane < M) {
         const double OR = O_nt / s.R[lane];  // Eq. (3)
         const double zv = s.z[lane] * v_nt;
-        gam = OR + zv / s.f1[lane];          // gamma
+        gam = OR + div_z(zv, s.f1[lane]);   // gamma
         if (!uni || lane == 0) {             // uniform users: one copy serves every member
             s.orzv[lane] = make_double2(OR, zv);
             s.kuup[lane] = make_double2(s.kap[lane] * u_nt, OR * s.pu[lane]);  // Eq. (4)
@@ -282,7 +282,7 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
         // monotone), a non-member's term is e_loc, so each term >= the min of the two; the user-order
         // RN sum of the minima is <= the sum of the terms, and the edge term (psi f_e) f_e >= 0.
         if (UNI) {  // every user has user 0's kappa, f_min, p_u and R: one bound term per n~
-            const double rv = __ddiv_rd(1.0, R0), kv = k0, fv = f00, pv = p0;  // user 0's values
+            const double rv = recip_rd(R0), kv = k0, fv = f00, pv = p0;  // user 0's values
             for (int nt = lane; nt < N; nt += 32) {
                 const double em = (((kv * md.u[nt]) * fv) * fv) + __dmul_rd(md.O[nt], rv) * pv;
                 double S = 0.0;
@@ -293,7 +293,7 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
                 s.lb[nt] = S;
             }
         } else {
-            if (lane < M) s.rinv[lane] = __ddiv_rd(1.0, x.R);
+            if (lane < M) s.rinv[lane] = recip_rd(x.R);
             __syncwarp();
             for (int nt = lane; nt < N; nt += 32) {
                 const double u_nt = md.u[nt], O_nt = md.O[nt];
@@ -529,7 +529,7 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
         const double budget = (lo_ - a.x) - te;
         const bool low = (a.y == 0.0) || (__fma_rn(t.x, budget, -a.y) > 0.0);
         f = low ? t.x : clampf(a.y / budget, t.x, t.y);
-        arr = a.y / f + a.x;
+        arr = div_z(a.y, f) + a.x;
         if (arr < t_free) arr = t_free;
     }
     arr = warp_max_nonneg(arr);  // arrivals >= t_free >= 0

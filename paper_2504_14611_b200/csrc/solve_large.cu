@@ -95,7 +95,7 @@ __device__ int large_setup(const DevModel &md, int nt, int M, bool homog, double
         const long long u = off + m;
         const double OR = O_nt / b.R[u];  // Eq. (3)
         const double zv = b.zeta[u] * v_nt;
-        s.gam[m] = OR + zv / b.f_max[u];  // gamma
+        s.gam[m] = OR + div_z(zv, b.f_max[u]);  // gamma
         s.orzv[m] = make_double2(OR, zv);
         s.kuup[m] = make_double2(b.kappa[u] * u_nt, OR * b.p_u[u]);  // Eq. (4)
     }
