@@ -134,16 +134,28 @@ struct InstRegs {  // lane-resident user parameters (lane = user)
 // predicates and precedence as the oracle's check_inst: BADMODEL, then BADPARAM
 // (model id, M range, user boxes, edge boxes, grid length), then LOCAL_INFEASIBLE
 // (P:127), then REQUIRE.  Lanes >= M get T = +inf and zeros.
-__device__ __forceinline__ int warp_validate(const DevModel *models, const DevBatch &b, long long i, int lane,
-                                             InstRegs &x, int &M, long long &k, const DevModel *&mdp,
-                                             long long &off) {
-    off = b.user_off[i];
-    const long long M64 = (b.user_end ? b.user_end[i] : b.user_off[i + 1]) - off;
+// (off, M64, mid) = user_off[i], the user count and model_id[i], loaded by the caller (K1 loads
+// the next instance's while it solves the current one).  The user loads are issued before the
+// model checks so that their latency overlaps the model-table loads.
+__device__ __forceinline__ int warp_validate_pre(const DevModel *models, const DevBatch &b, long long i, int lane,
+                                                 long long off, long long M64, int mid, InstRegs &x, int &M,
+                                                 long long &k, const DevModel *&mdp) {
     M = (M64 >= 1 && M64 <= kMaxM) ? (int)M64 : 0;
     k = 0;
     x.z = x.k = x.f0 = x.f1 = x.R = x.p = 0.0;
     x.T = dinf();
-    const int mid = b.model_id[i];
+#ifndef JDOB_LATE_USERS
+    if (lane < M) {  // users of an instance rejected below are loaded but not used
+        const long long u = off + lane;
+        x.z = b.zeta[u];
+        x.k = b.kappa[u];
+        x.f0 = b.f_min[u];
+        x.f1 = b.f_max[u];
+        x.R = b.R[u];
+        x.p = b.p_u[u];
+        x.T = b.T[u];
+    }
+#endif
     if (mid < 0 || mid >= b.n_models) {
         mdp = nullptr;
         return JDOB_ST_BADPARAM;
@@ -154,6 +166,7 @@ __device__ __forceinline__ int warp_validate(const DevModel *models, const DevBa
     if (M64 > kMaxM) return kStDefer;  // more users than lanes: the block-per-instance path
     bool ok = true;
     if (lane < M) {
+#ifdef JDOB_LATE_USERS
         const long long u = off + lane;
         x.z = b.zeta[u];
         x.k = b.kappa[u];
@@ -162,6 +175,7 @@ __device__ __forceinline__ int warp_validate(const DevModel *models, const DevBa
         x.R = b.R[u];
         x.p = b.p_u[u];
         x.T = b.T[u];
+#endif
         ok = dfinite(x.z) && dfinite(x.k) && dfinite(x.f0) && dfinite(x.f1) && dfinite(x.R) && dfinite(x.p) &&
              dfinite(x.T);
         ok = ok && (x.z >= 0.0) && (x.k >= 0.0) && (x.f0 > 0.0) && (x.f0 <= x.f1) && (x.R > 0.0) &&
@@ -183,6 +197,14 @@ __device__ __forceinline__ int warp_validate(const DevModel *models, const DevBa
     const double Tmin = warp_min_nonneg(x.T);  // T > 0 (checked above), +inf beyond M
     if (Tmin < t_free) return JDOB_ST_REQUIRE;
     return JDOB_ST_OK;
+}
+
+__device__ __forceinline__ int warp_validate(const DevModel *models, const DevBatch &b, long long i, int lane,
+                                             InstRegs &x, int &M, long long &k, const DevModel *&mdp,
+                                             long long &off) {
+    off = b.user_off[i];
+    const long long M64 = (b.user_end ? b.user_end[i] : b.user_off[i + 1]) - off;
+    return warp_validate_pre(models, b, i, lane, off, M64, b.model_id[i], x, M, k, mdp);
 }
 
 __device__ __forceinline__ double shfl_d(double x, int src, unsigned mask = 0xffffffffu) {

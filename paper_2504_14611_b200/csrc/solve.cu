@@ -194,14 +194,15 @@ __device__ __forceinline__ void write_local(const DevResult &r, long long i, lon
 // are marked kStDefer), false = the rest (only instances marked kStDefer by the first kernel).
 // Two specialised kernels keep each one's code, and so its instruction-cache footprint, small.
 template <bool COUNTS, bool PRUNE, bool UNI>
-__device__ __forceinline__ void solve_instance(long long i, const DevModel *models, const DevBatch &b,
-                                               const DevResult &r, int mode, SolveSmem &s, int lane) {
+__device__ __forceinline__ void solve_instance(long long i, long long off, long long M64, int mid,
+                                               const DevModel *models, const DevBatch &b, const DevResult &r,
+                                               int mode, SolveSmem &s, int lane) {
     __syncwarp();
-    long long off, k;
+    long long k;
     int M;
     const DevModel *mdp;
     InstRegs x;
-    const int st = warp_validate(models, b, i, lane, x, M, k, mdp, off);
+    const int st = warp_validate_pre(models, b, i, lane, off, M64, mid, x, M, k, mdp);
     if (st == kStDefer) return;  // M > 32: solved by k_solve_large (solve_large.cu)
     const double t_free = b.t_free[i], fe_max = b.fe_max[i], rho = b.rho[i];
     if (st == JDOB_ST_BADPARAM || st == JDOB_ST_BADMODEL) {
@@ -516,7 +517,14 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
         return;
     }
     // winner: recompute D20 and D22 lane = user (same arithmetic as the sweep)
-    if (bN != last_nt) setup_nt(md, bN, M, homog, uni, t_free, s, lane);
+#ifdef JDOB_WIN_SETUP
+    const bool win_direct = false;
+#else
+    // homogeneous users: ranks and sorted deadlines are per instance, only (O/R, zv) depend on n~,
+    // so the winner's are formed directly (same expressions as setup_nt) instead of a new set-up
+    const bool win_direct = homog;
+#endif
+    if (!win_direct && bN != last_nt) setup_nt(md, bN, M, homog, uni, t_free, s, lane);
     const int Bo = M - bP;
     const double lo_ = s.Lg[bP].x;
     const double fe = grid_fe(fe_max, rho, bJ);
@@ -525,7 +533,9 @@ __device__ __forceinline__ void solve_instance(long long i, const DevModel *mode
     const bool member = (lane < M) && (s.rank[lane] >= bP);
     double f = floc, arr = t_free;
     if (member) {
-        const double2 a = s.orzv[uni ? 0 : lane], t = s.fmm[lane];  // (O/R, zv), (f_min, f_max)
+        const double2 a = win_direct ? make_double2(md.O[bN] / s.R[lane], s.z[lane] * md.v[bN])
+                                     : s.orzv[uni ? 0 : lane];  // (O/R, zv)
+        const double2 t = s.fmm[lane];                          // (f_min, f_max)
         const double budget = (lo_ - a.x) - te;
         const bool low = (a.y == 0.0) || (__fma_rn(t.x, budget, -a.y) > 0.0);
         f = low ? t.x : clampf(a.y / budget, t.x, t.y);
@@ -570,7 +580,31 @@ __global__ void __launch_bounds__(kSolveWarps * 32, UNI ? JDOB_SOLVE_MINB_U : JD
     const long long gw = (long long)blockIdx.x * kSolveWarps + (threadIdx.x >> 5);
     const long long nw = (long long)gridDim.x * kSolveWarps;
     if (UNI) {
-        for (long long i = gw; i < b.n_inst; i += nw) solve_instance<COUNTS, PRUNE, UNI>(i, models, b, r, mode, s, lane);
+        // (user_off, user count, model id) of the warp's next instance are loaded while it solves the
+        // current one, so each instance's user loads issue at once (one HBM latency less per instance)
+        auto head = [&](long long i, long long &o, long long &m, int &id) {
+            if (i < b.n_inst) {
+                o = b.user_off[i];
+                m = (b.user_end ? b.user_end[i] : b.user_off[i + 1]) - o;
+                id = b.model_id[i];
+            }
+        };
+        long long o = 0, m = 0;
+        int id = 0;
+        head(gw, o, m, id);
+        for (long long i = gw; i < b.n_inst; i += nw) {
+            const long long co = o, cm = m;
+            const int cid = id;
+#ifndef JDOB_NO_PF
+            head(i + nw, o, m, id);
+#else
+            head(i, o, m, id);
+#endif
+            solve_instance<COUNTS, PRUNE, UNI>(i, co, cm, cid, models, b, r, mode, s, lane);
+#ifdef JDOB_NO_PF
+            head(i + nw, o, m, id);
+#endif
+        }
     } else {
         // only the instances the uniform-users kernel left (kStDefer): 32 statuses per coalesced read
         for (long long base = gw * 32; base < b.n_inst; base += nw * 32) {
@@ -579,7 +613,9 @@ __global__ void __launch_bounds__(kSolveWarps * 32, UNI ? JDOB_SOLVE_MINB_U : JD
             while (def) {
                 const int q = __ffs(def) - 1;
                 def &= def - 1u;
-                solve_instance<COUNTS, PRUNE, UNI>(base + q, models, b, r, mode, s, lane);
+                const long long ii2 = base + q, o = b.user_off[ii2];
+                const long long m = (b.user_end ? b.user_end[ii2] : b.user_off[ii2 + 1]) - o;
+                solve_instance<COUNTS, PRUNE, UNI>(ii2, o, m, b.model_id[ii2], models, b, r, mode, s, lane);
             }
         }
     }
