@@ -47,28 +47,52 @@ __global__ void __launch_bounds__(32) k_stats_partial(DevBatch b, DevResult r, d
     const long long W = gridDim.x;
     const long long gw = blockIdx.x;
     const long long i0 = b.n_inst * gw / W, i1 = b.n_inst * (gw + 1) / W;
-    for (long long i = i0 + lane; i < i1; i += 32) {
-        const int M = (int)(b.user_off[i + 1] - b.user_off[i]);
-        int bk = b.bucket ? b.bucket[i] : ((M >= 1 && M <= kMaxM) ? M - 1 : 0);
-        if (bk < 0 || bk >= n_buckets) continue;
-        int *c = cnt + bk * kStatsF;
-        if (r.status[i] != JDOB_ST_OK) {
-            atomicAdd(c + 8, 1);
-            continue;
+    // the lane's instances i0 + lane, + 32, ... in that order, four per step: the loads of the four are
+    // issued together (latency overlap), the accumulation keeps the order (same bits)
+    constexpr int U = 4;
+    for (long long i = i0 + lane; i < i1; i += 32 * U) {
+        int Mq[U], bq[U], sq[U], nq[U];
+        unsigned mq[U];
+        double Eq[U], Lq[U];
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            const long long ii = i + 32 * q;
+            sq[q] = JDOB_ST_BADPARAM;
+            bq[q] = -1;
+            if (ii < i1) {
+                Mq[q] = (int)(b.user_off[ii + 1] - b.user_off[ii]);
+                bq[q] = b.bucket ? b.bucket[ii] : ((Mq[q] >= 1 && Mq[q] <= kMaxM) ? Mq[q] - 1 : 0);
+                sq[q] = r.status[ii];
+                Eq[q] = r.E[ii];
+                Lq[q] = r.E_lc[ii];
+                mq[q] = r.mask[ii];
+                nq[q] = r.n_tilde[ii];
+            }
         }
-        const double E = r.E[i], El = r.E_lc[i];
-        const double rr = 100.0 * (El - E) / El;
-        double *a = fs + (size_t)bk * kLaneF * 32 + lane;
-        a[0 * 32] = a[0 * 32] + rr;
-        a[1 * 32] = a[1 * 32] + rr * rr;
-        a[2 * 32] = (rr > a[2 * 32]) ? rr : a[2 * 32];
-        a[3 * 32] = (rr < a[3 * 32]) ? rr : a[3 * 32];
-        a[4 * 32] = a[4 * 32] + E / (double)M;
-        a[5 * 32] = a[5 * 32] + El / (double)M;
-        atomicAdd(c + 0, 1);
-        if (r.mask[i] != 0u) atomicAdd(c + 7, 1);
-        const int nt = r.n_tilde[i];
-        if (nt >= 0 && nt < 64) atomicAdd(c + 9 + nt, 1);
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            const int bk = bq[q];
+            if (bk < 0 || bk >= n_buckets) continue;  // also: beyond the range
+            int *c = cnt + bk * kStatsF;
+            if (sq[q] != JDOB_ST_OK) {
+                atomicAdd(c + 8, 1);
+                continue;
+            }
+            const double E = Eq[q], El = Lq[q];
+            const int M = Mq[q];
+            const double rr = 100.0 * (El - E) / El;
+            double *a = fs + (size_t)bk * kLaneF * 32 + lane;
+            a[0 * 32] = a[0 * 32] + rr;
+            a[1 * 32] = a[1 * 32] + rr * rr;
+            a[2 * 32] = (rr > a[2 * 32]) ? rr : a[2 * 32];
+            a[3 * 32] = (rr < a[3 * 32]) ? rr : a[3 * 32];
+            a[4 * 32] = a[4 * 32] + E / (double)M;
+            a[5 * 32] = a[5 * 32] + El / (double)M;
+            atomicAdd(c + 0, 1);
+            if (mq[q] != 0u) atomicAdd(c + 7, 1);
+            const int nt = nq[q];
+            if (nt >= 0 && nt < 64) atomicAdd(c + 9 + nt, 1);
+        }
     }
     __syncwarp();
     double *dst = partials + (size_t)blockIdx.x * n_buckets * kStatsF;
@@ -95,6 +119,7 @@ __global__ void k_stats_final(const double *partials, int n_blocks, int n_bucket
     if (x >= n_buckets * kStatsF) return;
     const int f = x % kStatsF;
     double v = field_init(f);
+#pragma unroll 8
     for (int blk = lane; blk < n_blocks; blk += 32) v = combine(f, v, partials[(size_t)blk * n_buckets * kStatsF + x]);
 #pragma unroll
     for (int d = 16; d >= 1; d >>= 1) v = combine(f, v, __shfl_xor_sync(0xffffffffu, v, d));

@@ -28,6 +28,27 @@ def t_solve(cfg, n):
     return {"cfg": cfg, "n": n, "ms": ms, "inst_per_s": n / ms * 1e3, "E_sum": float(res["E"].sum().item())}
 
 
+def t_stats(cfg, n):
+    """solve with the bucketed statistics (K4) minus solve without: K4's share of a step."""
+    b = G.config_batch(cfg, n_inst=n)
+    db = J.DeviceBatch(b)
+    out = {}
+    for st in (False, True):
+        kw = dict(stats=True, n_buckets=int(b.meta.get("n_buckets", 32))) if st else {}
+        res = J.solve_batch(db, f_user=False, **kw)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(7):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            J.solve_batch(db, f_user=False, out=res, **kw)
+            e.record()
+            torch.cuda.synchronize()
+            ts.append(s.elapsed_time(e))
+        out[st] = float(np.median(ts))
+    return {"cfg": cfg + "_stats", "n": n, "ms": out[True] - out[False], "solve_ms": out[False]}
+
+
 def t_eval(cfg, n):
     b = G.config_batch(cfg, n_inst=n)
     db = J.DeviceBatch(b)
@@ -82,7 +103,8 @@ if __name__ == "__main__":
     which = sys.argv[1:] or ["c2", "c3", "c5", "bf"]
     todo = {"c2": lambda: t_solve("c2", 1 << 20), "c3": lambda: t_solve("c3", 100_000),
             "c5": lambda: t_solve("c5", 1_000_000), "bf": lambda: t_bf(0.25),
-            "og": lambda: t_grouped("c3", 100_000), "eval": lambda: t_eval("c2", 1 << 20)}
+            "og": lambda: t_grouped("c3", 100_000), "eval": lambda: t_eval("c2", 1 << 20),
+            "stats": lambda: t_stats("c2", 1 << 20), "stats5": lambda: t_stats("c5", 1_000_000)}
     for r in (todo[w]() for w in which):
         r["lib"] = os.path.basename(lib)
         print(json.dumps(r), flush=True)
