@@ -21,6 +21,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_bf
     python tools/profile_bf.py 1.0 > $OUT/prof_bf.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_eval -c 1 -o $OUT/prof_eval -f \
     python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --no-bf > $OUT/prof_eval.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_stats_partial -c 1 -o $OUT/prof_stats -f \
+    python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --no-bf > $OUT/prof_stats.log 2>&1
 for tool in memcheck racecheck synccheck initcheck; do
     timeout 900 compute-sanitizer --tool $tool python tools/sanitize_run.py > $OUT/sanitize_$tool.txt 2>&1
 done
