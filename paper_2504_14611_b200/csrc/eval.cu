@@ -8,10 +8,6 @@
 
 namespace jdob {
 
-#ifndef EVAL_BPS
-#define EVAL_BPS 8
-#endif
-
 // n_m of user m (global user index u, local index m) of instance i: the given partition
 // vector, or the identical plan (n~, mask) of jdob_solve_batch.
 __device__ __forceinline__ int part_of(const int *partition, const int *plan_nt, const unsigned *plan_mask,
@@ -20,10 +16,11 @@ __device__ __forceinline__ int part_of(const int *partition, const int *plan_nt,
     return ((plan_mask[i] >> m) & 1u) ? plan_nt[i] : N;
 }
 
-__device__ __forceinline__ void eval_one(const DevModel *models, const DevBatch &b, const int *partition,
-                                         const int *plan_nt, const unsigned *plan_mask, const double *f_e,
-                                         double slack, double *E_out, double *tf_out, double *f_user,
-                                         unsigned *viol_out, int *status_out, long long i) {
+__global__ void k_eval(const DevModel *models, DevBatch b, const int *partition, const int *plan_nt,
+                       const unsigned *plan_mask, const double *f_e, double slack, double *E_out, double *tf_out,
+                       double *f_user, unsigned *viol_out, int *status_out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= b.n_inst) return;
     const long long off = b.user_off[i];
     const long long M64 = b.user_off[i + 1] - off;
     const int mid = b.model_id[i];
@@ -172,32 +169,12 @@ __device__ __forceinline__ void eval_one(const DevModel *models, const DevBatch 
     status_out[i] = st;
 }
 
-__global__ void k_eval(const DevModel *models, DevBatch b, const int *partition, const int *plan_nt,
-                       const unsigned *plan_mask, const double *f_e, double slack, double *E_out, double *tf_out,
-                       double *f_user, unsigned *viol_out, int *status_out) {
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < b.n_inst;
-         i += (long long)gridDim.x * blockDim.x)
-        eval_one(models, b, partition, plan_nt, plan_mask, f_e, slack, E_out, tf_out, f_user, viol_out, status_out, i);
-}
-
 void launch_eval(const DevModel *models, const DevBatch &b, const int *partition, const int *plan_nt,
                  const unsigned *plan_mask, const double *f_e, double slack, double *E, double *tf, double *f_user,
                  unsigned *viol, int *status, cudaStream_t s) {
     if (b.n_inst <= 0) return;
-    // persistent grid of EVAL_BPS blocks per SM with the largest L1 carveout (no shared memory is
-    // used): a thread's user loop re-reads lines that its warp's strided loads brought into L1.
-    // Measured on C2: 2 blocks/SM 0.62 ms, 4 0.41, 6-12 0.37, one-shot grid 0.385.
     const int bs = 128;
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    cudaFuncSetAttribute(k_eval, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
-    long long grid = (long long)sms * EVAL_BPS;
-    const long long want = (b.n_inst + bs - 1) / bs;
-    if (want < grid) grid = want;
+    long long grid = (b.n_inst + bs - 1) / bs;
     k_eval<<<(unsigned)grid, bs, 0, s>>>(models, b, partition, plan_nt, plan_mask, f_e, slack, E, tf, f_user, viol,
                                           status);
 }

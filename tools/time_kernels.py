@@ -11,21 +11,22 @@ import jdobgen as G  # noqa: E402
 import paper_2504_14611_b200 as J  # noqa: E402
 
 
-def t_solve(cfg, n):
+def t_solve(cfg, n, mode=None):
+    mode = J.MODE_FULL if mode is None else mode
     b = G.config_batch(cfg, n_inst=n)
     db = J.DeviceBatch(b)
-    res = J.solve_batch(db, f_user=False)
+    res = J.solve_batch(db, f_user=False, mode=mode)
     torch.cuda.synchronize()
     ts = []
     for _ in range(5):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        J.solve_batch(db, f_user=False, out=res)
+        J.solve_batch(db, f_user=False, out=res, mode=mode)
         e.record()
         torch.cuda.synchronize()
         ts.append(s.elapsed_time(e))
     ms = float(np.median(ts))
-    return {"cfg": cfg, "n": n, "ms": ms, "inst_per_s": n / ms * 1e3, "E_sum": float(res["E"].sum().item())}
+    return {"cfg": cfg + ("" if mode == J.MODE_FULL else "_mode%d" % mode), "n": n, "ms": ms, "inst_per_s": n / ms * 1e3, "E_sum": float(res["E"].sum().item())}
 
 
 def t_stats(cfg, n):
@@ -104,7 +105,8 @@ if __name__ == "__main__":
     todo = {"c2": lambda: t_solve("c2", 1 << 20), "c3": lambda: t_solve("c3", 100_000),
             "c5": lambda: t_solve("c5", 1_000_000), "bf": lambda: t_bf(0.25),
             "og": lambda: t_grouped("c3", 100_000), "eval": lambda: t_eval("c2", 1 << 20),
-            "stats": lambda: t_stats("c2", 1 << 20), "stats5": lambda: t_stats("c5", 1_000_000)}
+            "stats": lambda: t_stats("c2", 1 << 20), "c2lc": lambda: t_solve("c2", 1 << 20, J.MODE_LC),
+            "c2noedge": lambda: t_solve("c2", 1 << 20, J.MODE_NO_EDGE_DVFS), "stats5": lambda: t_stats("c5", 1_000_000)}
     for r in (todo[w]() for w in which):
         r["lib"] = os.path.basename(lib)
         print(json.dumps(r), flush=True)
