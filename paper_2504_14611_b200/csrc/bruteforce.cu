@@ -134,10 +134,28 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
         double *sEl = sm + 5 * NM, *sFmin = sEl + 32, *sFmax = sEl + 64, *sT = sEl + 96;
         double *sInv = sEl + 128;
         double *sSuf = sInv + kInvTab;  // [17][kBfThreads] per-lane suffix sums (N <= 15 path)
+        double *sSlb = sSuf + 17 * kBfThreads, *sPlb = sSlb + 64;  // [nmin] lower bounds of S_{nmin+1}, Psi
         const long long kt = k < kInvTab ? k : kInvTab;
         for (int x = threadIdx.x; x < 5 * NM; x += blockDim.x) sm[x] = tab[x];
         for (int x = threadIdx.x; x < 128; x += blockDim.x) sEl[x] = user[x];
         for (long long x = threadIdx.x; x < kt; x += blockDim.x) sInv[x] = invtab[x];
+        if (threadIdx.x == 0) {
+            // For a vector whose first offloaded sub-task is nmin + 1, b_n >= 1 exactly for n > nmin and
+            // b_n = 0 below, so S_{nmin+1} = RN-sum_{n=N..nmin+1} d_n(b_n) A_n >= the same RN-sum of
+            // d_n(1) A_n (d non-decreasing in b, R19; RN monotone) and Psi >= the RN-sum of
+            // min_{1<=b<=M} c_n(b) A_n, in the literal loop's order (descending n).
+            double S = 0.0, P = 0.0;
+            sSlb[N] = 0.0;
+            sPlb[N] = 0.0;
+            for (int n = N; n >= 1; n--) {
+                double cm = md.cA[n * B1 + 1];
+                for (int bb = 2; bb <= M; bb++) cm = (md.cA[n * B1 + bb] < cm) ? md.cA[n * B1 + bb] : cm;
+                S = S + md.dA[n * B1 + 1];
+                P = P + cm;
+                sSlb[n - 1] = S;
+                sPlb[n - 1] = P;
+            }
+        }
         __syncthreads();
         if (idx_end > size) idx_end = size;
         if (idx_begin < idx_end) {
@@ -201,11 +219,6 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                 const double inc = __longlong_as_double(*(volatile long long *)&hdr->best_bits);
                 if (lbu >= bestE || lbu > inc) continue;  // the edge term only adds (>= 0)
 #endif
-                // batch sizes, suffix sums S_n and Psi (descending n), per-user S_{n_m + 1}
-                double Sm[MAXM];
-#pragma unroll
-                for (int m = 0; m < MAXM; m++) Sm[m] = 0.0;
-                double S = 0.0, Psi = 0.0, Smin = 0.0;
                 int nmin = N;
                 double l_o = dinf();
 #pragma unroll
@@ -216,6 +229,28 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                         if (T < l_o) l_o = T;
                     }
                 }
+                const unsigned long long jlo = (vec == vb) ? idx_begin - vb * uk : 0ull;
+                const unsigned long long jhi = (vec == ve - 1) ? idx_end - (ve - 1) * uk : uk;
+#if JDOB_BF_PRUNE
+                // The vector bound below with S_{nmin+1} and Psi replaced by their lower bounds from
+                // nmin alone (sSlb, sPlb): skips most vectors before the batch-size and suffix sums
+                {
+                    double fel = grid_fe(fe_max, rho, (long long)(jhi - 1));
+                    if (nmin < N) {
+                        const double X = __dmul_ru(__dadd_ru(__dmul_ru(l_o, 0x1.0000000000001p+0), -t_free),
+                                                   0x1.0000000000004p+0);
+                        const double fd = div_lb(sSlb[nmin], X);  // <= S_{nmin+1} / X
+                        fel = (fd > fel) ? fd : fel;
+                    }
+                    const double LB = lbu + (sPlb[nmin] * fel) * fel;
+                    if (LB >= bestE || LB > inc) continue;
+                }
+#endif
+                // batch sizes, suffix sums S_n and Psi (descending n), per-user S_{n_m + 1}
+                double Sm[MAXM];
+#pragma unroll
+                for (int m = 0; m < MAXM; m++) Sm[m] = 0.0;
+                double S = 0.0, Psi = 0.0, Smin = 0.0;
                 if (M <= 15 && N <= 15) {
                     // digit histogram in 4-bit fields: b_n = M - #{m : n_m >= n}, accumulated while n
                     // descends; S_n kept per lane in shared memory and read back at n_m + 1
@@ -274,8 +309,6 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                         }
                     }
                 }
-                const unsigned long long jlo = (vec == vb) ? idx_begin - vb * uk : 0ull;
-                const unsigned long long jhi = (vec == ve - 1) ? idx_end - (ve - 1) * uk : uk;
 #if JDOB_BF_PRUNE
                 // Vector bound (exact, DESIGN.md §4 "brute-force bound").  Every candidate the literal
                 // scan evaluates passes D6': RN(t_free + RN(Smin RN(1/f_e))) <= l_o, which implies
@@ -498,7 +531,7 @@ void launch_bruteforce_impl(const DevModel *models, const DevBatch &b, int model
     long long *part_idx = (long long *)p;
     k_bf_setup<<<1, 32, 0, s>>>(models, b, space, hdr, tab, user, inv);
     const int Mc = (M >= 1 && M <= kMaxM) ? M : 1;
-    const size_t smem = sizeof(double) * (5 * (size_t)(N + 1) * Mc + 128 + kInvTab + 17 * kBfThreads);
+    const size_t smem = sizeof(double) * (5 * (size_t)(N + 1) * Mc + 128 + kInvTab + 17 * kBfThreads + 128);
     if (Mc == 8)
         launch_main<8, true>(models, model_id, space, idx_begin, idx_end, hdr, tab, user, inv, part_E, part_idx, smem,
                              s);
