@@ -84,7 +84,13 @@ __device__ __forceinline__ double clampf(double G, double fmin, double fmax) {
 // a / b for b > 0 finite.  A zero numerator sends the correctly rounded division to its slow
 // path (~140 instructions: the fast path's exponent test fails for a zero quotient), and
 // 0 / b = 0 with a's sign, i.e. a itself: same bits, no division.  zeta v_0 = 0 at n~ = 0.
-__device__ __forceinline__ double div_z(double a, double b) { return (a == 0.0) ? a : a / b; }
+// (The compiler if-converts "a == 0 ? a : a / b" and divides anyway, so the zero numerator is
+// replaced by 1 before the division and the quotient discarded.)
+__device__ __forceinline__ double div_z(double a, double b) {
+    const bool z = (a == 0.0);
+    const double q = (z ? 1.0 : a) / b;
+    return z ? a : q;
+}
 
 // RD(1 / x) for x > 0 (the bound of DESIGN.md §4 "n~ pruning"), without the div_rd subroutine:
 // q = RN(1 / x); if q x - 1 > 0 exactly (the sign of the fma) then q > 1/x and RD(1/x) is q's
