@@ -132,6 +132,12 @@ __device__ __forceinline__ long long grid_k(double fe_min, double fe_max, double
     return j;
 }
 
+// Per-warp cache of the grid length k for the last (f_e,min, f_e,max, rho) seen (shared memory).
+struct GridKCache {
+    double fe_min, fe_max, rho;
+    long long k;
+};
+
 struct InstRegs {  // lane-resident user parameters (lane = user)
     double z, k, f0, f1, R, p, T;
 };
@@ -145,7 +151,7 @@ struct InstRegs {  // lane-resident user parameters (lane = user)
 // model checks so that their latency overlaps the model-table loads.
 __device__ __forceinline__ int warp_validate_pre(const DevModel *models, const DevBatch &b, long long i, int lane,
                                                  long long off, long long M64, int mid, InstRegs &x, int &M,
-                                                 long long &k, const DevModel *&mdp) {
+                                                 long long &k, const DevModel *&mdp, GridKCache *kc = nullptr) {
     M = (M64 >= 1 && M64 <= kMaxM) ? (int)M64 : 0;
     k = 0;
     x.z = x.k = x.f0 = x.f1 = x.R = x.p = 0.0;
@@ -192,7 +198,18 @@ __device__ __forceinline__ int warp_validate_pre(const DevModel *models, const D
     if (!(dfinite(t_free) && dfinite(fe_min) && dfinite(fe_max) && dfinite(rho) && (t_free >= 0.0) &&
           (fe_min > 0.0) && (fe_min <= fe_max) && (rho > 0.0)))
         return JDOB_ST_BADPARAM;
-    k = grid_k(fe_min, fe_max, rho);
+    if (kc) {  // warp-uniform: every lane reads the cache before lane 0 may rewrite it
+        const bool hit = __all_sync(0xffffffffu, kc->fe_min == fe_min && kc->fe_max == fe_max && kc->rho == rho);
+        if (hit) {
+            k = kc->k;
+        } else {
+            __syncwarp();
+            k = grid_k(fe_min, fe_max, rho);
+            if (lane == 0) *kc = GridKCache{fe_min, fe_max, rho, k};
+        }
+    } else {
+        k = grid_k(fe_min, fe_max, rho);
+    }
     if (k > kMaxK) return JDOB_ST_BADPARAM;
     const double vN = mdp->v[mdp->N];
     // P:127 literally RN(zeta v_N / f_max) > T; when T f_max - zeta v_N > 0 exactly (the fma's sign)

@@ -59,6 +59,7 @@ struct SolveSmem {
     double inv[kInvCache];
     double2 inv_key;                     // (f_e,max, rho) of the cached 1/f_e(j), j < inv_n
     int inv_n;
+    GridKCache kc;                       // k of the last (f_e,min, f_e,max, rho)
     double rinv[kMaxM];                  // RD(1 / R_m): lower-bound upload term
     double lb[64];                       // per n~: lower bound of every configuration's energy
 };
@@ -202,7 +203,7 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     int M;
     const DevModel *mdp;
     InstRegs x;
-    const int st = warp_validate_pre(models, b, i, lane, off, M64, mid, x, M, k, mdp);
+    const int st = warp_validate_pre(models, b, i, lane, off, M64, mid, x, M, k, mdp, &s.kc);
     if (st == kStDefer) return;  // M > 32: solved by k_solve_large (solve_large.cu)
     const double t_free = b.t_free[i], fe_max = b.fe_max[i], rho = b.rho[i];
     if (st == JDOB_ST_BADPARAM || st == JDOB_ST_BADMODEL) {
@@ -575,6 +576,7 @@ __global__ void __launch_bounds__(kSolveWarps * 32, UNI ? JDOB_SOLVE_MINB_U : JD
     if (lane == 0) {
         s.inv_key = make_double2(0.0, 0.0);  // rho > 0 in every valid instance: no false hit
         s.inv_n = 0;
+        s.kc = GridKCache{0.0, 0.0, 0.0, 0};  // rho > 0 in every valid instance: no false hit
     }
     __syncwarp();
     const long long gw = (long long)blockIdx.x * kSolveWarps + (threadIdx.x >> 5);
