@@ -92,6 +92,23 @@ def test_random_uniform_users(J, seed, M_hi, N_hi, k_max):
 
 
 @pytest.mark.parametrize("uniform", [False, True])
+def test_grid_length_cache(J, uniform):
+    """K1 caches k per warp keyed by (f_e,min, f_e,max, rho): instances that share f_e,max and rho but
+    not f_e,min (different k), interleaved so that every warp meets several grids in turn, and runs
+    of equal grids (cache hits).  C2-sized batch so the persistent warps take many instances each."""
+    b = g.config_batch("c2", n_inst=40000)
+    if not uniform:  # user 0 of every instance gets its own kappa: the general kernel
+        b.kappa[b.user_off[:-1]] *= 1.5
+    rng = np.random.default_rng(11)
+    choices = np.array([0.2e9, 0.2e9, 0.5e9, 1.3e9, 2.05e9])      # k = 64, 64, 54, 27, 2 at rho = 30 MHz
+    b.fe_min = choices[rng.integers(0, len(choices), b.n_inst)]
+    b.fe_min[: b.n_inst // 4] = 0.5e9                                # a long run of one grid
+    _, gpu = run(J, b, counts=False)
+    orc = O.solve_batch(b)
+    assert_solve_parity(gpu, orc, counts=False)
+
+
+@pytest.mark.parametrize("uniform", [False, True])
 def test_deep_models_and_long_grids(J, uniform):
     """N > 32 (two n~ bounds per lane, two-word candidate ballots), grids longer than the 1/f_e cache
     (k up to 300 > 192), M up to 32: literal, pruned and executed-work sweeps against the oracle."""
