@@ -153,8 +153,9 @@ def ncu_traffic(kernel):
         return None
 
 
-def cpu_baseline(batch, seconds, label):
-    """The oracle, as it stands, on a bounded sample of the same workload, all host cores."""
+def cpu_baseline(batch, seconds, label, gpu_host=None):
+    """The oracle, as it stands, on a bounded sample of the same workload, all host cores; its results
+    are then compared bit for bit with the GPU's for the same instances (parity of the bench run)."""
     import oracle as O
     cores = os.cpu_count() or 1
     probe = batch.subset(0, min(batch.n_inst, 2000))
@@ -164,10 +165,21 @@ def cpu_baseline(batch, seconds, label):
     n = int(min(batch.n_inst, max(probe.n_inst, rate * seconds)))
     sub = batch.subset(0, n)
     t0 = time.perf_counter()
-    O.solve_batch(sub, threads=cores)
+    orc = O.solve_batch(sub, threads=cores)
     dt = time.perf_counter() - t0
+    parity = None
+    if gpu_host is not None:
+        bad = 0
+        for f, g in gpu_host.items():
+            a, o = g[:n], np.asarray(orc[f])
+            if a.dtype == np.float64:
+                bad += int((a.view(np.int64) != o.view(np.int64)).sum())
+            else:
+                bad += int((a.view(np.int32) != o.astype(a.dtype).view(np.int32)).sum())
+        parity = (f"{n}/{n} instances of the cpu_baseline sample bit-exact vs oracle" if bad == 0
+                  else f"MISMATCH: {bad} differing fields in the {n}-instance cpu_baseline sample")
     return {"value": n / dt, "unit": "instances/s", "cores": cores, "kind": "oracle",
-            "sample": f"first {n} instances of {label} ({dt:.1f} s, C oracle -O2, {cores} threads)"}
+            "sample": f"first {n} instances of {label} ({dt:.1f} s, C oracle -O2, {cores} threads)"}, parity
 
 
 def bf_leg(J, torch, world, rank, reps, dist):
@@ -240,20 +252,12 @@ def run_mine(args):
     wk = J.solve_batch(db, work=True, f_user=False)["work"].cpu().numpy()
     work, n_member_exec = fp64_work(batch, wk[:, 1:], setups=wk[:, 0], lower_bound=True)
     setup_frac = float(wk[:, 0].sum()) / float(sum(batch.models[m].N for m in batch.model_id))
-    # parity spot check against the oracle on 64 sampled instances (rank 0)
-    parity = None
-    if rank == 0:
-        import oracle as O
-        idx = np.linspace(0, n - 1, 64).astype(np.int64)
-        orc = O.solve_batch(batch.take(idx))
-        ok = all(np.array_equal(res_c[f].cpu().numpy()[idx].view(np.int64 if res_c[f].dtype == torch.float64
-                                                                       else np.int32),
-                                orc[f].view(np.int64 if orc[f].dtype == np.float64 else np.int32))
-                 for f in ("E", "t_free_next", "f_e", "n_tilde", "j", "status", "mask"))
-        parity = f"{'64/64' if ok else 'MISMATCH'} sampled instances bit-exact vs oracle"
     del res_c
 
     res = J.solve_batch(db, stats=True, n_buckets=n_buckets, f_user=False)
+    # the product path's decisions for the whole batch, on the host: the cpu_baseline leg compares
+    # its oracle sample with them (the only place the bench run meets the oracle)
+    gpu_host = {f: res[f].cpu().numpy() for f in ("E", "t_free_next", "f_e", "n_tilde", "j", "status", "mask")}
     ev = J.eval_plans(db, plans=res, f_user=False)
     stream = torch.cuda.current_stream()
 
@@ -332,9 +336,9 @@ def run_mine(args):
     if not args.no_bf:
         bf = bf_leg(J, torch, world, rank, args.bf_reps, dist)
 
-    cpu = None
+    cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(batch, args.cpu_seconds, label)
+        cpu, parity = cpu_baseline(batch, args.cpu_seconds, label, gpu_host)
 
     if rank == 0:
         peak_clk = (clk or {}).get("sm_max_mhz") or 1965.0
