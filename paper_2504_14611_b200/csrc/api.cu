@@ -407,7 +407,10 @@ int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob
     keep_pool_warm();
     const long long n = b->n_inst;
     const long long nu = n > 0 ? (long long)b->user_off[n] : 0;
-    constexpr int NS = 2;  // copy/compute pipeline depth
+#ifndef JDOB_HOST_NS
+#define JDOB_HOST_NS 2
+#endif
+    constexpr int NS = JDOB_HOST_NS;  // copy/compute pipeline depth
     // device layout: model tables | batch | outputs | NS workspaces
     size_t bytes = 0;
     for (int i = 0; i < n_models; i++) {
@@ -492,13 +495,29 @@ int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob
         cudaEventCreateWithFlags(&evs[k], cudaEventDisableTiming);
         cudaStreamWaitEvent(st[k], ev0, 0);
     }
-    const long long per = 131072;
-    long long nchunks = (n + per - 1) / per;
-    if (nchunks < 1) nchunks = 1;
-    if (nchunks > 64) nchunks = 64;
-    for (long long c = 0; c < nchunks && rc == JDOB_OK; c++) {
+#ifndef JDOB_HOST_CHUNK
+#define JDOB_HOST_CHUNK 131072
+#endif
+    // chunk boundaries: JDOB_HOST_CHUNK instances each, then a geometric tail (halving, >= 16384) so
+    // that the solve and copy-out left after the last copy-in are short
+    long long per = JDOB_HOST_CHUNK;
+    if (n > 48 * per) per = (n + 47) / 48;
+    long long bounds[72];
+    int nchunks = 0;
+    bounds[0] = 0;
+    for (long long pos = 0; pos < n && nchunks < 70;) {
+        const long long rem = n - pos;
+        long long sz = per;
+#ifndef JDOB_HOST_NO_TAIL
+        if (rem <= 2 * per) sz = (rem / 2 > 16384) ? rem / 2 : 16384;
+#endif
+        if (sz > rem || nchunks == 69) sz = rem;
+        pos += sz;
+        bounds[++nchunks] = pos;
+    }
+    for (int c = 0; c < nchunks && rc == JDOB_OK; c++) {
         cudaStream_t ss = st[c % NS];
-        const long long i0 = n * c / nchunks, i1 = n * (c + 1) / nchunks;
+        const long long i0 = bounds[c], i1 = bounds[c + 1];
         if (i1 <= i0) continue;
         const long long u0 = b->user_off[i0], u1 = b->user_off[i1];
         auto h2 = [&](const void *dst, const void *src, size_t nb) {
