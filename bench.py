@@ -331,6 +331,19 @@ def run_mine(args):
         e2e = {"value": world * n * reps / (ms / 1e3), "unit": "instances/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "api": "jdob_solve_batch_host (pinned host buffers)", "reps": reps}
         del hb
+        # copy roof: one plain pinned host -> device copy of the same number of bytes (no kernels)
+        hx = torch.empty(int(h2d), dtype=torch.uint8).pin_memory()
+        dx = torch.empty(int(h2d), dtype=torch.uint8, device="cuda")
+        dx.copy_(hx, non_blocking=True)
+        torch.cuda.synchronize()
+        s.record(stream)
+        dx.copy_(hx, non_blocking=True)
+        e.record(stream)
+        torch.cuda.synchronize()
+        roof_ms = s.elapsed_time(e)
+        e2e["h2d_copy_roof"] = {"ms": roof_ms, "gbs": h2d / (roof_ms / 1e3) / 1e9,
+                                "frac": roof_ms / (ms / reps)}
+        del hx, dx
 
     bf = None
     if not args.no_bf:
