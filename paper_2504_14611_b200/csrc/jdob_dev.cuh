@@ -84,11 +84,14 @@ __device__ __forceinline__ double clampf(double G, double fmin, double fmax) {
 // a / b for b > 0 finite.  A zero numerator sends the correctly rounded division to its slow
 // path (~140 instructions: the fast path's exponent test fails for a zero quotient), and
 // 0 / b = 0 with a's sign, i.e. a itself: same bits, no division.  zeta v_0 = 0 at n~ = 0.
-// (The compiler if-converts "a == 0 ? a : a / b" and divides anyway, so the zero numerator is
-// replaced by 1 before the division and the quotient discarded.)
+// (The compiler if-converts "a == 0 ? a : a / b" and divides anyway, and it folds a numerator
+// select back to a / b, so the zero numerator is replaced by 1 behind an opaque move before the
+// division and that quotient discarded.)
 __device__ __forceinline__ double div_z(double a, double b) {
     const bool z = (a == 0.0);
-    const double q = (z ? 1.0 : a) / b;
+    double n;
+    asm("mov.b64 %0, %1;" : "=d"(n) : "d"(z ? 1.0 : a));
+    const double q = n / b;
     return z ? a : q;
 }
 
