@@ -116,7 +116,11 @@ __global__ void k_eval(const DevModel *models, DevBatch b, const int *partition,
         }
     }
     const double fe = f_e[i];
-    const double inv = 1.0 / fe;
+    // f_e = 0 marks an all-local plan (R18); 1 / f_e is only used with members, so without members
+    // the divisor is 1 (behind an opaque move: no slow-path division of 1 / 0)
+    double fe_d;
+    asm("mov.b64 %0, %1;" : "=d"(fe_d) : "d"(any ? fe : 1.0));
+    const double inv = 1.0 / fe_d;
     const double tol = slack * fabs(l_o);
     double tf = t_free;
     if (any) {

@@ -95,6 +95,16 @@ __device__ __forceinline__ double div_z(double a, double b) {
     return z ? a : q;
 }
 
+// a / b where a zero numerator over a positive finite b returns a (the quotient's exact value)
+// without the slow path; every other case is the literal a / b (0 / 0 = NaN, x / 0 = inf, ...).
+__device__ __forceinline__ double div_z0(double a, double b) {
+    const bool z = (a == 0.0) && (b > 0.0) && (b <= 1.7976931348623157e308);
+    double n;
+    asm("mov.b64 %0, %1;" : "=d"(n) : "d"(z ? 1.0 : a));
+    const double q = n / b;
+    return z ? a : q;
+}
+
 // RD(1 / x) for x > 0 (the bound of DESIGN.md §4 "n~ pruning"), without the div_rd subroutine:
 // q = RN(1 / x); if q x - 1 > 0 exactly (the sign of the fma) then q > 1/x and RD(1/x) is q's
 // predecessor (no representable number lies strictly between RD and RN when they differ),

@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(32) k_stats_partial(DevBatch b, DevResult r, d
             }
             const double E = Eq[q], El = Lq[q];
             const int M = Mq[q];
-            const double rr = 100.0 * (El - E) / El;
+            const double rr = div_z0(100.0 * (El - E), El);  // E = E_LC: 0 without the slow path
             double *a = fs + (size_t)bk * kLaneF * 32 + lane;
             a[0 * 32] = a[0 * 32] + rr;
             a[1 * 32] = a[1 * 32] + rr * rr;
