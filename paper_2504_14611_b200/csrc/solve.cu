@@ -529,7 +529,7 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     const int Bo = M - bP;
     const double lo_ = s.Lg[bP].x;
     const double fe = grid_fe(fe_max, rho, bJ);
-    const double inv = 1.0 / fe;
+    const double inv = (bJ < kInvCache) ? s.inv[bJ] : 1.0 / fe;  // the sweep's cached 1/f_e(j), same bits
     const double te = md.phi[bN * B1 + Bo] * inv;
     const bool member = (lane < M) && (s.rank[lane] >= bP);
     double f = floc, arr = t_free;
