@@ -388,8 +388,8 @@ __device__ void large_instance(long long i, const DevModel *models, const DevBat
             const double2 a = s.orzv[m], t = s.fmm[m];
             const double budget = (lo_ - a.x) - te;
             const bool low = (a.y == 0.0) || (__fma_rn(t.x, budget, -a.y) > 0.0);
-            f = low ? t.x : clampf(a.y / budget, t.x, t.y);
-            const double arr = a.y / f + a.x;
+            f = low ? t.x : clampf(div_z(a.y, budget), t.x, t.y);  // zv = 0 (n~ = 0): no slow-path 0 / budget
+            const double arr = div_z(a.y, f) + a.x;
             arr_max = (arr > arr_max) ? arr : arr_max;
         } else {
             f = clampf((b.zeta[u] * vN) / b.T[u], b.f_min[u], b.f_max[u]);
