@@ -157,6 +157,37 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
             }
         }
         __syncthreads();
+#if JDOB_BF_PRUNE && !defined(JDOB_BF_NO_DVFS_LB)
+        // Offloader terms of the user bound with the deadline-driven device frequency (exact for the
+        // brute force, whose infeasible candidates are skipped): an evaluated candidate with user m
+        // offloading at n has budget = RN(RN(l_o - O/R) - RN(S_{n+1} RN(1/f_e))) <= X =
+        // RN(RN(T_m - O/R) - RN(Slb[n] RN(1/f_e,max))) (l_o <= T_m, S_{n+1} >= Slb[n], f_e <=
+        // f_e,max), and either f* = f_min with zv / X < f_min, or f* = RN(zv / budget) >=
+        // RN(zv / X) with 0 < budget <= X; X <= 0 or RN(zv / X) > f_max leave no feasible candidate.
+        {
+            const double inv_max = sInv[0];  // RN(1 / f_e(0)) = RN(1 / f_e,max)
+            for (int x = threadIdx.x; x < N * M; x += blockDim.x) {
+                const int n = x / M, m = x % M;
+                const double zv = sZV[x];
+                if (zv == 0.0) continue;  // f* = f_min (R9): the f_min term stands
+                const double X = (sT[m] - sOR[x]) - sSlb[n] * inv_max;
+                double t;
+                if (!(X > 0.0)) {
+                    t = dinf();
+                } else {
+                    const double g = zv / X, fm = sFmin[m];
+                    if (g > sFmax[m]) {
+                        t = dinf();
+                    } else {
+                        const double f = (g > fm) ? g : fm;
+                        t = ((sKU[x] * f) * f) + sUP[x];
+                    }
+                }
+                sLB[x] = t;
+            }
+        }
+        __syncthreads();
+#endif
         if (idx_end > size) idx_end = size;
         if (idx_begin < idx_end) {
             const unsigned long long uk = (unsigned long long)k;
