@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
         double *sInv = sEl + 128;
         double *sSuf = sInv + kInvTab;  // [17][kBfThreads] per-lane suffix sums (N <= 15 path)
         double *sSlb = sSuf + 17 * kBfThreads, *sPlb = sSlb + 64;  // [nmin] lower bounds of S_{nmin+1}, Psi
+        double *sG = sPlb + 64;  // [n][m] lower bound of user m's arrival O/R + zv/f* when offloading at n
         const long long kt = k < kInvTab ? k : kInvTab;
         for (int x = threadIdx.x; x < 5 * NM; x += blockDim.x) sm[x] = tab[x];
         for (int x = threadIdx.x; x < 128; x += blockDim.x) sEl[x] = user[x];
@@ -157,6 +158,22 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
             }
         }
         __syncthreads();
+#if JDOB_BF_PRUNE
+        // Arrival lower bounds for the D7' f_e bound.  A feasible candidate has budget > 0 (>= 0 when
+        // zv = 0) and RN(zv / budget) <= f_max, which with budget = RN(RN(l_o - O/R) - RN(S RN(1/f_e)))
+        // gives S / f_e <= ((l_o - O/R)(1 + u) - (zv / f_max)(1 - 2u)) / (1 - u)^2 (u = 2^-53).  With
+        // G = RN(O/R + RN(zv RD(1/f_max))) (1 - 2^-46) <= (O/R + zv/f_max)(1 - 2^-47) and the margins
+        // of X below, S / X <= f_e for every feasible candidate.
+        for (int x = threadIdx.x; x < N * M; x += blockDim.x) {
+            const int m = x % M;
+#ifndef JDOB_BF_NO_D7_FE
+            sG[x] = (sOR[x] + sZV[x] * recip_rd(sFmax[m])) * (1.0 - 0x1p-46);
+#else
+            sG[x] = 0.0;
+#endif
+        }
+        __syncthreads();
+#endif
 #if JDOB_BF_PRUNE && !defined(JDOB_BF_NO_DVFS_LB)
         // Offloader terms of the user bound with the deadline-driven device frequency (exact for the
         // brute force, whose infeasible candidates are skipped): an evaluated candidate with user m
@@ -268,8 +285,13 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                 {
                     double fel = grid_fe(fe_max, rho, (long long)(jhi - 1));
                     if (nmin < N) {
-                        const double X = __dmul_ru(__dadd_ru(__dmul_ru(l_o, 0x1.0000000000001p+0), -t_free),
-                                                   0x1.0000000000004p+0);
+                        // D6' (t_free) and D7' of the users offloading at nmin (their arrival): f_e >=
+                        // S_{nmin+1} / (l_o - max(t_free, arrival)) up to rounding, covered by the margins
+                        double gmax = t_free;
+#pragma unroll
+                        for (int m = 0; m < MAXM; m++)
+                            if (m < M && nv[m] == nmin) gmax = (sG[nmin * M + m] > gmax) ? sG[nmin * M + m] : gmax;
+                        const double X = __dmul_ru(__dadd_ru(__dmul_ru(l_o, 1.0 + 0x1p-48), -gmax), 1.0 + 0x1p-48);
                         const double fd = div_lb(sSlb[nmin], X);  // <= S_{nmin+1} / X
                         fel = (fd > fel) ? fd : fel;
                     }
@@ -355,8 +377,11 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                         const double fe0 = grid_fe(fe_max, rho, (long long)jlo);
                         const double inv0 = (jlo < (unsigned long long)kt) ? sInv[jlo] : 1.0 / fe0;
                         if (!(t_free + Smin * inv0 <= l_o)) continue;  // D6' fails at once: no candidate
-                        const double X = __dmul_ru(__dadd_ru(__dmul_ru(l_o, 0x1.0000000000001p+0), -t_free),
-                                                   0x1.0000000000004p+0);
+                        double gmax = t_free;
+#pragma unroll
+                        for (int m = 0; m < MAXM; m++)
+                            if (m < M && nv[m] == nmin) gmax = (sG[nmin * M + m] > gmax) ? sG[nmin * M + m] : gmax;
+                        const double X = __dmul_ru(__dadd_ru(__dmul_ru(l_o, 1.0 + 0x1p-48), -gmax), 1.0 + 0x1p-48);
                         const double fd = div_lb(Smin, X);  // <= Smin / X
                         fel = (fd > fel) ? fd : fel;
                     }
@@ -562,7 +587,8 @@ void launch_bruteforce_impl(const DevModel *models, const DevBatch &b, int model
     long long *part_idx = (long long *)p;
     k_bf_setup<<<1, 32, 0, s>>>(models, b, space, hdr, tab, user, inv);
     const int Mc = (M >= 1 && M <= kMaxM) ? M : 1;
-    const size_t smem = sizeof(double) * (5 * (size_t)(N + 1) * Mc + 128 + kInvTab + 17 * kBfThreads + 128);
+    const size_t smem = sizeof(double) * (5 * (size_t)(N + 1) * Mc + 128 + kInvTab + 17 * kBfThreads + 128 +
+                                          (size_t)(N + 1) * Mc);
     if (Mc == 8)
         launch_main<8, true>(models, model_id, space, idx_begin, idx_end, hdr, tab, user, inv, part_E, part_idx, smem,
                              s);
