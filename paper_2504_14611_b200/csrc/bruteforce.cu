@@ -279,6 +279,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                 }
                 const unsigned long long jlo = (vec == vb) ? idx_begin - vb * uk : 0ull;
                 const unsigned long long jhi = (vec == ve - 1) ? idx_end - (ve - 1) * uk : uk;
+                double Xd7 = 0.0;  // the D6'/D7' denominator of this vector (set when it has offloaders)
 #if JDOB_BF_PRUNE
                 // The vector bound below with S_{nmin+1} and Psi replaced by their lower bounds from
                 // nmin alone (sSlb, sPlb): skips most vectors before the batch-size and suffix sums
@@ -291,8 +292,8 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
 #pragma unroll
                         for (int m = 0; m < MAXM; m++)
                             if (m < M && nv[m] == nmin) gmax = (sG[nmin * M + m] > gmax) ? sG[nmin * M + m] : gmax;
-                        const double X = __dmul_ru(__dadd_ru(__dmul_ru(l_o, 1.0 + 0x1p-48), -gmax), 1.0 + 0x1p-48);
-                        const double fd = div_lb(sSlb[nmin], X);  // <= S_{nmin+1} / X
+                        Xd7 = __dmul_ru(__dadd_ru(__dmul_ru(l_o, 1.0 + 0x1p-48), -gmax), 1.0 + 0x1p-48);
+                        const double fd = div_lb(sSlb[nmin], Xd7);  // <= S_{nmin+1} / X
                         fel = (fd > fel) ? fd : fel;
                     }
                     const double LB = lbu + (sPlb[nmin] * fel) * fel;
@@ -377,12 +378,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                         const double fe0 = grid_fe(fe_max, rho, (long long)jlo);
                         const double inv0 = (jlo < (unsigned long long)kt) ? sInv[jlo] : 1.0 / fe0;
                         if (!(t_free + Smin * inv0 <= l_o)) continue;  // D6' fails at once: no candidate
-                        double gmax = t_free;
-#pragma unroll
-                        for (int m = 0; m < MAXM; m++)
-                            if (m < M && nv[m] == nmin) gmax = (sG[nmin * M + m] > gmax) ? sG[nmin * M + m] : gmax;
-                        const double X = __dmul_ru(__dadd_ru(__dmul_ru(l_o, 1.0 + 0x1p-48), -gmax), 1.0 + 0x1p-48);
-                        const double fd = div_lb(Smin, X);  // <= Smin / X
+                        const double fd = div_lb(Smin, Xd7);  // <= Smin / X (X of the n_min-only bound)
                         fel = (fd > fel) ? fd : fel;
                     }
                     const double LB = lbu + (Psi * fel) * fel;
