@@ -209,22 +209,28 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
         if (idx_begin < idx_end) {
             const unsigned long long uk = (unsigned long long)k;
             const unsigned long long vb = idx_begin / uk, ve = (idx_end + uk - 1) / uk;
-            const unsigned long long nvec = ve - vb;
-            const unsigned long long nchunks = (nvec + 31) / 32;
+            // General space: a lane takes a block of radix consecutive vectors that differ only in the
+            // last user's digit (the least significant one), so the other digits, their bound terms and
+            // their n_min / l_o are formed once per block; blocks advance by 32 nw per step through a
+            // mixed-radix add of the stride's digits (64-bit division only here).  Identical space:
+            // one vector per lane and step.  Either way a lane visits its vectors in increasing order.
+            const int radix = N + 1;
+            const bool blk = (space == 0);
+            const int L = blk ? radix : 1;
+            const unsigned long long ubeg = blk ? vb / (unsigned long long)radix : vb;
+            const unsigned long long uend = blk ? (ve + radix - 1) / (unsigned long long)radix : ve;
+            const unsigned long long nchunks = (uend - ubeg + 31) / 32;
             const unsigned long long gw = (unsigned long long)blockIdx.x * kBfWarps + w;
             const unsigned long long nw = (unsigned long long)gridDim.x * kBfWarps;
             const double *dA = md.dA, *cA = md.cA;
-            const int radix = N + 1;
-            // General space: the lane's vector advances by 32 nw per step, so its digits are kept and
-            // advanced by a mixed-radix add of the stride's digits (64-bit division only twice, here)
-            int dig[MAXM], sdig[MAXM];
+            int dig[MAXM], sdig[MAXM];  // digits of the block index: users 0 .. M-2 (dig[M-1] unused)
             {
-                unsigned long long t = vb + gw * 32 + lane, u = 32ull * nw;
+                unsigned long long t = ubeg + gw * 32 + lane, u = 32ull * nw;
 #pragma unroll
                 for (int m = MAXM - 1; m >= 0; m--) {
                     dig[m] = 0;
                     sdig[m] = 0;
-                    if (m < M && space == 0) {
+                    if (m < M - 1 && blk) {
                         dig[m] = (int)(t % (unsigned long long)radix);
                         t /= (unsigned long long)radix;
                         sdig[m] = (int)(u % (unsigned long long)radix);
@@ -232,12 +238,12 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                     }
                 }
             }
-            auto advance = [&]() {  // dig += sdig (mod radix^M)
-                if (space != 0) return;
+            auto advance = [&]() {  // dig += sdig (mod radix^(M-1))
+                if (!blk) return;
                 int carry = 0;
 #pragma unroll
                 for (int m = MAXM - 1; m >= 0; m--) {
-                    if (m < M) {
+                    if (m < M - 1) {
                         const int d = dig[m] + sdig[m] + carry;
                         carry = d >= radix ? 1 : 0;
                         dig[m] = carry ? d - radix : d;
@@ -245,13 +251,32 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                 }
             };
             for (unsigned long long c = gw; c < nchunks; c += nw, advance()) {
-                const unsigned long long vec = vb + c * 32 + lane;
-                if (vec >= ve) continue;
+                const unsigned long long unit = ubeg + c * 32 + lane;
+                if (unit >= uend) continue;
+                // users 0 .. M-2 of the block (general space): bound terms in user order, n_min, l_o
+                double lbu_hi = 0.0, lo_hi = dinf();
+                int nmin_hi = N;
+                if (blk) {
+#pragma unroll
+                    for (int m = 0; m < MAXM; m++)
+                        if (m < M - 1) {
+#if JDOB_BF_PRUNE
+                            lbu_hi = lbu_hi + sLB[dig[m] * M + m];
+#endif
+                            if (dig[m] < N) {
+                                if (dig[m] < nmin_hi) nmin_hi = dig[m];
+                                lo_hi = (sT[m] < lo_hi) ? sT[m] : lo_hi;
+                            }
+                        }
+                }
+                for (int t = 0; t < L; t++) {
+                const unsigned long long vec = blk ? unit * (unsigned long long)radix + t : unit;
+                if (vec < vb || vec >= ve) continue;
                 // the partition vector
                 int nv[MAXM];
-                if (space == 0) {
+                if (blk) {
 #pragma unroll
-                    for (int m = 0; m < MAXM; m++) nv[m] = dig[m];
+                    for (int m = 0; m < MAXM; m++) nv[m] = (m == M - 1) ? t : dig[m];
                 } else {
                     const unsigned long long mask = vec & ((1ull << M) - 1ull);
                     const int nt = (int)(vec >> M);
@@ -259,22 +284,36 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                     for (int m = 0; m < MAXM; m++) nv[m] = (nt < N && ((mask >> m) & 1ull)) ? nt : N;
                 }
 #if JDOB_BF_PRUNE
-                // user terms of the vector bound first (table lookups): most vectors stop here
+                // user terms of the vector bound first (table lookups, in user order): most vectors
+                // stop here
                 double lbu = 0.0;
+                if (blk) {
+                    lbu = lbu_hi + sLB[t * M + (M - 1)];
+                } else {
 #pragma unroll
-                for (int m = 0; m < MAXM; m++)
-                    if (m < M) lbu = lbu + sLB[nv[m] * M + m];
+                    for (int m = 0; m < MAXM; m++)
+                        if (m < M) lbu = lbu + sLB[nv[m] * M + m];
+                }
                 const double inc = __longlong_as_double(*(volatile long long *)&hdr->best_bits);
                 if (lbu >= bestE || lbu > inc) continue;  // the edge term only adds (>= 0)
 #endif
                 int nmin = N;
                 double l_o = dinf();
+                if (blk) {
+                    nmin = nmin_hi;
+                    l_o = lo_hi;
+                    if (t < N) {
+                        if (t < nmin) nmin = t;
+                        l_o = (sT[M - 1] < l_o) ? sT[M - 1] : l_o;
+                    }
+                } else {
 #pragma unroll
-                for (int m = 0; m < MAXM; m++) {
-                    if (m < M && nv[m] < N) {
-                        if (nv[m] < nmin) nmin = nv[m];
-                        const double T = sT[m];
-                        if (T < l_o) l_o = T;
+                    for (int m = 0; m < MAXM; m++) {
+                        if (m < M && nv[m] < N) {
+                            if (nv[m] < nmin) nmin = nv[m];
+                            const double T = sT[m];
+                            if (T < l_o) l_o = T;
+                        }
                     }
                 }
                 const unsigned long long jlo = (vec == vb) ? idx_begin - vb * uk : 0ull;
@@ -503,6 +542,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                 if (bestE < best_before)  // publish the lane's new best as the shared incumbent
                     atomicMin(&hdr->best_bits, (unsigned long long)__double_as_longlong(bestE));
 #endif
+                }  // t: the vectors of the lane's block
             }
         }
     }
