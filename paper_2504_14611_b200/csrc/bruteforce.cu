@@ -425,12 +425,35 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                 }
                 const double best_before = bestE;
 #endif
+                unsigned long long j0 = jlo;
+#if JDOB_BF_PRUNE && !defined(JDOB_BF_NO_JSKIP)
+                // Edge-only skip of the high-f_e prefix: E(j) >= RN(lbu + RN(RN(Psi f_e(j)) f_e(j))),
+                // non-increasing in j, so the j with that bound >= the lane's best (larger indices lose
+                // ties) or > the incumbent form a prefix of [jlo, jhi); binary search for its end.
+                {
+                    const double thr = (bestE < inc) ? bestE : inc;  // skip iff b >= bestE or b > inc
+                    auto skip = [&](unsigned long long j) {
+                        const double fe = grid_fe(fe_max, rho, (long long)j);
+                        const double b = lbu + (Psi * fe) * fe;
+                        return b >= bestE || b > inc;
+                    };
+                    if (thr < dinf() && skip(jlo)) {
+                        unsigned long long lo = jlo + 1, hi = jhi;  // first non-skipped j in [lo, hi]
+                        while (lo < hi) {
+                            const unsigned long long mid = (lo + hi) >> 1;
+                            if (skip(mid)) lo = mid + 1;
+                            else hi = mid;
+                        }
+                        j0 = lo;
+                    }
+                }
+#endif
                 if constexpr (REG) {
                     // M <= 8: (A) budgets and the exact low-clamp test for every offloader, no
                     // branches; (B) the rare literal divisions / feasibility checks; (C) the energies
                     // in user order.  Keeping the branch out of the straight-line code lets the
                     // users' dependency chains overlap.
-                    for (unsigned long long j = jlo; j < jhi; j++) {
+                    for (unsigned long long j = j0; j < jhi; j++) {
                         const double fe = grid_fe(fe_max, rho, (long long)j);
                         const double inv = (j < (unsigned long long)kt) ? sInv[j] : 1.0 / fe;
                         if (any && !(t_free + Smin * inv <= l_o)) break;  // D6' (monotone in j)
@@ -477,7 +500,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                         }
                     }
                 } else {
-                for (unsigned long long j = jlo; j < jhi; j++) {
+                for (unsigned long long j = j0; j < jhi; j++) {
                         const double fe = grid_fe(fe_max, rho, (long long)j);
                         const double inv = (j < (unsigned long long)kt) ? sInv[j] : 1.0 / fe;
                         if (any && !(t_free + Smin * inv <= l_o)) break;  // D6' (monotone in j)
