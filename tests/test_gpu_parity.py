@@ -339,6 +339,33 @@ def test_bf_random_full_and_ranges(J):
                 assert int(I.item()) == Io
 
 
+def test_bf_tight_deadlines(J):
+    """Deadlines just above the local minimum (beta in [0, 0.6]) and t_free > 0: most candidates are
+    infeasible and the optimum sits near the feasibility boundary, where the exact vector bounds
+    (deadline-driven offloader terms, the D7'-implied f_e bound, the edge-only j skip) are tightest.
+    M = 7 and 8 (the M = 8 instantiation is the C4 path), both spaces, full and partial ranges."""
+    b = g.random_batch(seed=152, n_inst=24, M_lo=7, M_hi=8, N_lo=1, N_hi=2, k_max=12, tfree_frac=0.5)
+    rng = np.random.default_rng(2)
+    for i in range(b.n_inst):
+        o0, o1 = int(b.user_off[i]), int(b.user_off[i + 1])
+        lat = g.min_local_latency(b.models[b.model_id[i]], b.zeta[o0:o1], b.f_max[o0:o1])
+        b.T[o0:o1] = (1.0 + rng.uniform(0.0, 0.6, o1 - o0)) * lat
+        if b.t_free[i] > 0:
+            b.t_free[i] = rng.uniform(0.0, 0.5) * b.T[o0:o1].min()
+    for i in range(b.n_inst):
+        bi = b.subset(i, i + 1)
+        db = J.DeviceBatch(bi)
+        for space in (0, 1):
+            size = O.bf_space_size(bi, space)
+            lo = int(rng.integers(0, size))
+            for r0, r1 in ((0, size), (lo, size), (0, max(lo, 1))):
+                E, I, S = J.bruteforce(db, space, r0, r1)
+                Eo, Io, So = O.bf(bi, space, r0, r1)
+                assert int(S.item()) == So
+                assert_bits_equal(E.cpu().numpy(), np.array([Eo]), f"E {i} {space} {r0} {r1}")
+                assert int(I.item()) == Io
+
+
 def test_bf_zero_energy_ties(J):
     """kappa = p_u = c = 0: every feasible candidate has E = 0, so the answer is the lowest feasible
     index -- the vector bound (LB = 0 >= best = 0) must never drop a lower-index tie."""
