@@ -336,11 +336,13 @@ def run_mine(args):
         dx = torch.empty(int(h2d), dtype=torch.uint8, device="cuda")
         dx.copy_(hx, non_blocking=True)
         torch.cuda.synchronize()
-        s.record(stream)
-        dx.copy_(hx, non_blocking=True)
-        e.record(stream)
-        torch.cuda.synchronize()
-        roof_ms = s.elapsed_time(e)
+        roof_ms = float("inf")
+        for _ in range(3):  # best of three single copies
+            s.record(stream)
+            dx.copy_(hx, non_blocking=True)
+            e.record(stream)
+            torch.cuda.synchronize()
+            roof_ms = min(roof_ms, s.elapsed_time(e))
         e2e["h2d_copy_roof"] = {"ms": roof_ms, "gbs": h2d / (roof_ms / 1e3) / 1e9,
                                 "frac": roof_ms / (ms / reps)}
         del hx, dx
