@@ -153,6 +153,7 @@ struct GridKCache {
 
 struct InstRegs {  // lane-resident user parameters (lane = user)
     double z, k, f0, f1, R, p, T;
+    double t_free, fe_min, fe_max, rho;  // the instance's scalars (every lane)
 };
 
 // Warp-cooperative load and validation of instance i (lane = user), with the same
@@ -169,6 +170,13 @@ __device__ __forceinline__ int warp_validate_pre(const DevModel *models, const D
     k = 0;
     x.z = x.k = x.f0 = x.f1 = x.R = x.p = 0.0;
     x.T = dinf();
+#ifndef JDOB_LATE_SCALARS
+    // the instance scalars are loaded with the users' values, so that both latencies overlap
+    x.t_free = b.t_free[i];
+    x.fe_min = b.fe_min[i];
+    x.fe_max = b.fe_max[i];
+    x.rho = b.rho[i];
+#endif
 #ifndef JDOB_LATE_USERS
     if (lane < M) {  // users of an instance rejected below are loaded but not used
         const long long u = off + lane;
@@ -207,7 +215,13 @@ __device__ __forceinline__ int warp_validate_pre(const DevModel *models, const D
              (x.p >= 0.0) && (x.T > 0.0);
     }
     if (__any_sync(0xffffffffu, !ok)) return JDOB_ST_BADPARAM;
-    const double t_free = b.t_free[i], fe_min = b.fe_min[i], fe_max = b.fe_max[i], rho = b.rho[i];
+#ifdef JDOB_LATE_SCALARS
+    x.t_free = b.t_free[i];
+    x.fe_min = b.fe_min[i];
+    x.fe_max = b.fe_max[i];
+    x.rho = b.rho[i];
+#endif
+    const double t_free = x.t_free, fe_min = x.fe_min, fe_max = x.fe_max, rho = x.rho;
     if (!(dfinite(t_free) && dfinite(fe_min) && dfinite(fe_max) && dfinite(rho) && (t_free >= 0.0) &&
           (fe_min > 0.0) && (fe_min <= fe_max) && (rho > 0.0)))
         return JDOB_ST_BADPARAM;

@@ -205,7 +205,7 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     InstRegs x;
     const int st = warp_validate_pre(models, b, i, lane, off, M64, mid, x, M, k, mdp, &s.kc);
     if (st == kStDefer) return;  // M > 32: solved by k_solve_large (solve_large.cu)
-    const double t_free = b.t_free[i], fe_max = b.fe_max[i], rho = b.rho[i];
+    const double t_free = x.t_free, fe_max = x.fe_max, rho = x.rho;
     if (st == JDOB_ST_BADPARAM || st == JDOB_ST_BADMODEL) {
         write_bad(r, i, off, M, mdp ? mdp->N : 0, t_free, st, lane);
         return;
