@@ -191,7 +191,10 @@ JDOB_API int jdob_solve_batch(const jdob_model *models, int32_t n_models, const 
  * arrays of `out`, and synchronises `stream` before returning.  Every pointer in
  * models/b/out is a HOST pointer (pinned memory gives asynchronous copies).
  * Device memory is stream-ordered (cudaMallocAsync) and freed before returning.
- * If `h2d_bytes`/`d2h_bytes` are non-NULL they receive the bytes copied.
+ * If `h2d_bytes`/`d2h_bytes` are non-NULL they receive the bytes copied.  The batch is processed in
+ * chunks on two streams (copy-in, solve, copy-out overlap); a chunk's copy-ins are submitted as one
+ * cudaMemcpyBatchAsync, or as one cudaMemcpyAsync per array when the environment variable
+ * JDOB_HOST_COPIES=single is set (e.g. under compute-sanitizer initcheck).
  */
 JDOB_API int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob_batch *b, int32_t mode,
                           const jdob_result *out, void *stream, int64_t *h2d_bytes, int64_t *d2h_bytes);

@@ -2,6 +2,7 @@
 // layout, model-aggregate setup (K0) and kernel launches.  No torch types, no
 // exceptions across the boundary, nothing allocated beyond a call.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -553,8 +554,14 @@ int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob
             at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
             at.flags = cudaMemcpyFlagPreferOverlapWithCompute;
             size_t ai = 0, fail = 0;
-            if (cudaMemcpyBatchAsync(bd, bs, bn, nb_, &at, &ai, 1, &fail, ss) != cudaSuccess) {
-                cudaGetLastError();
+            // JDOB_HOST_COPIES=single: one cudaMemcpyAsync per array (compute-sanitizer's initcheck does
+            // not record the writes of batched copies and would flag every later read)
+            static const bool single = [] {
+                const char *e = getenv("JDOB_HOST_COPIES");
+                return e && strcmp(e, "single") == 0;
+            }();
+            if (single || cudaMemcpyBatchAsync(bd, bs, bn, nb_, &at, &ai, 1, &fail, ss) != cudaSuccess) {
+                if (!single) cudaGetLastError();
                 for (size_t q = 0; q < nb_; q++) cudaMemcpyAsync(bd[q], bs[q], bn[q], cudaMemcpyHostToDevice, ss);
             }
         }
