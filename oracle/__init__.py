@@ -16,6 +16,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "jdob_oracle.c")
 LIB = os.path.join(HERE, "liboracle.so")
+# tools/mutate_oracle.py points this at a mutated build (mutation testing of the pins)
+LIB_OVERRIDE = os.environ.get("JDOB_ORACLE_LIB")
 CFLAGS = ["-O2", "-std=gnu11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-pthread", "-Wall"]
 
 ST_OK, ST_LOCAL_INFEASIBLE, ST_REQUIRE, ST_BADPARAM, ST_BADMODEL, ST_TOOBIG = range(6)
@@ -79,8 +81,11 @@ def lib():
     global _lib
     with _lock:
         if _lib is None:
-            build()
-            L = C.CDLL(LIB)
+            if LIB_OVERRIDE:
+                L = C.CDLL(LIB_OVERRIDE)
+            else:
+                build()
+                L = C.CDLL(LIB)
             P = C.POINTER
             L.oracle_check_model.argtypes = [P(OModel)]
             L.oracle_check_inst.argtypes = [P(OModel), P(OInst)]
