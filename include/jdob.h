@@ -135,11 +135,12 @@ typedef struct {
  *   stats [n_buckets * JDOB_STATS_FIELDS] : optional (NULL = skip) energy-saving
  *                          statistics (a12, R16), fields per bucket:
  *                          [0] #OK instances, [1] sum r, [2] sum r^2, [3] max r,
- *                          [4] min r, [5] sum E/M, [6] sum E_lc/M, [7] #offloading,
+ *                          [4] min r, [5] sum E/M, [6] sum E_lc/M, [7] #offloading
+ *                          plans (f_e* > 0: some user offloads, R18; valid for any M),
  *                          [8] #status != OK, [9+n] #instances with n~* = n (n <= 63);
  *                          r = 100 (E_lc - E) / E_lc.  Deterministic for a given
- *                          n_inst (fixed reduction tree).  Default buckets (bucket == NULL)
- *                          cover M_i <= n_buckets.
+ *                          n_inst (fixed reduction tree).  Default buckets (bucket == NULL):
+ *                          bucket M_i - 1; instances with M_i > n_buckets are not counted.
  */
 typedef struct {
     double *E, *E_lc, *t_free_next, *f_e;
@@ -190,7 +191,12 @@ JDOB_API int jdob_solve_batch(const jdob_model *models, int32_t n_models, const 
  * f_e, n_tilde, j, status, mask (and f_user/stats when non-NULL) back to the host
  * arrays of `out`, and synchronises `stream` before returning.  Every pointer in
  * models/b/out is a HOST pointer (pinned memory gives asynchronous copies).
- * Device memory is stream-ordered (cudaMallocAsync) and freed before returning.
+ * Device memory is stream-ordered, allocated from a memory pool private to the library
+ * (cudaMallocFromPoolAsync) and returned to that pool before returning; the pool keeps the
+ * largest call's footprint mapped for the next call (the device's default pool and the
+ * caller's allocators are not touched) until jdob_release_pool() trims it.
+ * Errors: as jdob_solve_batch, plus JDOB_EINVAL when the host user_off is not a
+ * non-decreasing sequence starting at >= 0 (checked per chunk before its copies).
  * If `h2d_bytes`/`d2h_bytes` are non-NULL they receive the bytes copied.  The batch is processed in
  * chunks on two streams (copy-in, solve, copy-out overlap); a chunk's copy-ins are submitted as one
  * cudaMemcpyBatchAsync, or as one cudaMemcpyAsync per array when the environment variable
@@ -198,6 +204,13 @@ JDOB_API int jdob_solve_batch(const jdob_model *models, int32_t n_models, const 
  */
 JDOB_API int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob_batch *b, int32_t mode,
                           const jdob_result *out, void *stream, int64_t *h2d_bytes, int64_t *d2h_bytes);
+
+/*
+ * Release the device memory the library's private pool keeps between jdob_solve_batch_host
+ * calls (cudaMemPoolTrimTo(pool, 0) on every device the library has used).  Host call; safe
+ * when no jdob_solve_batch_host call is in flight.  Returns JDOB_OK or JDOB_ECUDA.
+ */
+JDOB_API int jdob_release_pool(void);
 
 /*
  * Exhaustive search (rows a9-a10): argmin of the energy over candidate indices

@@ -60,7 +60,8 @@ class OResult(C.Structure):
 
 class OOgResult(C.Structure):
     _fields_ = [("E", C.c_double), ("t_free_next", C.c_double), ("status", C.c_int), ("n_groups", C.c_int),
-                ("group_of", C.c_int * 32), ("part", C.c_int * 32), ("f_user", C.c_double * 32),
+                ("group_of", C.c_int * MAXM_LARGE), ("part", C.c_int * MAXM_LARGE),
+                ("f_user", C.c_double * MAXM_LARGE),
                 ("group_fe", C.c_double * 32), ("group_start", C.c_int * 33)]
 
 
@@ -109,7 +110,7 @@ def lib():
                                             P(C.c_double), P(C.c_double), P(C.c_double), P(C.c_uint),
                                             P(C.c_int)]
             L.oracle_stats.argtypes = [C.c_longlong, P(C.c_longlong), P(C.c_int), C.c_int, P(C.c_double),
-                                       P(C.c_double), P(C.c_int), P(C.c_uint), P(C.c_int), P(C.c_double)]
+                                       P(C.c_double), P(C.c_int), P(C.c_double), P(C.c_int), P(C.c_double)]
             L.oracle_grid_k.argtypes = [P(OInst)]
             L.oracle_og.argtypes = [P(OModel), P(OInst), C.c_int, P(OOgResult)]
             _lib = L
@@ -308,10 +309,10 @@ def stats(batch, res, n_buckets=None) -> np.ndarray:
     E = np.ascontiguousarray(res["E"], np.float64)
     El = np.ascontiguousarray(res["E_lc"], np.float64)
     nt = np.ascontiguousarray(res["n_tilde"], np.int32)
-    mk = np.ascontiguousarray(res["mask"], np.uint32)
+    fe = np.ascontiguousarray(res["f_e"], np.float64)
     ss = np.ascontiguousarray(res["status"], np.int32)
     lib().oracle_stats(n, off.ctypes.data_as(C.POINTER(C.c_longlong)), None if bk is None else _ip(bk), n_buckets,
-                       _dp(E), _dp(El), _ip(nt), mk.ctypes.data_as(C.POINTER(C.c_uint)), _ip(ss), _dp(st))
+                       _dp(E), _dp(El), _ip(nt), _dp(fe), _ip(ss), _dp(st))
     return st
 
 

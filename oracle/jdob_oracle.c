@@ -849,13 +849,15 @@ int oracle_eval_batch(const o_batch *b, long long n_inst, const int *partition, 
 /* ------------------------------------------------------------------ */
 /* Energy-saving statistics (a12, R16): per bucket                     */
 /* [0] count OK, [1] sum r, [2] sum r^2, [3] max r, [4] min r,          */
-/* [5] sum E_star over M, [6] sum E_LC over M, [7] #offloading, [8] #status != OK,    */
+/* [5] sum E_star over M, [6] sum E_LC over M, [7] #offloading (plans    */
+/* with f_e* > 0: some user offloads, R18), [8] #status != OK,           */
 /* [9..72] histogram of n~* (0..63);  r = 100 (E_LC - E*) / E_LC.        */
-/* Summation in instance order.                                          */
+/* Default bucket (no bucket array): M - 1 for M <= n_buckets, else the  */
+/* instance is not counted.  Summation in instance order.                */
 /* ------------------------------------------------------------------ */
 #define O_STATS_FIELDS 80
 int oracle_stats(long long n_inst, const long long *user_off, const int *bucket, int n_buckets, const double *E,
-                 const double *E_lc, const int *n_tilde, const unsigned *mask, const int *status, double *stats) {
+                 const double *E_lc, const int *n_tilde, const double *f_e, const int *status, double *stats) {
     for (long long x = 0; x < (long long)n_buckets * O_STATS_FIELDS; x++) stats[x] = 0.0;
     for (int bk = 0; bk < n_buckets; bk++) {
         stats[bk * O_STATS_FIELDS + 3] = -O_INF;
@@ -863,7 +865,7 @@ int oracle_stats(long long n_inst, const long long *user_off, const int *bucket,
     }
     for (long long i = 0; i < n_inst; i++) {
         int M = (int)(user_off[i + 1] - user_off[i]);
-        int bk = bucket ? bucket[i] : (M >= 1 && M <= O_MAXM ? M - 1 : 0);
+        int bk = bucket ? bucket[i] : (M >= 1 && M <= n_buckets ? M - 1 : -1);
         if (bk < 0 || bk >= n_buckets) continue;
         double *s = stats + (long long)bk * O_STATS_FIELDS;
         if (status[i] != O_ST_OK) {
@@ -878,7 +880,7 @@ int oracle_stats(long long n_inst, const long long *user_off, const int *bucket,
         if (r < s[4]) s[4] = r;
         s[5] = s[5] + E[i] / (double)M;
         s[6] = s[6] + E_lc[i] / (double)M;
-        if (mask[i] != 0u) s[7] = s[7] + 1.0;
+        if (f_e[i] > 0.0) s[7] = s[7] + 1.0;
         if (n_tilde[i] >= 0 && n_tilde[i] <= 63) s[9 + n_tilde[i]] = s[9 + n_tilde[i]] + 1.0;
     }
     return 0;
@@ -902,9 +904,9 @@ int oracle_grid_k(const o_inst *in) { return (int)o_grid_k(in); }
 typedef struct {
     double E, t_free_next;
     int status, n_groups;
-    int group_of[O_MAXM];     /* per user (input index): group number in execution order */
-    int part[O_MAXM];         /* per user: partition point, N = local */
-    double f_user[O_MAXM];
+    int group_of[O_MAXM_LARGE]; /* per user (input index): group number in execution order */
+    int part[O_MAXM_LARGE];     /* per user: partition point, N = local */
+    double f_user[O_MAXM_LARGE];
     double group_fe[O_MAXM];  /* per group: f_e, 0 = all local */
     int group_start[O_MAXM + 1];
 } o_og_result;
@@ -949,7 +951,7 @@ int oracle_og(const o_model *m, const o_inst *in, int mode, o_og_result *r) {
         r->E = lr.E;
         r->t_free_next = in->t_free;
         r->n_groups = 0;
-        for (int u = 0; u < M && u < O_MAXM; u++) {
+        for (int u = 0; u < M && u < O_MAXM_LARGE; u++) {
             r->part[u] = m->N;
             r->f_user[u] = lr.f_user[u];
         }

@@ -84,13 +84,14 @@ def lib():
                                              C.c_size_t, C.c_void_p]
             L.jdob_last_error.restype = C.c_char_p
             L.jdob_version.restype = C.c_char_p
+            L.jdob_release_pool.restype = C.c_int
             _lib = L
     return _lib
 
 
 EXPORTED = ("jdob_workspace_bytes", "jdob_solve_batch", "jdob_solve_batch_host", "jdob_bruteforce",
             "jdob_bf_space_size", "jdob_eval", "jdob_grouped_workspace_bytes", "jdob_solve_grouped",
-            "jdob_last_error", "jdob_version")
+            "jdob_last_error", "jdob_version", "jdob_release_pool")
 
 
 def _check(rc):
@@ -236,16 +237,16 @@ def eval_plans(db: DeviceBatch, partition=None, f_e=None, slack: float = 1e-9, f
 
 
 def plan_partition(db: DeviceBatch, res: dict):
-    """Per-user partition points of J-DOB plans: n~* for offloaders, N for locals (device)."""
-    torch = _torch()
-    dev = db.device
-    off = db.t["user_off"]
-    M = (off[1:] - off[:-1])
-    inst = torch.repeat_interleave(torch.arange(db.n_inst, device=dev), M)
-    local = torch.arange(db.n_users, device=dev) - off[:-1][inst]
-    Ns = torch.tensor(db.Ns, dtype=torch.int32, device=dev)[db.t["model_id"].long()]
-    bit = (res["mask"][inst].long() >> local) & 1
-    return torch.where(bit == 1, res["n_tilde"][inst], Ns[inst]).to(torch.int32)
+    """Per-user partition points of J-DOB plans (n~* for offloaders, N for locals): the kernel's own
+    `partition` output, requested with solve_batch(..., partition=True)."""
+    if res.get("partition") is None:
+        raise ValueError("solve_batch(..., partition=True) writes the per-user partition")
+    return res["partition"]
+
+
+def release_pool() -> None:
+    """jdob_release_pool: trim the device memory the host API's private pool keeps between calls."""
+    _check(lib().jdob_release_pool())
 
 
 def bf_space_size(space: int, N: int, M: int, k: int) -> int:

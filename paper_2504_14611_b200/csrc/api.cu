@@ -146,18 +146,38 @@ static DevBatch to_dev(const jdob_batch *b) {
 
 // Keep the device's default memory pool from returning memory to the OS at every
 // synchronisation, so jdob_solve_batch_host's stream-ordered buffers are reused.
-static void keep_pool_warm() {
+// Library-private stream-ordered memory pool per device for the host API: its release threshold is
+// the maximum, so a call's footprint stays mapped for the next call (no per-call map/unmap); the
+// device's default pool (and so other cudaMallocAsync users in the process) is left untouched.
+// jdob_release_pool() trims it.
+static cudaMemPool_t g_pool[64];
+static bool g_pool_made[64];
+
+static cudaMemPool_t host_pool() {
     int dev = 0;
     cudaGetDevice(&dev);
-    static bool done[64] = {false};
-    if (dev >= 0 && dev < 64 && !done[dev]) {
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            unsigned long long thr = ~0ull;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    if (dev < 0 || dev >= 64) return nullptr;
+    if (!g_pool_made[dev]) {
+        cudaMemPoolProps pp = {};
+        pp.allocType = cudaMemAllocationTypePinned;
+        pp.location.type = cudaMemLocationTypeDevice;
+        pp.location.id = dev;
+        if (cudaMemPoolCreate(&g_pool[dev], &pp) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
         }
-        done[dev] = true;
+        unsigned long long thr = ~0ull;
+        cudaMemPoolSetAttribute(g_pool[dev], cudaMemPoolAttrReleaseThreshold, &thr);
+        g_pool_made[dev] = true;
     }
+    return g_pool[dev];
+}
+
+int jdob_release_pool(void) {
+    g_err.clear();
+    for (int d = 0; d < 64; d++)
+        if (g_pool_made[d] && cudaMemPoolTrimTo(g_pool[d], 0) != cudaSuccess) return cuda_check("release_pool");
+    return JDOB_OK;
 }
 
 static int num_sms() {
@@ -330,7 +350,9 @@ int jdob_solve_grouped(const jdob_model *models, int32_t n_models, const jdob_ba
     o.partition = out->partition;
     o.f_user = out->f_user;
     o.group_fe = out->group_fe;
-    if (launch_grouped(dm, to_dev(b), mode, w, o, s, num_sms())) return cuda_check("grouped");
+    bool wide = false;  // some model admits M > 32: such instances are reported with their LC answer
+    for (int i = 0; i < n_models; i++) wide |= models[i].B_max > JDOB_MAX_M;
+    if (launch_grouped(dm, to_dev(b), mode, w, o, s, num_sms(), wide)) return cuda_check("grouped");
     return cuda_check("grouped");
 }
 
@@ -405,8 +427,9 @@ int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob
         return fail(JDOB_EINVAL, "n_buckets = %d outside [1, %d]", out->n_buckets, JDOB_MAX_BUCKETS);
     if (mode < JDOB_MODE_FULL || mode > JDOB_MODE_BINARY) return fail(JDOB_EINVAL, "bad mode %d", mode);
     cudaStream_t s = (cudaStream_t)stream;
-    keep_pool_warm();
+    cudaMemPool_t pool = host_pool();
     const long long n = b->n_inst;
+    if (n > 0 && b->user_off[0] < 0) return fail(JDOB_EINVAL, "user_off[0] = %lld < 0", (long long)b->user_off[0]);
     const long long nu = n > 0 ? (long long)b->user_off[n] : 0;
 #ifndef JDOB_HOST_NS
 #define JDOB_HOST_NS 2
@@ -427,7 +450,9 @@ int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob
     const size_t wsb = jdob_workspace_bytes(models, n_models, 0);
     bytes += in_inst + in_user + outb + NS * al(wsb);
     char *base = nullptr;
-    if (cudaMallocAsync((void **)&base, bytes, s) != cudaSuccess) return cuda_check("cudaMallocAsync");
+    if ((pool ? cudaMallocFromPoolAsync((void **)&base, bytes, pool, s) : cudaMallocAsync((void **)&base, bytes, s)) !=
+        cudaSuccess)
+        return cuda_check("cudaMallocAsync");
     char *p = base;
     long long h2d = 0, d2h = 0;
     auto take = [&](size_t nb) -> char * {
@@ -520,6 +545,15 @@ int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob
         cudaStream_t ss = st[c % NS];
         const long long i0 = bounds[c], i1 = bounds[c + 1];
         if (i1 <= i0) continue;
+        // the host offsets size this chunk's copies: a decreasing pair would wrap a byte count, so
+        // the chunk is checked before anything of it is submitted (the chunks before it are valid)
+        bool mono = true;
+        for (long long q = i0; q < i1; q++) mono &= b->user_off[q] <= b->user_off[q + 1];
+        mono &= b->user_off[i1] <= nu;  // within the arrays sized by user_off[n_inst]
+        if (!mono) {
+            rc = fail(JDOB_EINVAL, "user_off decreases inside instances [%lld, %lld]", i0, i1);
+            break;
+        }
         const long long u0 = b->user_off[i0], u1 = b->user_off[i1];
 #ifndef JDOB_HOST_NO_BATCH
         // the chunk's copy-ins as one batch submission (cudaMemcpyBatchAsync, stream-ordered sources)

@@ -162,8 +162,13 @@ __global__ void k_og_final_write(const DevModel *models, DevBatch b, OgWork w, G
     const long long s0 = inst * kMaxM;
     const int mid = b.model_id[inst];
     const int N = (mid >= 0 && mid < b.n_models) ? models[mid].N : 0;
+    // M > 32 (K1 deferred it; grouping takes M <= 32): the final pass solved the whole instance in LC
+    // mode on the block path; report BADPARAM with that LC answer unless the instance is malformed
+    // or locally infeasible (the oracle's precedence)
+    int st_out = (st == JDOB_ST_OK) ? JDOB_ST_OK : w.r_st[s0];
+    if (st != JDOB_ST_OK && M > kMaxM && st_out != JDOB_ST_LOCAL_INFEASIBLE) st_out = JDOB_ST_BADPARAM;
     if (lane == 0) {
-        o.status[inst] = (st == JDOB_ST_OK) ? JDOB_ST_OK : w.r_st[s0];
+        o.status[inst] = st_out;
         o.n_groups[inst] = ng;
         o.E[inst] = (st == JDOB_ST_OK) ? w.cE[inst * kCells + M] : w.r_E[s0];
         o.t_free_next[inst] = (st == JDOB_ST_OK) ? w.cT[inst * kCells + M] : b.t_free[inst];
@@ -228,7 +233,7 @@ static DevResult stage_result(const OgWork &w, double *f_user) {
 }
 
 int launch_grouped(const DevModel *models, const DevBatch &b, int mode, const OgWork &w, const GroupedOut &o,
-                   cudaStream_t s, int num_sms) {
+                   cudaStream_t s, int num_sms, bool wide) {
     const long long n = b.n_inst;
     if (n <= 0) return 0;
     cudaMemsetAsync(w.mmax, 0, sizeof(int), s);
@@ -245,6 +250,9 @@ int launch_grouped(const DevModel *models, const DevBatch &b, int mode, const Og
     }
     k_og_final_build<<<(unsigned)((n + bs - 1) / bs), bs, 0, s>>>(b, w);
     launch_solve(models, stage_batch(b, w, n * kMaxM), stage_result(w, w.fs), mode, s, num_sms);
+    // instances with 32 < M <= B_max (K1 defers them; grouping is defined for M <= 32): the whole
+    // instance, in slot inst * 32, gets its LC answer from the block-per-instance kernel
+    if (wide) launch_solve_large(models, stage_batch(b, w, n * kMaxM), stage_result(w, w.fs), JDOB_MODE_LC, s, num_sms);
     k_og_final_write<<<(unsigned)((n * 32 + bs - 1) / bs), bs, 0, s>>>(models, b, w, o);
     return 0;
 }

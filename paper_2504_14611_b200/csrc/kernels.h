@@ -47,7 +47,7 @@ struct GroupedOut {
 
 void launch_aggregates(const ModelChunk &chunk, cudaStream_t s);
 int launch_grouped(const DevModel *models, const DevBatch &b, int mode, const OgWork &w, const GroupedOut &o,
-                   cudaStream_t s, int num_sms);
+                   cudaStream_t s, int num_sms, bool wide);  // wide: some model has B_max > 32
 void launch_solve(const DevModel *models, const DevBatch &b, const DevResult &r, int mode, cudaStream_t s,
                   int num_sms);
 void launch_solve_large(const DevModel *models, const DevBatch &b, const DevResult &r, int mode, cudaStream_t s,

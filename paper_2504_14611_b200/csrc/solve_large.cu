@@ -126,7 +126,7 @@ __device__ void large_instance(long long i, const DevModel *models, const DevBat
                                LargeView &s, double *dscr, int *iscr, long long *cscr) {
     const int tid = threadIdx.x;
     const long long off = b.user_off[i];
-    const int M = (int)(b.user_off[i + 1] - off);
+    const int M = (int)((b.user_end ? b.user_end[i] : b.user_off[i + 1]) - off);  // user_end: OG's views
     const DevModel &md = models[b.model_id[i]];
     const int N = md.N;
     const double t_free = b.t_free[i], fe_min = b.fe_min[i], fe_max = b.fe_max[i], rho = b.rho[i];
@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(kLT) k_solve_large(const DevModel *models, Dev
         __syncthreads();
         const long long i = base + threadIdx.x;
         if (i < i1) {
-            const long long M64 = b.user_off[i + 1] - b.user_off[i];
+            const long long M64 = (b.user_end ? b.user_end[i] : b.user_off[i + 1]) - b.user_off[i];
             const int mid = b.model_id[i];
             // the instances K1 deferred: valid model, 32 < M <= min(1024, B_max)
             if (M64 > kMaxM && M64 <= kMaxMLarge && mid >= 0 && mid < b.n_models && *models[mid].valid &&

@@ -52,8 +52,7 @@ __global__ void __launch_bounds__(32) k_stats_partial(DevBatch b, DevResult r, d
     constexpr int U = 4;
     for (long long i = i0 + lane; i < i1; i += 32 * U) {
         int Mq[U], bq[U], sq[U], nq[U];
-        unsigned mq[U];
-        double Eq[U], Lq[U];
+        double Eq[U], Lq[U], Fq[U];
 #pragma unroll
         for (int q = 0; q < U; q++) {
             const long long ii = i + 32 * q;
@@ -61,11 +60,12 @@ __global__ void __launch_bounds__(32) k_stats_partial(DevBatch b, DevResult r, d
             bq[q] = -1;
             if (ii < i1) {
                 Mq[q] = (int)(b.user_off[ii + 1] - b.user_off[ii]);
-                bq[q] = b.bucket ? b.bucket[ii] : ((Mq[q] >= 1 && Mq[q] <= kMaxM) ? Mq[q] - 1 : 0);
+                // default bucket M - 1; instances with M > n_buckets are not counted
+                bq[q] = b.bucket ? b.bucket[ii] : ((Mq[q] >= 1 && Mq[q] <= n_buckets) ? Mq[q] - 1 : -1);
                 sq[q] = r.status[ii];
                 Eq[q] = r.E[ii];
                 Lq[q] = r.E_lc[ii];
-                mq[q] = r.mask[ii];
+                Fq[q] = r.f_e[ii];
                 nq[q] = r.n_tilde[ii];
             }
         }
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(32) k_stats_partial(DevBatch b, DevResult r, d
             a[4 * 32] = a[4 * 32] + E / (double)M;
             a[5 * 32] = a[5 * 32] + El / (double)M;
             atomicAdd(c + 0, 1);
-            if (mq[q] != 0u) atomicAdd(c + 7, 1);
+            if (Fq[q] > 0.0) atomicAdd(c + 7, 1);  // the plan offloads (f_e* = 0 only when all-local, R18)
             const int nt = nq[q];
             if (nt >= 0 && nt < 64) atomicAdd(c + 9 + nt, 1);
         }

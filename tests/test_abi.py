@@ -25,7 +25,7 @@ def declared_symbols():
 
 def test_header_symbols_exported(L):
     syms = declared_symbols()
-    assert len(syms) == 10, syms
+    assert len(syms) == 11, syms
     for s in syms:
         assert hasattr(L, s), s
     import paper_2504_14611_b200 as J

@@ -232,9 +232,10 @@ def test_eval_parity_and_plan_feasibility(J):
     import torch
     b = g.random_batch(seed=130, n_inst=2000, M_hi=24, N_hi=10, k_max=64)
     db = J.DeviceBatch(b)
-    res = J.solve_batch(db)
+    res = J.solve_batch(db, partition=True)
     part = J.plan_partition(db, res)
     fe = res["f_e"]
+    assert_bits_equal(part.cpu().numpy(), O.partition_from_plan(b, to_np(res)), "partition vs mask-derived")
     ev = to_np(J.eval_plans(db, part, fe, slack=1e-9))
     ev2 = to_np(J.eval_plans(db, plans=res, slack=1e-9))
     for f in ev:
@@ -273,6 +274,27 @@ def test_host_api_matches_device(J):
     host["mask"] = host["mask"].view(np.uint32)
     for f in ("E", "E_lc", "t_free_next", "f_e", "n_tilde", "j", "status", "mask", "f_user"):
         assert_bits_equal(host[f], gpu[f], f)
+
+
+def test_host_api_rejects_bad_offsets_and_releases_pool(J):
+    """ADVICE r01: a decreasing host user_off is rejected (EINVAL) before any copy of the bad chunk;
+    the private pool can be trimmed and the next call works."""
+    b = g.random_batch(seed=142, n_inst=300, M_hi=8, N_hi=5, k_max=20)
+    hb = J.HostBuffers(b)
+    uo = hb.t["user_off"]
+    keep = uo.clone()
+    uo[150] = uo[151] + 5                                  # user_off[150] > user_off[151]
+    with pytest.raises(J.JdobError, match="user_off"):
+        J.solve_batch_host(hb)
+    uo.copy_(keep)
+    uo[0] = -1
+    with pytest.raises(J.JdobError, match="user_off"):
+        J.solve_batch_host(hb)
+    uo.copy_(keep)
+    J.release_pool()
+    J.solve_batch_host(hb)
+    orc = O.solve_batch(b)
+    assert_bits_equal(hb.out["E"].numpy(), orc["E"], "E after release")
 
 
 def test_host_api_large_m_and_partition(J):
@@ -539,3 +561,13 @@ def test_large_m_complexity_smoke(J):
     for f in ("E", "n_tilde", "j", "t_free_next"):
         assert_bits_equal(gpu[f], orc[f], f)
     assert_bits_equal(gpu["partition"], orc["part"], "partition")
+
+
+def test_og_more_than_32_users(J):
+    """OG on a batch mixing M <= 32 with 32 < M <= B_max (reported BADPARAM with the LC answer, as the
+    oracle does), plus a malformed and a locally infeasible large instance."""
+    small = g.random_batch(seed=173, n_inst=50, M_lo=1, M_hi=12, N_lo=1, N_hi=6, k_max=30, tfree_frac=0.4)
+    big = _large_batch([33, 48, 64, 40, 41], seed=21)
+    big.R[int(big.user_off[3]) + 2] = np.nan          # malformed user -> BADPARAM, NaN answer
+    big.T[int(big.user_off[4]) + 7] = 1e-6            # locally infeasible -> LOCAL_INFEASIBLE, LC answer
+    _og_parity(J, g.concat([small, big]))

@@ -173,7 +173,7 @@ def test_stats_of_golden_plans():
         s[4] = min(s[4], red)
         s[5] += E / M
         s[6] += El / M
-        s[7] += GOLD[c]["jdob"]["mask"] != 0
+        s[7] += GOLD[c]["jdob"]["f_e"] > 0.0          # the plan offloads (R18: f_e = 0 iff all-local)
         s[9 + GOLD[c]["jdob"]["n_tilde"]] += 1
     fin = np.isfinite(exp)
     assert np.array_equal(np.isnan(exp), np.isnan(st))

@@ -124,3 +124,19 @@ def test_og_plans_feasible(rand):
                 assert all(p == rand.models[rand.model_id[i]].N for p in part)
             tf = ev["t_free_next"]
         assert tf == r["t_free_next"]
+
+
+def test_og_more_than_32_users_reports_lc():
+    """Grouping is defined for M <= 32 (the per-cell group masks); a valid larger instance is reported
+    BADPARAM with its LC answer (f* = the LC frequencies), a locally infeasible one keeps that status."""
+    from tests.test_oracle_large import large_instance
+    for M in (33, 64):
+        b = large_instance(M, seed=M)
+        r = O.og(b)
+        E_lc, f_loc, _ = O.lc(b)
+        assert r["status"] == O.ST_BADPARAM and r["E"] == E_lc and r["n_groups"] == 0
+        assert np.array_equal(r["f_user"], f_loc) and (r["part"] == b.models[0].N).all()
+        assert r["t_free_next"] == b.t_free[0]
+    b = large_instance(40, seed=1)
+    b.T[5] = 1e-6
+    assert O.og(b)["status"] == O.ST_LOCAL_INFEASIBLE

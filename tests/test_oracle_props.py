@@ -205,7 +205,7 @@ def test_stats_definition(rand_mid):
         if sel.sum():
             assert abs(st[bk, 1] - red.sum()) <= 1e-9 * max(1, abs(red.sum()))
             assert st[bk, 3] == red.max() and st[bk, 4] == red.min()
-            assert st[bk, 7] == (r["mask"][sel] != 0).sum()
+            assert st[bk, 7] == (r["mask"][sel] != 0).sum() == (r["f_e"][sel] > 0).sum()
             assert st[bk, 9:73].sum() == sel.sum()
 
 
