@@ -198,9 +198,8 @@ JDOB_API int jdob_solve_batch(const jdob_model *models, int32_t n_models, const 
  * Errors: as jdob_solve_batch, plus JDOB_EINVAL when the host user_off is not a
  * non-decreasing sequence starting at >= 0 (checked per chunk before its copies).
  * If `h2d_bytes`/`d2h_bytes` are non-NULL they receive the bytes copied.  The batch is processed in
- * chunks on two streams (copy-in, solve, copy-out overlap); a chunk's copy-ins are submitted as one
- * cudaMemcpyBatchAsync, or as one cudaMemcpyAsync per array when the environment variable
- * JDOB_HOST_COPIES=single is set (e.g. under compute-sanitizer initcheck).
+ * chunks on two streams (copy-in, solve, copy-out overlap); a chunk's copy-ins are one
+ * cudaMemcpyAsync per array.
  */
 JDOB_API int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob_batch *b, int32_t mode,
                           const jdob_result *out, void *stream, int64_t *h2d_bytes, int64_t *d2h_bytes);

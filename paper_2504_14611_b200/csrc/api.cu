@@ -555,51 +555,17 @@ int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob
             break;
         }
         const long long u0 = b->user_off[i0], u1 = b->user_off[i1];
-#ifndef JDOB_HOST_NO_BATCH
-        // the chunk's copy-ins as one batch submission (cudaMemcpyBatchAsync, stream-ordered sources)
-        void *bd[16];
-        void *bs[16];
-        size_t bn[16];
-        size_t nb_ = 0;
-        auto h2 = [&](const void *dst, const void *src, size_t nb) {
-            if (nb) {
-                bd[nb_] = (void *)dst;
-                bs[nb_] = (void *)src;
-                bn[nb_] = nb;
-                nb_++;
-            }
-            h2d += (long long)nb;
-        };
-#else
+        // the chunk's copy-ins: one cudaMemcpyAsync per array on the chunk's stream
         auto h2 = [&](const void *dst, const void *src, size_t nb) {
             if (nb) cudaMemcpyAsync((void *)dst, src, nb, cudaMemcpyHostToDevice, ss);
             h2d += (long long)nb;
         };
-#endif
         h2(db.model_id + i0, b->model_id + i0, (i1 - i0) * 4);
         // user_off[i0..i1] (the shared boundary element is written with identical bytes by both chunks)
         h2(db.user_off + i0, b->user_off + i0, (i1 - i0 + 1) * 8);
         for (int t = 0; t < 7; t++) h2(*uf[t] + u0, uh[t] + u0, (u1 - u0) * 8);
         for (int t = 0; t < 4; t++) h2(*inf[t] + i0, ih[t] + i0, (i1 - i0) * 8);
         if (b->bucket) h2(db.bucket + i0, b->bucket + i0, (i1 - i0) * 4);
-#ifndef JDOB_HOST_NO_BATCH
-        {
-            cudaMemcpyAttributes at = {};
-            at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-            at.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-            size_t ai = 0, fail = 0;
-            // JDOB_HOST_COPIES=single: one cudaMemcpyAsync per array (compute-sanitizer's initcheck does
-            // not record the writes of batched copies and would flag every later read)
-            static const bool single = [] {
-                const char *e = getenv("JDOB_HOST_COPIES");
-                return e && strcmp(e, "single") == 0;
-            }();
-            if (single || cudaMemcpyBatchAsync(bd, bs, bn, nb_, &at, &ai, 1, &fail, ss) != cudaSuccess) {
-                if (!single) cudaGetLastError();
-                for (size_t q = 0; q < nb_; q++) cudaMemcpyAsync(bd[q], bs[q], bn[q], cudaMemcpyHostToDevice, ss);
-            }
-        }
-#endif
         jdob_batch cb = db;
         cb.n_inst = i1 - i0;
         cb.model_id = db.model_id + i0;

@@ -21,5 +21,4 @@ python tools/launch_summary.py $O/launches.csv > profiles/r01_launch_list_summar
  for a in "prof_solve solve k_solveILb0ELb1ELb1E" "prof_solve_c5 solve k_solveILb0ELb1ELb1E" "prof_bf bf k_bf_mainILi8ELb1E"; do
    set -- $a; echo "== $1"; python tools/slowpath_calls.py $O/$1.ncu-rep /tmp/$2_prof_$T.o $3; done) > profiles/r01_slowpath_calls.txt 2>&1
 (echo "# compute-sanitizer over tools/sanitize_run.py (every kernel: K0, K1 uniform + general incl. pruned/literal/work variants, K1L, K2 with the vector bounds, K3, K4, K5, host pipeline), capture $1"
- echo "# initcheck runs the host path with JDOB_HOST_COPIES=single: it does not record writes made by cudaMemcpyBatchAsync"
  for t in memcheck racecheck synccheck initcheck; do echo "== $t"; cat $O/sanitize_$t.txt; done) > profiles/r01_compute_sanitizer.txt
