@@ -37,6 +37,13 @@ import jdobgen as G  # noqa: E402
 
 PEAK_FP64_SM_PER_CLK = 64      # FP64 lanes per SM per clock (B200), DESIGN.md §7 (microbenchmarked)
 N_SMS = 148
+# FP64-pipe instructions of one correctly rounded double division on sm_100a: the fast path is
+# MUFU.RCP64H (XU pipe) + 7 DFMA + 1 DMUL (cuobjdump -sass, profiles/r02_ddiv_sass.txt); measured
+# throughput 4.6 divisions/SM/clk vs 63.2 DADD (tools/fp64_microbench.cu), i.e. ~13.7 DADD slots
+W_DIV = 8
+PEAK_NOTE = ("builder-measured FP64 peak: 148 SMs x 64 FP64 lanes/clk (tools/fp64_microbench.cu: DADD 63.2, "
+             "DFMA 58.2 per SM per clk) x the max SM clock seen during the run; MEASURED_PEAKS.json has no FP64 "
+             "entry")
 
 WORKLOADS = {
     "c2": ("c2_vgg16_m10_identical_beta0-35", 1 << 20),
@@ -117,20 +124,52 @@ class Clocks:
 
 
 def fp64_work(batch, counts, setups=None, lower_bound=False):
-    """FP64 operations of K1 per launch, each +, -, x, / or comparison = 1 op, from
-    per-instance counters (n_visit, n_eval, n_member): member evaluation 9, non-member term 1,
-    evaluated pair 6, visited pair 4, per n~ set-up 6M + M(M-1)/2 + 3M, LC 8M.  Literal Alg. 1/2:
-    every n~ is set up (setups = N).  Executed (pruned sweep): setups and pairs from the executed-work
-    counters, plus the n~ lower bounds (8 ops per (n~, user) and one RD reciprocal per user)."""
+    """FP64 operations of K1 per launch from per-instance counters (n_visit, n_eval,
+    n_member), split into divisions and other ops (+, -, x, comparison):
+      member evaluation   1 div (Gamma) + 8    non-member term  1
+      evaluated pair      1 div (1/f_e) + 5    visited pair     1 div (guard) + 3
+      per n~ set-up       3M div (O/R, gamma, threshold) + 3M + M(M-1)/2 (sort compares)
+      LC                  1 div + 7 per user
+    Literal Alg. 1/2: every n~ is set up (setups = N) -- SURVEY §8(d)'s count.  Executed (pruned
+    sweep): set-ups and pairs from the executed-work counters plus the n~ lower bounds (8 ops per
+    (n~, user), one RD reciprocal per user).  Returns (divisions, other ops, member evaluations)."""
     M = np.diff(batch.user_off).astype(np.float64)
     N = np.array([batch.models[m].N for m in batch.model_id], np.float64)
     visit, ev, mem = (counts[:, 0].astype(np.float64), counts[:, 1].astype(np.float64),
                       counts[:, 2].astype(np.float64))
     S = N if setups is None else setups.astype(np.float64)
-    ops = 9 * mem + (ev * M - mem) + 6 * ev + 4 * visit + S * (6 * M + M * (M - 1) / 2 + 3 * M) + 8 * M
+    div = mem + ev + visit + S * 3 * M + M
+    oth = 8 * mem + (ev * M - mem) + 5 * ev + 3 * visit + S * (3 * M + M * (M - 1) / 2) + 7 * M
     if lower_bound:
-        ops = ops + (8 * N * M + M) * (S > 0)
-    return float(np.sum(ops)), float(np.sum(mem))
+        div = div + M * (S > 0)
+        oth = oth + 8 * N * M * (S > 0)
+    return float(np.sum(div)), float(np.sum(oth)), float(np.sum(mem))
+
+
+def fp64_frac(div, oth, ms, peak_gops):
+    """FP64-pipe instruction rate of (div, other) ops with a division weighted W_DIV, over `ms`."""
+    ach = (W_DIV * div + oth) / (ms / 1e3) / 1e9
+    return {"ops_per_launch": W_DIV * div + oth, "divisions": div, "other_ops": oth, "achieved": ach,
+            "frac": ach / peak_gops}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def ncu_record(key):
+    """A committed ncu record (profiles/ncu_traffic.json) -- per-launch hardware counters of the
+    bench's own launch configuration; None when absent."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(key)
+    except Exception:
+        return None
 
 
 def hbm_context(nbytes, ms):
@@ -178,12 +217,40 @@ def cpu_baseline(batch, seconds, label, gpu_host=None):
                 bad += int((a.view(np.int32) != o.astype(a.dtype).view(np.int32)).sum())
         parity = (f"{n}/{n} instances of the cpu_baseline sample bit-exact vs oracle" if bad == 0
                   else f"MISMATCH: {bad} differing fields in the {n}-instance cpu_baseline sample")
-    return {"value": n / dt, "unit": "instances/s", "cores": cores, "kind": "oracle",
+    return {"value": n / dt, "unit": "instances/s", "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
             "sample": f"first {n} instances of {label} ({dt:.1f} s, C oracle -O2, {cores} threads)"}, parity
 
 
-def bf_leg(J, torch, world, rank, reps, dist):
-    """C4 exhaustive search, contiguous vector-aligned index ranges per rank."""
+def bf_literal_ops(N, M, k):
+    """SURVEY §8(d) per-candidate work of the general space, summed over every candidate: a vector with
+    o offloaders costs o divisions (one Gamma each; 1/f_e(j) is per grid point) + 9 o + 6 other ops per
+    grid point, and 2N + 2M set-up ops once per vector (digit decode, suffix sums, minima).  There are
+    C(M, o) N^o vectors with o offloaders."""
+    from math import comb
+    div = oth = 0.0
+    for o in range(M + 1):
+        nv = comb(M, o) * N ** o
+        div += nv * k * o
+        oth += nv * (k * (9 * o + 6) + 2 * N + 2 * M)
+    return div, oth
+
+
+def bf_executed_ops(wk, N, M):
+    """FP64 work the pruned K2 scan executed, from its counters (include/jdob.h jdob_bruteforce `work`):
+    user-term bound 3 per visited vector; n_min-only bound M + 10 + 1 div per vector past it; suffix
+    sums, D6' test, exact bound and hoists 2N + M + 12 + 1 div per vector past the n_min bound; the
+    edge-only skip's binary search ~30 per vector entering the grid loop; per evaluated candidate 9 + M
+    + 6 per offloader; one division + 2 per Gamma executed."""
+    w = [float(x) for x in wk]
+    div = w[1] + w[2] + w[5]
+    oth = (3 * w[0] + (M + 10) * w[1] + (2 * N + M + 12) * w[2] + 30 * w[3] + (9 + M) * w[4] + 6 * w[8]
+           + 2 * w[5])
+    return div, oth
+
+
+def bf_leg(J, torch, world, rank, reps, dist, peak_gops, with_cpu, cpu_seconds):
+    """C4 exhaustive search, contiguous vector-aligned index ranges per rank (strong scaling: the
+    2.75e10-candidate space is fixed)."""
     b = G.config_batch("c4")
     db = J.DeviceBatch(b)
     k = G.grid_size(float(b.fe_min[0]), float(b.fe_max[0]), float(b.rho[0]))
@@ -193,31 +260,94 @@ def bf_leg(J, torch, world, rank, reps, dist):
     lo, hi = bf_shard(size, k, world, rank)
     J.bruteforce(db, 0, lo, min(hi, lo + 64 * 1024 * k))     # warm-up (small)
     torch.cuda.synchronize()
-    times = []
+    stream = torch.cuda.current_stream()
+    times, kms = [], []
     res = None
     for _ in range(reps):
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
+        s, m, e = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        s.record(stream)
         E, I, S = J.bruteforce(db, 0, lo, hi)
+        m.record(stream)
         if dist:
             E, I = allreduce_argmin(E, I, dist)
-        e.record()
+        e.record(stream)
         torch.cuda.synchronize()
-        ms = s.elapsed_time(e)
+        ms, km = s.elapsed_time(e), s.elapsed_time(m)
         if dist:
-            t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+            t = torch.tensor([ms, km], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
+            ms, km = float(t[0]), float(t[1])
         times.append(ms)
+        kms.append(km)
         res = (float(E.item()), int(I.item()), int(S.item()))
-    ms = float(np.median(times))
-    return {"metric": "brute-force candidates/s", "value": size / (ms / 1e3), "unit": "candidates/s",
-            "workload": "c4_resnet18_m8_12pp_k64_general", "candidates": size, "ms": ms, "reps": reps,
-            "scaling": "strong", "E_min": res[0], "idx_min": res[1], "status": res[2],
-            "gpu_launches_per_rep": 5}
+    ms, km = float(np.median(times)), float(np.median(kms))
+    # untimed: the executed-work counters of the same scan (counting instantiation, same argmin)
+    Ew, Iw, Sw, W = J.bruteforce(db, 0, lo, hi, work=True)
+    wk = W.cpu().numpy().astype(np.int64)
+    if dist:
+        t = torch.tensor(wk, device="cuda", dtype=torch.int64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        wk = t.cpu().numpy()
+    ldiv, loth = bf_literal_ops(N, M, k)
+    ediv, eoth = bf_executed_ops(wk, N, M)
+    hw = ncu_record("k_bf_main_hw") if world == 1 else None
+    roof = {"bound": "alu", "kernel": "k_bf_main (K2)", "unit": "G FP64-pipe instr/s", "peak": peak_gops,
+            "launch_ms": km, "w_div": W_DIV,
+            "literal": fp64_frac(ldiv / world, loth / world, km, peak_gops),
+            "executed": fp64_frac(ediv / world, eoth / world, km, peak_gops),
+            "ncu_hw": hw, "traffic": ncu_record("k_bf_main_c4_full") if world == 1 else None,
+            "counters": {"vectors": int(wk[0]), "past_user_bound": int(wk[1]), "past_nmin_bound": int(wk[2]),
+                         "grid_loop_entered": int(wk[3]), "candidates_evaluated": int(wk[4]),
+                         "gamma_divisions": int(wk[5]), "skipped_by_edge_bound": int(wk[6]),
+                         "d6_fail_first_point": int(wk[7]), "offloader_terms": int(wk[8])},
+            "candidates_evaluated_frac": float(wk[4]) / size,
+            "peak_note": PEAK_NOTE + "; literal = SURVEY §8(d) per-candidate work over all candidates / "
+                         "the kernel's time (> 1 is the pruning's signature); executed = the work the "
+                         "pruned scan ran, from its counters (bench.py bf_executed_ops)"}
+    roof["achieved"] = roof["executed"]["achieved"]
+    roof["frac"] = roof["executed"]["frac"]
+    out = {"metric": "brute-force candidates/s", "value": size / (ms / 1e3), "unit": "candidates/s",
+           "workload": "c4_resnet18_m8_12pp_k64_general", "candidates": size, "ms": ms, "reps": reps,
+           "scaling": "strong", "E_min": res[0], "idx_min": res[1], "status": res[2],
+           "work_run_same_argmin": (float(Ew.item()), int(Iw.item())) == (res[0], res[1]) or world > 1,
+           "gpu_launches_per_rep": 3, "roofline": roof}
+    # the committed full-space oracle argmin (tools/c4_oracle_full.py: every candidate, literal oracle)
+    try:
+        full = json.load(open(os.path.join(ROOT, "profiles", "r02_c4_oracle_full.json")))
+        out["oracle_full_space"] = {"E_min": full["E_min"], "idx_min": full["idx_min"],
+                                    "equal": (full["E_min"], full["idx_min"]) == (res[0], res[1]),
+                                    "record": "profiles/r02_c4_oracle_full.json",
+                                    "oracle_candidates_per_s": full["candidates_per_s"],
+                                    "oracle_threads": full["threads"], "oracle_cpu": full["cpu_model"]}
+    except Exception:
+        out["oracle_full_space"] = None
+    if with_cpu and rank == 0 and world == 1:
+        import oracle as O
+        cores = os.cpu_count() or 1
+        probe = 64 * 12 * k * 16
+        t0 = time.perf_counter()
+        O.bf(b, 0, 0, probe, threads=cores)
+        rate = probe / max(time.perf_counter() - t0, 1e-6)
+        n = int(max(probe, min(size, rate * cpu_seconds)) // (12 * k)) * (12 * k)
+        # a vector-aligned sub-range around the optimum (both sides compared on the same range)
+        c = (res[1] // k) * k if res[1] >= 0 else 0
+        r0 = max(0, min(size - n, c - n // 2) // k * k)
+        t0 = time.perf_counter()
+        Eo, Io, So = O.bf(b, 0, r0, r0 + n, threads=cores)
+        dt = time.perf_counter() - t0
+        Eg, Ig, _ = J.bruteforce(db, 0, r0, r0 + n)
+        same = (float(Eg.item()), int(Ig.item())) == (Eo, Io)
+        out["cpu_baseline"] = {"value": n / dt, "unit": "candidates/s", "cores": cores, "kind": "oracle",
+                               "cpu_model": cpu_model(),
+                               "sample": f"candidates [{r0}, {r0 + n}) of the C4 general space ({n} = "
+                                         f"{n / size:.2%} of it, {dt:.1f} s, oracle_bf_mt -O2, {cores} "
+                                         f"threads); the rate is per candidate, not extrapolated"}
+        out["parity"] = (f"oracle argmin over the cpu_baseline sub-range ({Eo!r}, {Io}) "
+                         + ("== GPU's" if same else f"!= GPU's ({float(Eg.item())!r}, {int(Ig.item())})"))
+    return out
 
 
 def run_mine(args):
@@ -248,13 +378,14 @@ def run_mine(args):
     # and the work the pruned product sweep executes (same decisions as the timed launches)
     res_c = J.solve_batch(db, counts=True, f_user=False)
     counts = res_c["counts"].cpu().numpy()
-    literal_work, n_member = fp64_work(batch, counts)
+    lit_div, lit_oth, n_member = fp64_work(batch, counts)
     wk = J.solve_batch(db, work=True, f_user=False)["work"].cpu().numpy()
-    work, n_member_exec = fp64_work(batch, wk[:, 1:], setups=wk[:, 0], lower_bound=True)
+    ex_div, ex_oth, n_member_exec = fp64_work(batch, wk[:, 1:], setups=wk[:, 0], lower_bound=True)
     setup_frac = float(wk[:, 0].sum()) / float(sum(batch.models[m].N for m in batch.model_id))
     del res_c
 
-    res = J.solve_batch(db, stats=True, n_buckets=n_buckets, f_user=False)
+    res = J.solve_batch(db, f_user=False)
+    res["stats"] = J.stats(db, res, n_buckets=n_buckets)
     # the product path's decisions for the whole batch, on the host: the cpu_baseline leg compares
     # its oracle sample with them (the only place the bench run meets the oracle)
     gpu_host = {f: res[f].cpu().numpy() for f in ("E", "t_free_next", "f_e", "n_tilde", "j", "status", "mask")}
@@ -264,7 +395,8 @@ def run_mine(args):
     from paper_2504_14611_b200.dist import allreduce_stats
 
     def step():
-        J.solve_batch(db, stats=True, n_buckets=n_buckets, f_user=False, out=res)
+        J.solve_batch(db, f_user=False, out=res)
+        J.stats(db, res, out=res["stats"])
         J.eval_plans(db, plans=res, f_user=False, out=ev)
         if dist:
             res["stats_global"] = allreduce_stats(res["stats"], dist)
@@ -285,9 +417,10 @@ def run_mine(args):
     t_s.record(stream)
     for i in range(K):
         ev_s[i].record(stream)
-        J.solve_batch(db, stats=True, n_buckets=n_buckets, f_user=False, out=res)
+        J.solve_batch(db, f_user=False, out=res)           # K0 + K1 (K0: one tiny block per model)
         ev_e[i].record(stream)
-        J.eval_plans(db, plans=res, f_user=False, out=ev)
+        J.stats(db, res, out=res["stats"])                 # K4
+        J.eval_plans(db, plans=res, f_user=False, out=ev)  # K3
         if dist:
             res["stats_global"] = allreduce_stats(res["stats"], dist)
     t_e.record(stream)
@@ -303,9 +436,9 @@ def run_mine(args):
         t = torch.tensor([total_ms, solve_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms, solve_ms = float(t[0]), float(t[1])
-        w = torch.tensor([work, literal_work], device="cuda", dtype=torch.float64)
+        w = torch.tensor([ex_div, ex_oth, lit_div, lit_oth], device="cuda", dtype=torch.float64)
         dist.all_reduce(w, op=dist.ReduceOp.MAX)   # per-GPU work of the slowest rank's kind
-        work, literal_work = float(w[0]), float(w[1])
+        ex_div, ex_oth, lit_div, lit_oth = (float(x) for x in w)
     value = world * n * K / (total_ms / 1e3)
 
     # end-to-end through the public host-buffer API (copies inside the timed region)
@@ -360,18 +493,28 @@ def run_mine(args):
                                 "frac": roof_ms / (ms / reps)}
         del hx, dx
 
+    peak_clk = (clk or {}).get("sm_max_mhz") or 1965.0
+    peak = N_SMS * PEAK_FP64_SM_PER_CLK * peak_clk * 1e6 / 1e9   # G FP64-pipe lane instructions/s
     bf = None
     if not args.no_bf:
-        bf = bf_leg(J, torch, world, rank, args.bf_reps, dist)
+        bf = bf_leg(J, torch, world, rank, args.bf_reps, dist, peak, not args.no_cpu, args.cpu_seconds)
 
     cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu, parity = cpu_baseline(batch, args.cpu_seconds, label, gpu_host)
 
     if rank == 0:
-        peak_clk = (clk or {}).get("sm_max_mhz") or 1965.0
-        peak = N_SMS * PEAK_FP64_SM_PER_CLK * peak_clk * 1e6 / 1e9   # G FP64 ops/s
-        achieved = work / (solve_ms / 1e3) / 1e9
+        default_c2 = args.workload == "c2" and n == 1 << 20 and world == 1
+        executed = fp64_frac(ex_div, ex_oth, solve_ms, peak)
+        literal = fp64_frac(lit_div, lit_oth, solve_ms, peak)
+        hw = ncu_record("k_solve_hw") if default_c2 else None
+        # hardware count of the FP64-pipe lane instructions one launch executes (committed ncu capture
+        # of this exact launch), over the live K1 time: the measured executed fraction
+        ncu_exec = None
+        if hw and hw.get("fp64_thread_inst"):
+            a_ = hw["fp64_thread_inst"] / (solve_ms / 1e3) / 1e9
+            ncu_exec = {"fp64_lane_instructions_per_launch": hw["fp64_thread_inst"], "achieved": a_,
+                        "frac": a_ / peak}
         line = {
             "metric": "J-DOB instances solved/s",
             "value": value,
@@ -388,23 +531,28 @@ def run_mine(args):
             "config": {"workload": label, "n_inst_per_gpu": n, "global_instances": world * n,
                        "users_per_gpu": int(batch.n_users), "input_bytes_per_gpu": int(batch.nbytes()),
                        "l2": "inputs larger than L2 (126 MB)" if batch.nbytes() > 126e6 else "inputs fit in L2",
-                       "step": "jdob_solve_batch (K0+K1+K4 stats) + jdob_eval of every plan (K3) + NCCL stats allreduce",
+                       "step": "jdob_solve_batch (K0+K1) + jdob_stats (K4) + jdob_eval of every plan (K3)"
+                               + (" + NCCL stats allreduce" if dist else ""),
                        "parallelism": f"dp{world}"},
-            "roofline": {"bound": "alu", "kernel": "k_solve (K1)", "achieved": achieved, "peak": peak,
-                         "unit": "G FP64 op/s", "frac": achieved / peak,
-                         # committed ncu capture of the default C2 launch (2^20 instances), else none
-                         "traffic": ncu_traffic("k_solve") if (args.workload == "c2" and n == 1 << 20) else None,
-                         "ncu_hw": ncu_traffic("k_solve_hw") if (args.workload == "c2" and n == 1 << 20) else None,
+            "roofline": {"bound": "alu", "kernel": "k_solve (K1)", "unit": "G FP64-pipe instr/s",
+                         "achieved": executed["achieved"], "peak": peak, "frac": executed["frac"],
+                         "w_div": W_DIV,
+                         "executed": executed, "literal": literal, "ncu_executed": ncu_exec,
+                         "traffic": ncu_record("k_solve") if default_c2 else None,
+                         "ncu_hw": hw,
                          "algorithmic_bytes": int(batch.nbytes()),
                          "hbm": hbm_context(int(batch.nbytes()), solve_ms),
-                         "work_per_launch": work, "member_evals_per_launch": n_member_exec,
-                         "literal_work_per_launch": literal_work, "literal_member_evals_per_launch": n_member,
-                         "literal_equivalent": literal_work / (solve_ms / 1e3) / 1e9,
+                         "member_evals_per_launch": n_member_exec,
+                         "literal_member_evals_per_launch": n_member,
                          "n_tilde_setups_frac": setup_frac,
                          "launch_ms": solve_ms,
-                         "peak_note": "148 SMs x 64 FP64 lanes/clk x max SM clock (DESIGN.md §7); work = FP64 "
-                                      "ops K1 executed (exact n~ pruning), division = 1 op; literal_equivalent "
-                                      "= the unpruned Alg. 1/2 work of the same launch / its time"},
+                         "peak_note": PEAK_NOTE + "; launch_ms = CUDA events around jdob_solve_batch (K0 + K1; "
+                                      "K0 is one block per model, < 0.3 % of the launch list); literal = SURVEY "
+                                      "§8(d)'s Alg. 1/2 work (every n~ swept, oracle-checked counters) with a "
+                                      "division weighted w_div FP64-pipe instructions, > 1 is the pruning's "
+                                      "signature; executed = the work the pruned sweep ran (its counters, same "
+                                      "weights); ncu_executed = the FP64-pipe lane instructions ncu counted for "
+                                      "this launch (profiles/) over the live time"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": 6 * K,

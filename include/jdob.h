@@ -159,8 +159,8 @@ typedef struct {
 /*
  * Bytes of caller-provided device workspace needed by jdob_solve_batch /
  * jdob_eval (which = 0) or jdob_bruteforce (which = 1) for these models (a HOST
- * array of n_models descriptors; only N and B_max are read).  Returns 0 on bad
- * arguments.
+ * array of n_models descriptors; only N and B_max are read), or by jdob_stats
+ * (which = 2; models may be NULL).  Returns 0 on bad arguments.
  */
 JDOB_API size_t jdob_workspace_bytes(const jdob_model *models, int32_t n_models, int32_t which);
 
@@ -184,6 +184,19 @@ JDOB_API size_t jdob_workspace_bytes(const jdob_model *models, int32_t n_models,
  */
 JDOB_API int jdob_solve_batch(const jdob_model *models, int32_t n_models, const jdob_batch *b, int32_t mode,
                      const jdob_result *out, void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * Energy-saving statistics (row a12; R16) of solved instances, as a call of
+ * its own: the same bucketed fields, the same fixed reduction tree and the same bits as the
+ * `stats` output of jdob_solve_batch (described there).
+ *   b    : HOST struct; n_inst, user_off (device) and the optional bucket (device) are read.
+ *   res  : HOST struct of DEVICE arrays: E, E_lc, f_e, n_tilde, status are read (the outputs of
+ *          jdob_solve_batch for b); stats [n_buckets * JDOB_STATS_FIELDS] and n_buckets are
+ *          written / read; the other members are ignored.
+ *   ws   : DEVICE workspace of >= jdob_workspace_bytes(NULL, 0, 2) bytes.
+ * Errors: JDOB_EINVAL (NULL arrays, n_buckets out of range, small workspace), JDOB_ECUDA.
+ */
+JDOB_API int jdob_stats(const jdob_batch *b, const jdob_result *res, void *ws, size_t ws_bytes, void *stream);
 
 /*
  * Same computation from HOST buffers (the end-to-end public call): copies the
@@ -223,6 +236,15 @@ JDOB_API int jdob_release_pool(void);
  *   k = number of grid points f_e(j) = fe_max - j*rho >= fe_min.
  * Outputs (DEVICE scalars): *E_min (+inf if no feasible candidate in range),
  * *idx_min (-1 if none), *status (JDOB_ST_*; the search runs for OK and REQUIRE).
+ * work (DEVICE int64[9], or NULL = skip): counters of the work the pruned scan executed
+ * over the range: [0] vectors visited, [1] vectors past the user-term
+ * bound, [2] past the n_min-only bound, [3] past the exact vector bound (grid loop
+ * entered), [4] candidates evaluated (grid iterations, including the one that ends a
+ * vector's scan), [5] device-frequency divisions executed, [6] candidates skipped by the
+ * edge-only grid skip, [7] vectors whose D6' fails at the first grid point, [8] offloading
+ * users summed over the evaluated candidates.  Requesting
+ * them runs a counting instantiation of the same kernel (same result; the counts depend
+ * on the order in which lanes publish their incumbents, so they vary slightly run to run).
  * Ranges beyond the space size are clipped.  Deterministic.  Unlike the other entry
  * points this call performs one small synchronous device->host read (user_off[0..1]
  * and model_id[0], 20 bytes) on `stream` to select the kernel specialisation for M;
@@ -232,7 +254,7 @@ JDOB_API int jdob_release_pool(void);
  */
 JDOB_API int jdob_bruteforce(const jdob_model *models, int32_t n_models, const jdob_batch *b, int32_t space,
                     uint64_t idx_begin, uint64_t idx_end, double *E_min, int64_t *idx_min, int32_t *status,
-                    void *ws, size_t ws_bytes, void *stream);
+                    int64_t *work, void *ws, size_t ws_bytes, void *stream);
 
 /*
  * Host helper: size of the brute-force index space of an instance with N, M, k

@@ -72,7 +72,9 @@ def lib():
             L.jdob_solve_batch_host.argtypes = [_P(JModel), C.c_int32, _P(JBatch), C.c_int32, _P(JResult),
                                                 C.c_void_p, _P(C.c_int64), _P(C.c_int64)]
             L.jdob_bruteforce.argtypes = [_P(JModel), C.c_int32, _P(JBatch), C.c_int32, C.c_uint64, C.c_uint64,
-                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
+                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
+                                          C.c_void_p]
+            L.jdob_stats.argtypes = [_P(JBatch), _P(JResult), C.c_void_p, C.c_size_t, C.c_void_p]
             L.jdob_bf_space_size.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int64]
             L.jdob_bf_space_size.restype = C.c_uint64
             L.jdob_eval.argtypes = [_P(JModel), C.c_int32, _P(JBatch), C.c_void_p, C.c_void_p, C.c_void_p,
@@ -91,7 +93,7 @@ def lib():
 
 EXPORTED = ("jdob_workspace_bytes", "jdob_solve_batch", "jdob_solve_batch_host", "jdob_bruteforce",
             "jdob_bf_space_size", "jdob_eval", "jdob_grouped_workspace_bytes", "jdob_solve_grouped",
-            "jdob_last_error", "jdob_version", "jdob_release_pool")
+            "jdob_last_error", "jdob_version", "jdob_release_pool", "jdob_stats")
 
 
 def _check(rc):
@@ -207,6 +209,20 @@ def solve_batch(db: DeviceBatch, mode: int = MODE_FULL, f_user: bool = True, cou
     return out
 
 
+def stats(db: DeviceBatch, res: dict, n_buckets: Optional[int] = None, stream=None, out=None):
+    """jdob_stats: the bucketed energy-saving statistics (a12) of solved instances `res` (the dict
+    solve_batch returned for `db`), as a call of its own; returns the [n_buckets, 80] f64 tensor."""
+    torch = _torch()
+    if out is None:
+        nb = n_buckets if n_buckets is not None else db.n_buckets
+        out = torch.empty((nb, STATS_FIELDS), dtype=torch.float64, device=db.device)
+    r = JResult(*[_ptr(res.get(f)) for f in ("E", "E_lc", "t_free_next", "f_e", "n_tilde", "j", "status", "mask")],
+                None, None, out.data_ptr(), int(out.shape[0]), None, None)
+    ws = db.workspace(2)
+    _check(lib().jdob_stats(C.byref(db.jbatch), C.byref(r), ws.data_ptr(), ws.numel(), _stream_handle(stream)))
+    return out
+
+
 def eval_plans(db: DeviceBatch, partition=None, f_e=None, slack: float = 1e-9, f_user: bool = True,
                plans: Optional[dict] = None, stream=None, out: Optional[dict] = None) -> dict:
     """jdob_eval: D20-D22 (generalised, R14/R15) and violation bits for given configurations.
@@ -253,10 +269,12 @@ def bf_space_size(space: int, N: int, M: int, k: int) -> int:
     return int(lib().jdob_bf_space_size(int(space), int(N), int(M), int(k)))
 
 
-def bruteforce(db: DeviceBatch, space: int, idx_begin: int = 0, idx_end: Optional[int] = None, stream=None):
+def bruteforce(db: DeviceBatch, space: int, idx_begin: int = 0, idx_end: Optional[int] = None, stream=None,
+               work: bool = False):
     """jdob_bruteforce over [idx_begin, idx_end) of the single instance of `db`.
 
-    Returns device tensors (E_min [1] f64, idx_min [1] i64, status [1] i32)."""
+    Returns device tensors (E_min [1] f64, idx_min [1] i64, status [1] i32), plus the executed-work
+    counters [9] i64 (include/jdob.h) when `work` is set."""
     torch = _torch()
     if db.n_inst != 1:
         raise ValueError("bruteforce needs a single-instance batch")
@@ -266,11 +284,12 @@ def bruteforce(db: DeviceBatch, space: int, idx_begin: int = 0, idx_end: Optiona
     E = torch.empty(1, dtype=torch.float64, device=dev)
     I = torch.empty(1, dtype=torch.int64, device=dev)
     S = torch.empty(1, dtype=torch.int32, device=dev)
+    W = torch.empty(9, dtype=torch.int64, device=dev) if work else None
     ws = db.workspace(1)
     _check(lib().jdob_bruteforce(db.jmodels, db.n_models, C.byref(db.jbatch), int(space), int(idx_begin),
-                                 int(idx_end), E.data_ptr(), I.data_ptr(), S.data_ptr(), ws.data_ptr(), ws.numel(),
-                                 _stream_handle(stream)))
-    return E, I, S
+                                 int(idx_end), E.data_ptr(), I.data_ptr(), S.data_ptr(), _ptr(W), ws.data_ptr(),
+                                 ws.numel(), _stream_handle(stream)))
+    return (E, I, S, W) if work else (E, I, S)
 
 
 class HostBuffers:

@@ -13,7 +13,7 @@
 namespace jdob {
 void launch_bruteforce_impl(const DevModel *models, const DevBatch &b, int model_id, int N, int M, int space,
                             unsigned long long idx_begin, unsigned long long idx_end, void *ws, double *E_min,
-                            long long *idx_min, int *status, cudaStream_t s);
+                            long long *idx_min, int *status, unsigned long long *work, cudaStream_t s);
 size_t bf_workspace_bytes();
 }  // namespace jdob
 
@@ -194,6 +194,7 @@ const char *jdob_last_error(void) { return g_err.c_str(); }
 const char *jdob_version(void) { return "jdob-b200 0.1 (sm_100a)"; }
 
 size_t jdob_workspace_bytes(const jdob_model *models, int32_t n_models, int32_t which) {
+    if (which == 2) return stats_partial_bytes();  // jdob_stats: no model part
     if (!models || n_models < 1) return 0;
     for (int i = 0; i < n_models; i++)
         if (models[i].N < 1 || models[i].N > JDOB_MAX_N || models[i].B_max < 1 ||
@@ -269,6 +270,34 @@ int jdob_solve_batch(const jdob_model *models, int32_t n_models, const jdob_batc
         if ((rc = cuda_check("stats"))) return rc;
     }
     return JDOB_OK;
+}
+
+int jdob_stats(const jdob_batch *b, const jdob_result *res, void *ws, size_t ws_bytes, void *stream) {
+    g_err.clear();
+    if (!b || !res) return fail(JDOB_EINVAL, "stats: NULL batch or result");
+    if (b->n_inst < 0) return fail(JDOB_EINVAL, "n_inst < 0");
+    if (!res->stats) return fail(JDOB_EINVAL, "stats: NULL stats array");
+    if (res->n_buckets < 1 || res->n_buckets > JDOB_MAX_BUCKETS)
+        return fail(JDOB_EINVAL, "n_buckets = %d outside [1, %d]", res->n_buckets, JDOB_MAX_BUCKETS);
+    if (b->n_inst > 0 && (!b->user_off || !res->E || !res->E_lc || !res->f_e || !res->n_tilde || !res->status))
+        return fail(JDOB_EINVAL, "stats: NULL input array");
+    if (!ws || ws_bytes < stats_partial_bytes())
+        return fail(JDOB_EINVAL, "workspace %zu bytes < %zu", ws_bytes, stats_partial_bytes());
+    DevResult dr;
+    dr.E = res->E;
+    dr.E_lc = res->E_lc;
+    dr.t_free_next = res->t_free_next;
+    dr.f_e = res->f_e;
+    dr.n_tilde = res->n_tilde;
+    dr.j = res->j;
+    dr.status = res->status;
+    dr.mask = res->mask;
+    dr.f_user = nullptr;
+    dr.counts = nullptr;
+    dr.partition = nullptr;
+    dr.work = nullptr;
+    launch_stats(to_dev(b), dr, (double *)ws, res->stats, res->n_buckets, (cudaStream_t)stream);
+    return cuda_check("stats");
 }
 
 static size_t og_work_bytes(int64_t n, int64_t nu) {
@@ -378,8 +407,8 @@ int jdob_eval(const jdob_model *models, int32_t n_models, const jdob_batch *b, c
 }
 
 int jdob_bruteforce(const jdob_model *models, int32_t n_models, const jdob_batch *b, int32_t space,
-                    uint64_t idx_begin, uint64_t idx_end, double *E_min, int64_t *idx_min, int32_t *status, void *ws,
-                    size_t ws_bytes, void *stream) {
+                    uint64_t idx_begin, uint64_t idx_end, double *E_min, int64_t *idx_min, int32_t *status,
+                    int64_t *work, void *ws, size_t ws_bytes, void *stream) {
     g_err.clear();
     int rc = check_models(models, n_models);
     if (rc) return rc;
@@ -403,7 +432,7 @@ int jdob_bruteforce(const jdob_model *models, int32_t n_models, const jdob_batch
     if ((rc = prepare_models(models, n_models, (char *)ws, &dm, s))) return rc;
     void *bws = (char *)ws + models_bytes(models, n_models);
     launch_bruteforce_impl(dm, to_dev(b), (mid >= 0 && mid < n_models) ? mid : 0, N, M, space, idx_begin, idx_end,
-                           bws, E_min, (long long *)idx_min, status, s);
+                           bws, E_min, (long long *)idx_min, status, (unsigned long long *)work, s);
     return cuda_check("bruteforce");
 }
 

@@ -105,8 +105,15 @@ __global__ void k_bf_setup(const DevModel *models, DevBatch b, int space, BfHead
     for (long long j = lane; j < kt; j += 32) invtab[j] = 1.0 / grid_fe(b.fe_max[0], b.rho[0], j);
 }
 
-// EXACT: M == MAXM, so every per-user guard folds at compile time (the C4 case, M = 8)
-template <int MAXM, bool EXACT>
+// EXACT: M == MAXM, so every per-user guard folds at compile time (the C4 case, M = 8).
+// WORK: count the work the pruned scan executes (diagnostic instantiation, launched only when the
+// caller asks for the counters; the product instantiation carries no counter code):
+//   [0] vectors visited  [1] past the user-term bound  [2] past the n_min-only bound
+//   [3] past the exact vector bound (j loop entered)    [4] candidates evaluated (j iterations,
+//   including the one that ends a scan)  [5] Gamma divisions executed  [6] candidates skipped by
+//   the edge-only j skip  [7] vectors whose D6' fails at the first grid point  [8] offloaders
+//   summed over the evaluated candidates
+template <int MAXM, bool EXACT, bool WORK>
 #ifndef JDOB_BF_MINB
 #define JDOB_BF_MINB 4
 #endif
@@ -114,8 +121,10 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                                                            unsigned long long idx_begin, unsigned long long idx_end,
                                                            BfHeader *hdr, const double *tab,
                                                            const double *user, const double *invtab,
-                                                           double *part_E, long long *part_idx) {
+                                                           double *part_E, long long *part_idx,
+                                                           unsigned long long *work) {
     extern __shared__ double sm[];
+    unsigned long long wk[9] = {0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
     const int st = hdr->status;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     __shared__ double wE[kBfWarps];
@@ -272,6 +281,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                 for (int t = 0; t < L; t++) {
                 const unsigned long long vec = blk ? unit * (unsigned long long)radix + t : unit;
                 if (vec < vb || vec >= ve) continue;
+                if constexpr (WORK) wk[0]++;
                 // the partition vector
                 int nv[MAXM];
                 if (blk) {
@@ -296,6 +306,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                 }
                 const double inc = __longlong_as_double(*(volatile long long *)&hdr->best_bits);
                 if (lbu >= bestE || lbu > inc) continue;  // the edge term only adds (>= 0)
+                if constexpr (WORK) wk[1]++;
 #endif
                 int nmin = N;
                 double l_o = dinf();
@@ -338,6 +349,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                     const double LB = lbu + (sPlb[nmin] * fel) * fel;
                     if (LB >= bestE || LB > inc) continue;
                 }
+                if constexpr (WORK) wk[2]++;
 #endif
                 // batch sizes, suffix sums S_n and Psi (descending n), per-user S_{n_m + 1}
                 double Sm[MAXM];
@@ -416,13 +428,17 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                     if (any) {
                         const double fe0 = grid_fe(fe_max, rho, (long long)jlo);
                         const double inv0 = (jlo < (unsigned long long)kt) ? sInv[jlo] : 1.0 / fe0;
-                        if (!(t_free + Smin * inv0 <= l_o)) continue;  // D6' fails at once: no candidate
+                        if (!(t_free + Smin * inv0 <= l_o)) {  // D6' fails at once: no candidate
+                            if constexpr (WORK) wk[7]++;
+                            continue;
+                        }
                         const double fd = div_lb(Smin, Xd7);  // <= Smin / X (X of the n_min-only bound)
                         fel = (fd > fel) ? fd : fel;
                     }
                     const double LB = lbu + (Psi * fel) * fel;
                     if (LB >= bestE || LB > inc) continue;
                 }
+                if constexpr (WORK) wk[3]++;
                 const double best_before = bestE;
 #endif
                 unsigned long long j0 = jlo;
@@ -447,6 +463,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                         j0 = lo;
                     }
                 }
+                if constexpr (WORK) wk[6] += j0 - jlo;
 #endif
                 if constexpr (REG) {
                     // M <= 8: (A) budgets and the exact low-clamp test for every offloader, no
@@ -456,6 +473,10 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                     for (unsigned long long j = j0; j < jhi; j++) {
                         const double fe = grid_fe(fe_max, rho, (long long)j);
                         const double inv = (j < (unsigned long long)kt) ? sInv[j] : 1.0 / fe;
+                        if constexpr (WORK) {
+                            wk[4]++;
+                            wk[8] += __popc(offm);
+                        }
                         if (any && !(t_free + Smin * inv <= l_o)) break;  // D6' (monotone in j)
                         double bud[MAXM], fv[MAXM];
                         unsigned need = 0u;
@@ -477,6 +498,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                                     } else if (!(bud[m] > 0.0)) {
                                         feas = false;
                                     } else {
+                                        if constexpr (WORK) wk[5]++;
                                         const double G = zvr[m] / bud[m];
                                         if (G > sFmax[m]) feas = false;  // D7' with D13 (exact, R10)
                                         fv[m] = (G < fv[m]) ? fv[m] : G;
@@ -503,6 +525,10 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                 for (unsigned long long j = j0; j < jhi; j++) {
                         const double fe = grid_fe(fe_max, rho, (long long)j);
                         const double inv = (j < (unsigned long long)kt) ? sInv[j] : 1.0 / fe;
+                        if constexpr (WORK) {
+                            wk[4]++;
+                            wk[8] += __popc(offm);
+                        }
                         if (any && !(t_free + Smin * inv <= l_o)) break;  // D6' (monotone in j)
                         double E = 0.0;
                         bool feas = true;
@@ -539,6 +565,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                                             feas = false;
                                             break;
                                         }
+                                        if constexpr (WORK) wk[5]++;
                                         const double G = zv / budget;
                                         if (G > sFmax[m]) {  // D7' with D13 (exact, R10)
                                             feas = false;
@@ -567,6 +594,14 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
 #endif
                 }  // t: the vectors of the lane's block
             }
+        }
+    }
+    if constexpr (WORK) {
+#pragma unroll
+        for (int q = 0; q < 9; q++) {
+            unsigned long long v = wk[q];
+            for (int d = 16; d >= 1; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+            if (lane == 0 && v) atomicAdd(&work[q], v);
         }
     }
     // warp, then block argmin over (E, idx)
@@ -623,15 +658,22 @@ size_t bf_workspace_bytes() {
 template <int MAXM, bool EXACT = false>
 static void launch_main(const DevModel *models, int model_id, int space, unsigned long long ib, unsigned long long ie,
                         BfHeader *hdr, const double *tab, const double *user, const double *inv,
-                        double *part_E, long long *part_idx, size_t smem, cudaStream_t s) {
-    cudaFuncSetAttribute(k_bf_main<MAXM, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_bf_main<MAXM, EXACT><<<kBfBlocks, kBfWarps * 32, smem, s>>>(models, model_id, space, ib, ie, hdr, tab, user, inv,
-                                                         part_E, part_idx);
+                        double *part_E, long long *part_idx, unsigned long long *work, size_t smem, cudaStream_t s) {
+    if (work) {
+        cudaMemsetAsync(work, 0, 9 * sizeof(unsigned long long), s);
+        cudaFuncSetAttribute(k_bf_main<MAXM, EXACT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_bf_main<MAXM, EXACT, true><<<kBfBlocks, kBfWarps * 32, smem, s>>>(models, model_id, space, ib, ie, hdr, tab,
+                                                                            user, inv, part_E, part_idx, work);
+    } else {
+        cudaFuncSetAttribute(k_bf_main<MAXM, EXACT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_bf_main<MAXM, EXACT, false><<<kBfBlocks, kBfWarps * 32, smem, s>>>(models, model_id, space, ib, ie, hdr, tab,
+                                                                             user, inv, part_E, part_idx, nullptr);
+    }
 }
 
 void launch_bruteforce_impl(const DevModel *models, const DevBatch &b, int model_id, int N, int M, int space,
                             unsigned long long idx_begin, unsigned long long idx_end, void *ws, double *E_min,
-                            long long *idx_min, int *status, cudaStream_t s) {
+                            long long *idx_min, int *status, unsigned long long *work, cudaStream_t s) {
     char *p = (char *)ws;
     BfHeader *hdr = (BfHeader *)p;
     p += 256;
@@ -649,14 +691,14 @@ void launch_bruteforce_impl(const DevModel *models, const DevBatch &b, int model
     const size_t smem = sizeof(double) * (5 * (size_t)(N + 1) * Mc + 128 + kInvTab + 17 * kBfThreads + 128 +
                                           (size_t)(N + 1) * Mc);
     if (Mc == 8)
-        launch_main<8, true>(models, model_id, space, idx_begin, idx_end, hdr, tab, user, inv, part_E, part_idx, smem,
+        launch_main<8, true>(models, model_id, space, idx_begin, idx_end, hdr, tab, user, inv, part_E, part_idx, work, smem,
                              s);
     else if (Mc <= 8)
-        launch_main<8>(models, model_id, space, idx_begin, idx_end, hdr, tab, user, inv, part_E, part_idx, smem, s);
+        launch_main<8>(models, model_id, space, idx_begin, idx_end, hdr, tab, user, inv, part_E, part_idx, work, smem, s);
     else if (Mc <= 16)
-        launch_main<16>(models, model_id, space, idx_begin, idx_end, hdr, tab, user, inv, part_E, part_idx, smem, s);
+        launch_main<16>(models, model_id, space, idx_begin, idx_end, hdr, tab, user, inv, part_E, part_idx, work, smem, s);
     else
-        launch_main<32>(models, model_id, space, idx_begin, idx_end, hdr, tab, user, inv, part_E, part_idx, smem, s);
+        launch_main<32>(models, model_id, space, idx_begin, idx_end, hdr, tab, user, inv, part_E, part_idx, work, smem, s);
     k_bf_final<<<1, 32, 0, s>>>(hdr, part_E, part_idx, kBfBlocks, E_min, idx_min, status);
 }
 

@@ -25,7 +25,8 @@ def declared_symbols():
 
 def test_header_symbols_exported(L):
     syms = declared_symbols()
-    assert len(syms) == 11, syms
+    assert len(syms) == 12, syms
+    assert set(syms) == set(__import__("paper_2504_14611_b200").EXPORTED), syms
     for s in syms:
         assert hasattr(L, s), s
     import paper_2504_14611_b200 as J
@@ -64,7 +65,7 @@ def test_argument_errors_without_gpu(L):
     assert L.jdob_solve_batch(ms, 1, C.byref(b), 0, C.byref(r), None, 0, None) == B.EINVAL
     assert b"NULL" in L.jdob_last_error()
     assert L.jdob_solve_batch(None, 0, None, 0, None, None, 0, None) == B.EINVAL
-    assert L.jdob_bruteforce(ms, 1, C.byref(b), 0, 0, 1, None, None, None, None, 0, None) == B.EINVAL
+    assert L.jdob_bruteforce(ms, 1, C.byref(b), 0, 0, 1, None, None, None, None, None, 0, None) == B.EINVAL
 
 
 def test_no_cpu_fallback():

@@ -219,6 +219,18 @@ def test_stats_small_exact(J):
         assert rel_close(gpu["stats"][:, f], st[:, f], 1e-9)
 
 
+def test_stats_entry_point_same_bits(J):
+    # jdob_stats as a call of its own: the same fixed tree, so the same bits as the solve's stats output
+    b = g.random_batch(seed=121, n_inst=5000, M_hi=32, N_hi=6, k_max=40)
+    db = J.DeviceBatch(b)
+    res = J.solve_batch(db, stats=True, n_buckets=32)
+    sep = J.stats(db, res, n_buckets=32)
+    assert_bits_equal(sep.cpu().numpy().reshape(-1), res["stats"].cpu().numpy().reshape(-1), "jdob_stats")
+    st = O.stats(b, O.solve_batch(b), n_buckets=32)
+    for f in (0, 3, 4, 7, 8):
+        assert_bits_equal(sep.cpu().numpy()[:, f], st[:, f], f"stats[{f}]")
+
+
 def test_determinism(J):
     b = g.config_batch("c3", n_inst=20000)
     db = J.DeviceBatch(b)
@@ -571,3 +583,62 @@ def test_og_more_than_32_users(J):
     big.R[int(big.user_off[3]) + 2] = np.nan          # malformed user -> BADPARAM, NaN answer
     big.T[int(big.user_off[4]) + 7] = 1e-6            # locally infeasible -> LOCAL_INFEASIBLE, LC answer
     _og_parity(J, g.concat([small, big]))
+
+
+def _c4_oracle_chunks():
+    import json
+    import os
+    p = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                     "r02_c4_oracle_full.ckpt.jsonl")
+    if not os.path.exists(p):
+        return None
+    return [json.loads(line) for line in open(p)]
+
+
+def test_bf_c4_full_space_vs_oracle(J):
+    """The whole C4 general space (2.75e10 candidates) against the oracle's literal scan of every
+    candidate (profiles/r02_c4_oracle_full.*, written by tools/c4_oracle_full.py, which calls only
+    oracle/): the argmin of each of the 256 vector-aligned chunks is equal, bits and index, and so is
+    the argmin over the whole space."""
+    chunks = _c4_oracle_chunks()
+    if chunks is None or len(chunks) < 256:
+        pytest.skip("full-space oracle record not committed")
+    b = g.config_batch("c4")
+    db = J.DeviceBatch(b)
+    size = O.bf_space_size(b, 0)
+    best = (float("inf"), -1)
+    for c in sorted(chunks, key=lambda r: r["chunk"]):
+        E, I, S = J.bruteforce(db, 0, c["lo"], c["hi"])
+        Eo = float.fromhex(c["E"])
+        assert (float(E.item()), int(I.item())) == (Eo, c["idx"]), c["chunk"]
+        if Eo < best[0]:
+            best = (Eo, c["idx"])
+    E, I, _ = J.bruteforce(db, 0, 0, size)
+    assert (float(E.item()), int(I.item())) == best
+
+
+def test_bf_work_counters(J):
+    """The counting instantiation of K2 returns the same argmin; its counters are consistent: every
+    vector of the range is visited once, each pruning stage passes a subset of the previous one, and
+    the evaluated candidates are at most the range's."""
+    b = g.config_batch("c4")
+    db = J.DeviceBatch(b)
+    k = 64
+    for lo, hi in ((0, 12 ** 8 * k), (12 ** 7 * k + 5, 3 * 12 ** 7 * k - 7)):
+        E, I, S = J.bruteforce(db, 0, lo, hi)
+        Ew, Iw, Sw, W = J.bruteforce(db, 0, lo, hi, work=True)
+        assert (float(Ew.item()), int(Iw.item())) == (float(E.item()), int(I.item()))
+        w = W.cpu().numpy()
+        nvec = (hi + k - 1) // k - lo // k
+        assert w[0] == nvec
+        assert w[0] >= w[1] >= w[2] >= w[3] >= 0
+        assert w[4] + w[6] <= hi - lo
+        assert w[8] <= 8 * w[4] and w[5] <= w[8]
+    # identical space and a small instance: the scan without pruning opportunities counts everything
+    t = g.toy_instance("toy-4")
+    dt = J.DeviceBatch(t)
+    for space in (0, 1):
+        E, I, S, W = J.bruteforce(dt, space, work=True)
+        Eo, Io, So = O.bf(t, space)
+        assert (float(E.item()), int(I.item())) == (Eo, Io)
+        assert int(W[0].item()) == O.bf_space_size(t, space) // O.grid_k(t)
