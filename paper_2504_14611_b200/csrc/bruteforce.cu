@@ -15,7 +15,7 @@
 
 namespace jdob {
 
-constexpr int kInvTab = 2048;  // 1/f_e(j) cached in shared memory for j < kInvTab
+constexpr int kInvTab = 256;   // 1/f_e(j) cached in shared memory for j < kInvTab (C4: k = 64, C5: <= 191)
 constexpr int kBfThreads = kBfWarps * 32;
 
 #ifndef JDOB_BF_PRUNE
@@ -31,7 +31,24 @@ struct BfHeader {
     unsigned long long best_bits;  // incumbent energy (bits of a double >= 0), shared by every block
 };
 
-__global__ void k_bf_setup(const DevModel *models, DevBatch b, int space, BfHeader *hdr, double *tab /*[4][N+1][M]*/,
+// Per-(n, user) tables are stored user-major, element m (N + 1) + n: the brute force gathers them with
+// a lane-dependent n for a fixed user, so consecutive n must fall in distinct shared-memory banks.
+#ifndef JDOB_BF_NO_TRANS
+__device__ __forceinline__ int tix(int n, int m, int N, int M) { return m * (N + 1) + n; }
+#else
+__device__ __forceinline__ int tix(int n, int m, int N, int M) { return n * M + m; }
+#endif
+
+// Base-(N+1) digits of a lane's block index (users 0 .. M-2).  (Packing them as 6-bit fields of one
+// 64-bit word frees registers but costs more instructions than the spills it removes: measured.)
+template <int MAXM>
+struct Digits {
+    int a[MAXM];
+    __device__ __forceinline__ int get(int m) const { return a[m]; }
+    __device__ __forceinline__ void set(int m, int v) { a[m] = v; }
+};
+
+__global__ void k_bf_setup(const DevModel *models, DevBatch b, int space, BfHeader *hdr, double *tab /*[5][M][N+1]*/,
                            double *user /*[4][32]: eloc fmin fmax T*/, double *invtab) {
     const int lane = threadIdx.x & 31;
     long long off, k;
@@ -91,14 +108,14 @@ __global__ void k_bf_setup(const DevModel *models, DevBatch b, int space, BfHead
         const int NM = (N + 1) * M;
         for (int n = 0; n <= N; n++) {
             const double OR = md.O[n] / x.R;
-            tab[0 * NM + n * M + lane] = OR;                  // O_n / R_m
-            tab[1 * NM + n * M + lane] = x.z * md.v[n];       // zeta_m v_n
-            tab[2 * NM + n * M + lane] = x.k * md.u[n];       // kappa_m u_n
-            tab[3 * NM + n * M + lane] = OR * x.p;            // (O_n / R_m) p_m
+            const int t = tix(n, lane, N, M);
+            tab[0 * NM + t] = OR;                  // O_n / R_m
+            tab[1 * NM + t] = x.z * md.v[n];       // zeta_m v_n
+            tab[2 * NM + t] = x.k * md.u[n];       // kappa_m u_n
+            tab[3 * NM + t] = OR * x.p;            // (O_n / R_m) p_m
             // energy lower bound of user m at partition point n: the f_min offloader
             // term for n < N, e_loc for n = N -- the same expressions as the kernel's bound
-            tab[4 * NM + n * M + lane] = (n < N) ? (((x.k * md.u[n]) * x.f0) * x.f0) + OR * x.p
-                                                 : user[0 * 32 + lane];
+            tab[4 * NM + t] = (n < N) ? (((x.k * md.u[n]) * x.f0) * x.f0) + OR * x.p : user[0 * 32 + lane];
         }
     }
     const long long kt = k < kInvTab ? k : kInvTab;
@@ -139,16 +156,24 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
         const DevModel &md = models[model_id];
         const int NM = (N + 1) * M;
         double *sOR = sm, *sZV = sm + NM, *sKU = sm + 2 * NM, *sUP = sm + 3 * NM;
-        double *sLB = sm + 4 * NM;  // [N+1][M] per-user bound terms
+        double *sLB = sm + 4 * NM;  // [M][N+1] per-user bound terms (tix)
         double *sEl = sm + 5 * NM, *sFmin = sEl + 32, *sFmax = sEl + 64, *sT = sEl + 96;
         double *sInv = sEl + 128;
         double *sSuf = sInv + kInvTab;  // [17][kBfThreads] per-lane suffix sums (N <= 15 path)
         double *sSlb = sSuf + 17 * kBfThreads, *sPlb = sSlb + 64;  // [nmin] lower bounds of S_{nmin+1}, Psi
-        double *sG = sPlb + 64;  // [n][m] lower bound of user m's arrival O/R + zv/f* when offloading at n
+        double *sG = sPlb + 64;  // [M][N+1] lower bound of user m's arrival O/R + zv/f* when offloading at n
+        // d_n(b) A_n and c_n(b) A_n for b = 0..M (row stride M + 1): the batch sums gather them with a
+        // lane-dependent b, consecutive b in distinct banks
+        double *sDA = sG + (N + 1) * M, *sCA = sDA + (N + 1) * (M + 1);
         const long long kt = k < kInvTab ? k : kInvTab;
         for (int x = threadIdx.x; x < 5 * NM; x += blockDim.x) sm[x] = tab[x];
         for (int x = threadIdx.x; x < 128; x += blockDim.x) sEl[x] = user[x];
         for (long long x = threadIdx.x; x < kt; x += blockDim.x) sInv[x] = invtab[x];
+        for (int x = threadIdx.x; x < (N + 1) * (M + 1); x += blockDim.x) {
+            const int n = x / (M + 1), bb = x % (M + 1);
+            sDA[x] = md.dA[n * B1 + bb];
+            sCA[x] = md.cA[n * B1 + bb];
+        }
         if (threadIdx.x == 0) {
             // For a vector whose first offloaded sub-task is nmin + 1, b_n >= 1 exactly for n > nmin and
             // b_n = 0 below, so S_{nmin+1} = RN-sum_{n=N..nmin+1} d_n(b_n) A_n >= the same RN-sum of
@@ -173,8 +198,8 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
         // gives S / f_e <= ((l_o - O/R)(1 + u) - (zv / f_max)(1 - 2u)) / (1 - u)^2 (u = 2^-53).  With
         // G = RN(O/R + RN(zv RD(1/f_max))) (1 - 2^-46) <= (O/R + zv/f_max)(1 - 2^-47) and the margins
         // of X below, S / X <= f_e for every feasible candidate.
-        for (int x = threadIdx.x; x < N * M; x += blockDim.x) {
-            const int m = x % M;
+        for (int y = threadIdx.x; y < N * M; y += blockDim.x) {
+            const int m = y % M, x = tix(y / M, m, N, M);
 #ifndef JDOB_BF_NO_D7_FE
             sG[x] = (sOR[x] + sZV[x] * recip_rd(sFmax[m])) * (1.0 - 0x1p-46);
 #else
@@ -192,8 +217,8 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
         // RN(zv / X) with 0 < budget <= X; X <= 0 or RN(zv / X) > f_max leave no feasible candidate.
         {
             const double inv_max = sInv[0];  // RN(1 / f_e(0)) = RN(1 / f_e,max)
-            for (int x = threadIdx.x; x < N * M; x += blockDim.x) {
-                const int n = x / M, m = x % M;
+            for (int y = threadIdx.x; y < N * M; y += blockDim.x) {
+                const int n = y / M, m = y % M, x = tix(n, m, N, M);
                 const double zv = sZV[x];
                 if (zv == 0.0) continue;  // f* = f_min (R9): the f_min term stands
                 const double X = (sT[m] - sOR[x]) - sSlb[n] * inv_max;
@@ -231,18 +256,19 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
             const unsigned long long nchunks = (uend - ubeg + 31) / 32;
             const unsigned long long gw = (unsigned long long)blockIdx.x * kBfWarps + w;
             const unsigned long long nw = (unsigned long long)gridDim.x * kBfWarps;
-            const double *dA = md.dA, *cA = md.cA;
-            int dig[MAXM], sdig[MAXM];  // digits of the block index: users 0 .. M-2 (dig[M-1] unused)
+            const double *dA = sDA, *cA = sCA;
+            const int B1s = M + 1;  // row stride of the staged tables
+            Digits<MAXM> dig, sdig;  // digits of the block index and of the stride: users 0 .. M-2
             {
                 unsigned long long t = ubeg + gw * 32 + lane, u = 32ull * nw;
 #pragma unroll
                 for (int m = MAXM - 1; m >= 0; m--) {
-                    dig[m] = 0;
-                    sdig[m] = 0;
+                    dig.set(m, 0);
+                    sdig.set(m, 0);
                     if (m < M - 1 && blk) {
-                        dig[m] = (int)(t % (unsigned long long)radix);
+                        dig.set(m, (int)(t % (unsigned long long)radix));
                         t /= (unsigned long long)radix;
-                        sdig[m] = (int)(u % (unsigned long long)radix);
+                        sdig.set(m, (int)(u % (unsigned long long)radix));
                         u /= (unsigned long long)radix;
                     }
                 }
@@ -253,9 +279,9 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
 #pragma unroll
                 for (int m = MAXM - 1; m >= 0; m--) {
                     if (m < M - 1) {
-                        const int d = dig[m] + sdig[m] + carry;
+                        const int d = dig.get(m) + sdig.get(m) + carry;
                         carry = d >= radix ? 1 : 0;
-                        dig[m] = carry ? d - radix : d;
+                        dig.set(m, carry ? d - radix : d);
                     }
                 }
             };
@@ -270,14 +296,19 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                     for (int m = 0; m < MAXM; m++)
                         if (m < M - 1) {
 #if JDOB_BF_PRUNE
-                            lbu_hi = lbu_hi + sLB[dig[m] * M + m];
+                            lbu_hi = lbu_hi + sLB[tix(dig.get(m), m, N, M)];
 #endif
-                            if (dig[m] < N) {
-                                if (dig[m] < nmin_hi) nmin_hi = dig[m];
+                            const int dm = dig.get(m);
+                            if (dm < N) {
+                                if (dm < nmin_hi) nmin_hi = dm;
                                 lo_hi = (sT[m] < lo_hi) ? sT[m] : lo_hi;
                             }
                         }
                 }
+#if JDOB_BF_PRUNE
+                // the incumbent, read once per block of vectors (it only decides how much is skipped)
+                const double inc = __longlong_as_double(*(volatile long long *)&hdr->best_bits);
+#endif
                 for (int t = 0; t < L; t++) {
                 const unsigned long long vec = blk ? unit * (unsigned long long)radix + t : unit;
                 if (vec < vb || vec >= ve) continue;
@@ -286,7 +317,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                 int nv[MAXM];
                 if (blk) {
 #pragma unroll
-                    for (int m = 0; m < MAXM; m++) nv[m] = (m == M - 1) ? t : dig[m];
+                    for (int m = 0; m < MAXM; m++) nv[m] = (m == M - 1) ? t : dig.get(m);
                 } else {
                     const unsigned long long mask = vec & ((1ull << M) - 1ull);
                     const int nt = (int)(vec >> M);
@@ -298,13 +329,12 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                 // stop here
                 double lbu = 0.0;
                 if (blk) {
-                    lbu = lbu_hi + sLB[t * M + (M - 1)];
+                    lbu = lbu_hi + sLB[tix(t, M - 1, N, M)];
                 } else {
 #pragma unroll
                     for (int m = 0; m < MAXM; m++)
-                        if (m < M) lbu = lbu + sLB[nv[m] * M + m];
+                        if (m < M) lbu = lbu + sLB[tix(nv[m], m, N, M)];
                 }
-                const double inc = __longlong_as_double(*(volatile long long *)&hdr->best_bits);
                 if (lbu >= bestE || lbu > inc) continue;  // the edge term only adds (>= 0)
                 if constexpr (WORK) wk[1]++;
 #endif
@@ -334,6 +364,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                 // The vector bound below with S_{nmin+1} and Psi replaced by their lower bounds from
                 // nmin alone (sSlb, sPlb): skips most vectors before the batch-size and suffix sums
                 {
+                    const double Slo = sSlb[nmin], Plo = sPlb[nmin];
                     double fel = grid_fe(fe_max, rho, (long long)(jhi - 1));
                     if (nmin < N) {
                         // D6' (t_free) and D7' of the users offloading at nmin (their arrival): f_e >=
@@ -341,12 +372,12 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                         double gmax = t_free;
 #pragma unroll
                         for (int m = 0; m < MAXM; m++)
-                            if (m < M && nv[m] == nmin) gmax = (sG[nmin * M + m] > gmax) ? sG[nmin * M + m] : gmax;
+                            if (m < M && nv[m] == nmin) gmax = (sG[tix(nmin, m, N, M)] > gmax) ? sG[tix(nmin, m, N, M)] : gmax;
                         Xd7 = __dmul_ru(__dadd_ru(__dmul_ru(l_o, 1.0 + 0x1p-48), -gmax), 1.0 + 0x1p-48);
-                        const double fd = div_lb(sSlb[nmin], Xd7);  // <= S_{nmin+1} / X
+                        const double fd = div_lb(Slo, Xd7);  // <= S_{nmin+1} / X
                         fel = (fd > fel) ? fd : fel;
                     }
-                    const double LB = lbu + (sPlb[nmin] * fel) * fel;
+                    const double LB = lbu + (Plo * fel) * fel;
                     if (LB >= bestE || LB > inc) continue;
                 }
                 if constexpr (WORK) wk[2]++;
@@ -369,8 +400,8 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                     for (int n = N; n >= 1; n--) {
                         ge += (int)((hist >> (4 * n)) & 0xfull);
                         const int bn = M - ge;
-                        S = S + ((bn > 0) ? dA[n * B1 + bn] : 0.0);
-                        Psi = Psi + ((bn > 0) ? cA[n * B1 + bn] : 0.0);
+                        S = S + ((bn > 0) ? dA[n * B1s + bn] : 0.0);
+                        Psi = Psi + ((bn > 0) ? cA[n * B1s + bn] : 0.0);
                         Sa[n * kBfThreads] = S;
                     }
 #pragma unroll
@@ -383,8 +414,8 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
 #pragma unroll
                         for (int m = 0; m < MAXM; m++) bn += (m < M && nv[m] < n) ? 1 : 0;
                         if (bn > 0) {
-                            S = S + dA[n * B1 + bn];
-                            Psi = Psi + cA[n * B1 + bn];
+                            S = S + dA[n * B1s + bn];
+                            Psi = Psi + cA[n * B1s + bn];
                         } else {
                             S = S + 0.0;
                             Psi = Psi + 0.0;
@@ -406,7 +437,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                     if (m < M && nv[m] < N) {
                         offm |= 1u << m;
                         if constexpr (REG) {
-                            const int x = nv[m] * M + m;
+                            const int x = tix(nv[m], m, N, M);
                             lo[m] = l_o - sOR[x];
                             zvr[m] = sZV[x];
                             kur[m] = sKU[x];
@@ -544,7 +575,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                                     ku = kur[m];
                                     up = upr[m];
                                 } else {
-                                    const int x = nv[m] * M + m;
+                                    const int x = tix(nv[m], m, N, M);
                                     lom = l_o - sOR[x];
                                     zv = sZV[x];
                                     ku = sKU[x];
@@ -689,7 +720,7 @@ void launch_bruteforce_impl(const DevModel *models, const DevBatch &b, int model
     k_bf_setup<<<1, 32, 0, s>>>(models, b, space, hdr, tab, user, inv);
     const int Mc = (M >= 1 && M <= kMaxM) ? M : 1;
     const size_t smem = sizeof(double) * (5 * (size_t)(N + 1) * Mc + 128 + kInvTab + 17 * kBfThreads + 128 +
-                                          (size_t)(N + 1) * Mc);
+                                          (size_t)(N + 1) * Mc + 2 * (size_t)(N + 1) * (Mc + 1));
     if (Mc == 8)
         launch_main<8, true>(models, model_id, space, idx_begin, idx_end, hdr, tab, user, inv, part_E, part_idx, work, smem,
                              s);

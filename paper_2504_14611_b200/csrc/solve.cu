@@ -44,19 +44,20 @@ namespace jdob {
 
 constexpr int kInvCache = 192;    // 1/f_e(j) cached for j < kInvCache
 
-// UNI: the uniform-users kernel keeps one copy of the per-user values every member shares (user 0's)
-// and no per-user parameter tables (each lane's own values stay in registers): 4.4 KB per warp
-// instead of 7.7 KB, so shared memory does not limit its occupancy.
-template <bool UNI>
+// Order of the pruned n~ sweep (DESIGN.md §4 "n~ pruning"): 0 ascending n~ (the literal order),
+// 1 ascending with the bound also capped at E_LC, 2 best first (smallest lower bound first).
+#ifndef JDOB_PRUNE_ORDER
+#define JDOB_PRUNE_ORDER 0
+#endif
+
 struct SolveSmem {
-    static constexpr int MU = UNI ? 1 : kMaxM;  // per-user slots of values shared by uniform users
     // per-user values as 16-byte pairs (lane stride 16 B: 4-way store conflicts at most)
-    double2 orzv[MU];                    // O_n~/R_m, zeta_m v_n~
-    double2 kuup[MU];                    // kappa_m u_n~, (O_n~/R_m) p_m
+    double2 orzv[kMaxM];                 // O_n~/R_m, zeta_m v_n~
+    double2 kuup[kMaxM];                 // kappa_m u_n~, (O_n~/R_m) p_m
     double2 et[kMaxM];                   // e_loc,m, th_{r_m} if r_m >= i^ else +inf
-    double2 fmm[MU];                     // f_m,min, f_m,max
-    double kap[MU], pu[MU];              // kappa_m, p_m (read across lanes by the general lower bound)
-    double T[kMaxM], gam[MU];
+    double2 fmm[kMaxM];                  // f_m,min, f_m,max
+    double R[kMaxM], z[kMaxM], f1[kMaxM], kap[kMaxM], pu[kMaxM];  // user parameters (lane = user)
+    double T[kMaxM], gam[kMaxM];
     double th[kMaxM];
     double2 Lg[kMaxM];                   // per sorted position p: {l_o = L_p, guard threshold phi/(L_p - t_free)}
     double2 pp[kMaxM];                   // per sorted position p: {phi_n~(M - p), psi_n~(M - p)}
@@ -65,14 +66,13 @@ struct SolveSmem {
     double2 inv_key;                     // (f_e,max, rho) of the cached 1/f_e(j), j < inv_n
     int inv_n;
     GridKCache kc;                       // k of the last (f_e,min, f_e,max, rho)
-    double rinv[MU];                     // RD(1 / R_m): lower-bound upload term
+    double rinv[kMaxM];                  // RD(1 / R_m): lower-bound upload term
     double lb[64];                       // per n~: lower bound of every configuration's energy
 };
 
 // Ranks under the key (gamma desc, T asc, index asc) (R2), then order[] and the
 // suffix-min deadlines L_i = min_{i' >= i} T_order[i'] (Eq. fth's min, R1).
-template <class SM>
-__device__ __forceinline__ void sort_users(int M, double gam, double T, SM &s, int lane) {
+__device__ __forceinline__ void sort_users(int M, double gam, double T, SolveSmem &s, int lane) {
     int r = 0;
     for (int t = 0; t < M; t++) {
         const double gt = __shfl_sync(0xffffffffu, gam, t);
@@ -97,8 +97,7 @@ __device__ __forceinline__ void sort_users(int M, double gam, double T, SM &s, i
 
 // Homogeneous users (equal gamma): ranks under the key (T asc, index asc) from the deadlines in
 // shared memory (broadcast reads, no shuffles), then order[] and the suffix minima (= sorted T).
-template <class SM>
-__device__ __noinline__ void sort_users_T(int M, double T, SM &s, int lane) {
+__device__ __noinline__ void sort_users_T(int M, double T, SolveSmem &s, int lane) {
     int r = 0;
     for (int t = 0; t < M; t++) {
         const double Tt = s.T[t];
@@ -112,26 +111,25 @@ __device__ __noinline__ void sort_users_T(int M, double T, SM &s, int lane) {
     __syncwarp();
 }
 
-// Alg. 1 lines 4-6 for partition point nt.  Returns i^ (M if none).  x: the lane's user.
-template <bool UNI>
+// Alg. 1 lines 4-6 for partition point nt.  Returns i^ (M if none).
 __device__ __forceinline__ int setup_nt(const DevModel &md, int nt, int M, bool homog, bool uni, double t_free,
-                                        const InstRegs &x, SolveSmem<UNI> &s, int lane) {
+                                        SolveSmem &s, int lane) {
     const double v_nt = md.v[nt], u_nt = md.u[nt], O_nt = md.O[nt];
     double gam = 0.0;
     if (lane < M) {
-        const double OR = O_nt / x.R;  // Eq. (3)
-        const double zv = x.z * v_nt;
-        gam = OR + div_z(zv, x.f1);   // gamma
-        if (!uni || lane == 0) {       // uniform users: one copy serves every member
+        const double OR = O_nt / s.R[lane];  // Eq. (3)
+        const double zv = s.z[lane] * v_nt;
+        gam = OR + div_z(zv, s.f1[lane]);   // gamma
+        if (!uni || lane == 0) {             // uniform users: one copy serves every member
             s.orzv[lane] = make_double2(OR, zv);
-            s.kuup[lane] = make_double2(x.k * u_nt, OR * x.p);  // Eq. (4)
+            s.kuup[lane] = make_double2(s.kap[lane] * u_nt, OR * s.pu[lane]);  // Eq. (4)
         }
-        if (!UNI) s.gam[lane] = gam;
+        s.gam[lane] = gam;
     }
-    if (!UNI && !homog) sort_users(M, gam, s.T[lane], s, lane);  // homogeneous: order fixed per instance
+    if (!homog) sort_users(M, gam, s.T[lane], s, lane);  // homogeneous: order fixed per instance
     double th = 0.0;
     if (lane < M) {
-        const double gi = (UNI || homog) ? gam : s.gam[s.order[lane]];
+        const double gi = homog ? gam : s.gam[s.order[lane]];
         const double phi = md.phi[nt * md.B1 + (M - lane)], psi = md.psi[nt * md.B1 + (M - lane)];
         const double L = s.Lg[lane].x;
         th = phi / (L - gi);                          // Eq. (fth)
@@ -205,7 +203,7 @@ __device__ __forceinline__ void write_local(const DevResult &r, long long i, lon
 template <bool COUNTS, bool PRUNE, bool UNI>
 __device__ __forceinline__ void solve_instance(long long i, long long off, long long M64, int mid,
                                                const DevModel *models, const DevBatch &b, const DevResult &r,
-                                               int mode, SolveSmem<UNI> &s, int lane) {
+                                               int mode, SolveSmem &s, int lane) {
     __syncwarp();
     long long k;
     int M;
@@ -230,11 +228,12 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
         floc = (__fma_rn(x.f0, x.T, -zvN) > 0.0) ? x.f0 : clampf(zvN / x.T, x.f0, x.f1);
         eloc = ((x.k * uN) * floc) * floc;
         s.et[lane].x = eloc;
-        if (!UNI || lane == 0) {
-            s.fmm[lane] = make_double2(x.f0, x.f1);
-            s.kap[lane] = x.k;
-            s.pu[lane] = x.p;
-        }
+        s.fmm[lane] = make_double2(x.f0, x.f1);
+        s.R[lane] = x.R;
+        s.z[lane] = x.z;
+        s.f1[lane] = x.f1;
+        s.kap[lane] = x.k;
+        s.pu[lane] = x.p;
     }
     s.T[lane] = x.T;  // +inf beyond M
     __syncwarp();
@@ -259,13 +258,10 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
         __syncwarp();
     }
     // instance-level flags (warp-uniform)
-    // user 0's values (lane 0's registers)
-    const double R0 = __shfl_sync(0xffffffffu, x.R, 0), z0 = __shfl_sync(0xffffffffu, x.z, 0),
-                 f10 = __shfl_sync(0xffffffffu, x.f1, 0);
+    const double R0 = s.R[0], z0 = s.z[0], f10 = s.f1[0];  // user 0's values
     auto sb = [](double a, double c) { return __double_as_longlong(a) == __double_as_longlong(c); };
     const bool homog_ = __all_sync(0xffffffffu, lane >= M || (sb(x.R, R0) && sb(x.z, z0) && sb(x.f1, f10)));
-    const double f00 = __shfl_sync(0xffffffffu, x.f0, 0), k0 = __shfl_sync(0xffffffffu, x.k, 0),
-                 p0 = __shfl_sync(0xffffffffu, x.p, 0);
+    const double f00 = s.fmm[0].x, k0 = s.kap[0], p0 = s.pu[0];
     const bool uni_ = homog_ && __all_sync(0xffffffffu, lane >= M || (sb(x.f0, f00) && sb(x.k, k0) && sb(x.p, p0)));
     if (UNI && !uni_) {  // left to the general kernel
         if (lane == 0) r.status[i] = kStDefer;
@@ -305,7 +301,7 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                 s.lb[nt] = S;
             }
         } else {
-            if (!UNI && lane < M) s.rinv[lane] = recip_rd(x.R);
+            if (lane < M) s.rinv[lane] = recip_rd(x.R);
             __syncwarp();
             for (int nt = lane; nt < N; nt += 32) {
                 const double u_nt = md.u[nt], O_nt = md.O[nt];
@@ -340,14 +336,14 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
         aN = N;  // first all-local evaluation key (R8); n~ = N at j = 0 by default (R4)
         aJ = 0;
 
-#ifndef JDOB_ASCENDING_PRUNE
+#if JDOB_PRUNE_ORDER == 2
         unsigned long long done = 0ull;  // n~ swept in this pass (best-first order)
 #endif
         for (int nt = -1;;) {
             if (!prune) {
                 if (++nt >= N || (mode == JDOB_MODE_BINARY && nt != 0)) break;
             } else {
-#ifndef JDOB_ASCENDING_PRUNE
+#if JDOB_PRUNE_ORDER == 2
                 // best first: the unswept n~ with the smallest lower bound (ties: smallest n~) among those
                 // whose bound is <= min(best so far, E_LC).  A configuration at a skipped n~ has E >= lb >
                 // the best (it cannot win) or > E_LC (LC beats it); bounds equal to the best are swept, so
@@ -366,11 +362,19 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                 nt = __ffsll((long long)hit) - 1;
                 done |= 1ull << nt;
 #else
-                // next n~ whose lower bound is below the best so far (every configuration at a skipped
-                // n~ has E >= lb >= bEw, so none of them can win)
+                // next n~ (ascending) whose lower bound is below the best so far (every configuration at
+                // a skipped n~ has E >= lb >= bEw, so none of them can win; an equal E at a later n~
+                // loses the (E, n~, j) tie-break).  JDOB_PRUNE_ORDER 1 also caps the bound at E_LC: a
+                // configuration with E > E_LC loses to LC.
+#if JDOB_PRUNE_ORDER == 1
+                unsigned long long cand = __ballot_sync(0xffffffffu, lane < N && s.lb[lane] < bEw && s.lb[lane] <= E_lc);
+                if (N > 32) cand |= (unsigned long long)__ballot_sync(0xffffffffu, lane + 32 < N && s.lb[lane + 32] < bEw &&
+                                                                                s.lb[lane + 32] <= E_lc) << 32;
+#else
                 unsigned long long cand = __ballot_sync(0xffffffffu, lane < N && s.lb[lane] < bEw);
                 if (N > 32) cand |= (unsigned long long)__ballot_sync(0xffffffffu, lane + 32 < N &&
                                                                                 s.lb[lane + 32] < bEw) << 32;
+#endif
                 cand &= ~0ull << (nt + 1);
                 if (cand == 0ull) {
                     pruned |= nt + 1 < N;
@@ -383,7 +387,7 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
             }
             if (COUNTS) c_setup += 1;
             last_nt = nt;
-            const int ihat = setup_nt<UNI>(md, nt, M, homog, uni, t_free, x, s, lane);
+            const int ihat = setup_nt(md, nt, M, homog, uni, t_free, s, lane);
             // two grid points per lane (j0 + lane and j0 + 32 + lane): the two energy chains are
             // independent, which doubles the instruction-level parallelism of the sweep and lets both
             // share each user's shared-memory loads
@@ -455,7 +459,7 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                         EA = EA + ((!(feA < et.y)) ? emA : et.x);
                         EB = EB + ((!(feB < et.y)) ? emB : et.x);
                     }
-                } else if (!UNI) {
+                } else {
                     const long long fbA = __double_as_longlong(feA), fbB = __double_as_longlong(feB);
 #pragma unroll 2
                     for (int m = 0; m < M; m++) {
@@ -559,7 +563,7 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     // so the winner's are formed directly (same expressions as setup_nt) instead of a new set-up
     const bool win_direct = homog;
 #endif
-    if (!win_direct && bN != last_nt) setup_nt<UNI>(md, bN, M, homog, uni, t_free, x, s, lane);
+    if (!win_direct && bN != last_nt) setup_nt(md, bN, M, homog, uni, t_free, s, lane);
     const int Bo = M - bP;
     const double lo_ = s.Lg[bP].x;
     const double fe = grid_fe(fe_max, rho, bJ);
@@ -568,9 +572,9 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     const bool member = (lane < M) && (s.rank[lane] >= bP);
     double f = floc, arr = t_free;
     if (member) {
-        const double2 a = win_direct ? make_double2(md.O[bN] / x.R, x.z * md.v[bN])
+        const double2 a = win_direct ? make_double2(md.O[bN] / s.R[lane], s.z[lane] * md.v[bN])
                                      : s.orzv[uni ? 0 : lane];  // (O/R, zv)
-        const double2 t = make_double2(x.f0, x.f1);             // (f_min, f_max)
+        const double2 t = s.fmm[lane];                          // (f_min, f_max)
         const double budget = (lo_ - a.x) - te;
         const bool low = (a.y == 0.0) || (__fma_rn(t.x, budget, -a.y) > 0.0);
         f = low ? t.x : clampf(a.y / budget, t.x, t.y);
@@ -604,9 +608,9 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
 template <bool COUNTS, bool PRUNE, bool UNI>
 __global__ void __launch_bounds__(kSolveWarps * 32, UNI ? JDOB_SOLVE_MINB_U : JDOB_SOLVE_MINB)
     k_solve(const DevModel *models, DevBatch b, DevResult r, int mode) {
-    __shared__ SolveSmem<UNI> smem[kSolveWarps];
+    __shared__ SolveSmem smem[kSolveWarps];
     const int lane = threadIdx.x & 31;
-    SolveSmem<UNI> &s = smem[threadIdx.x >> 5];
+    SolveSmem &s = smem[threadIdx.x >> 5];
     if (lane == 0) {
         s.inv_key = make_double2(0.0, 0.0);  // rho > 0 in every valid instance: no false hit
         s.inv_n = 0;
