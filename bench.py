@@ -48,7 +48,7 @@ PEAK_NOTE = ("builder-measured FP64 peak: 148 SMs x 64 FP64 lanes/clk (tools/fp6
 WORKLOADS = {
     "c2": ("c2_vgg16_m10_identical_beta0-35", 1 << 20),
     "c3": ("c3_resnet18_m4-20_mixed_deadlines", 100_000),
-    "c5": ("c5_montecarlo_m1-32_3models_5regimes_3grids", 1_000_000),
+    "c5": ("c5_montecarlo_m1-32_3models_5regimes_3grids", 10_000_000),
 }
 
 
@@ -59,12 +59,17 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="mine", choices=["mine", "reference"])
     p.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
-    p.add_argument("--n-inst", type=int, default=None, help="instances per GPU")
+    p.add_argument("--n-inst", type=int, default=None,
+                   help="instances per GPU (weak scaling) or in total (--scaling strong)")
+    p.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                   help="weak: n instances per GPU; strong: a fixed total sharded over the GPUs")
     p.add_argument("--no-bf", action="store_true")
     p.add_argument("--bf-reps", type=int, default=2)
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
+    p.add_argument("--host-gen", action="store_true",
+                   help="c5: generate on the host and copy (default: generated on the device, no input H2D)")
     return p.parse_args()
 
 
@@ -134,7 +139,7 @@ def fp64_work(batch, counts, setups=None, lower_bound=False):
     sweep): set-ups and pairs from the executed-work counters plus the n~ lower bounds (8 ops per
     (n~, user), one RD reciprocal per user).  Returns (divisions, other ops, member evaluations)."""
     M = np.diff(batch.user_off).astype(np.float64)
-    N = np.array([batch.models[m].N for m in batch.model_id], np.float64)
+    N = np.array([m.N for m in batch.models], np.float64)[np.asarray(batch.model_id)]
     visit, ev, mem = (counts[:, 0].astype(np.float64), counts[:, 1].astype(np.float64),
                       counts[:, 2].astype(np.float64))
     S = N if setups is None else setups.astype(np.float64)
@@ -190,6 +195,24 @@ def ncu_traffic(kernel):
         return d.get(kernel)
     except Exception:
         return None
+
+
+class DevGenView:
+    """Host-side view of a device-generated C5 shard (jdob_generate_c5_*): sizes and per-instance
+    (M, model) for the work counters; subset() regenerates instances with the host generator (the same
+    bits, tests/test_gpu_gen.py) for the cpu_baseline sample."""
+
+    def __init__(self, db, models, lo, meta):
+        self.user_off = db.t["user_off"].cpu().numpy()
+        self.model_id = db.t["model_id"].cpu().numpy()
+        self.models, self.lo, self.meta = models, lo, meta
+        self.n_inst, self.n_users = db.n_inst, db.n_users
+
+    def nbytes(self):
+        return self.n_inst * (4 + 8 + 4 * 8 + 4) + 8 + self.n_users * 7 * 8
+
+    def subset(self, i0, i1):
+        return G.config_c5(n_inst=i1 - i0, inst_begin=self.lo + i0)
 
 
 def cpu_baseline(batch, seconds, label, gpu_host=None):
@@ -368,10 +391,20 @@ def run_mine(args):
         dist = D
     import paper_2504_14611_b200 as J
     label, n_default = WORKLOADS[args.workload]
-    n = args.n_inst or n_default
-    batch = G.config_batch(args.workload, n_inst=n, inst_begin=rank * n)
+    from paper_2504_14611_b200.dist import fold_stats, shard_range
+    n_arg = args.n_inst or n_default
+    n_total = n_arg * world if args.scaling == "weak" else n_arg
+    lo, hi = shard_range(n_total, world, rank)   # weak: [rank n, (rank + 1) n)
+    n = hi - lo
+    devgen = args.workload == "c5" and not args.host_gen
+    if devgen:   # each rank generates its own instances on the device: no input traffic
+        models, params = G.c5_device_inputs(inst_begin=lo)
+        db = J.DeviceBatch.generate_c5(models, params, n)
+        batch = DevGenView(db, models, lo, dict(config="c5", n_buckets=15))
+    else:
+        batch = G.config_batch(args.workload, n_inst=n, inst_begin=lo)
+        db = J.DeviceBatch(batch)
     n_buckets = int(batch.meta.get("n_buckets", 32))
-    db = J.DeviceBatch(batch)
     torch.cuda.synchronize()
 
     # untimed: algorithmic work counters -- literal Alg. 2 counts (checked against the oracle in tests)
@@ -381,25 +414,26 @@ def run_mine(args):
     lit_div, lit_oth, n_member = fp64_work(batch, counts)
     wk = J.solve_batch(db, work=True, f_user=False)["work"].cpu().numpy()
     ex_div, ex_oth, n_member_exec = fp64_work(batch, wk[:, 1:], setups=wk[:, 0], lower_bound=True)
-    setup_frac = float(wk[:, 0].sum()) / float(sum(batch.models[m].N for m in batch.model_id))
+    setup_frac = float(wk[:, 0].sum()) / float(np.array([m.N for m in batch.models])[np.asarray(batch.model_id)].sum())
     del res_c
 
     res = J.solve_batch(db, f_user=False)
-    res["stats"] = J.stats(db, res, n_buckets=n_buckets)
+    # this rank's root of the statistics tree over the whole job's batch (jdob_stats_part); the
+    # pairwise fold over ranks (dist.fold_stats) has the bits of one GPU over the whole batch
+    part = (n_total, world, rank)
+    res["stats"] = J.stats(db, res, n_buckets=n_buckets, part=part)
     # the product path's decisions for the whole batch, on the host: the cpu_baseline leg compares
     # its oracle sample with them (the only place the bench run meets the oracle)
     gpu_host = {f: res[f].cpu().numpy() for f in ("E", "t_free_next", "f_e", "n_tilde", "j", "status", "mask")}
     ev = J.eval_plans(db, plans=res, f_user=False)
     stream = torch.cuda.current_stream()
 
-    from paper_2504_14611_b200.dist import allreduce_stats
-
     def step():
         J.solve_batch(db, f_user=False, out=res)
-        J.stats(db, res, out=res["stats"])
+        J.stats(db, res, out=res["stats"], part=part)
         J.eval_plans(db, plans=res, f_user=False, out=ev)
         if dist:
-            res["stats_global"] = allreduce_stats(res["stats"], dist)
+            res["stats_global"] = fold_stats(res["stats"], dist)
 
     for _ in range(args.warmup):
         step()
@@ -419,10 +453,10 @@ def run_mine(args):
         ev_s[i].record(stream)
         J.solve_batch(db, f_user=False, out=res)           # K0 + K1 (K0: one tiny block per model)
         ev_e[i].record(stream)
-        J.stats(db, res, out=res["stats"])                 # K4
+        J.stats(db, res, out=res["stats"], part=part)      # K4
         J.eval_plans(db, plans=res, f_user=False, out=ev)  # K3
         if dist:
-            res["stats_global"] = allreduce_stats(res["stats"], dist)
+            res["stats_global"] = fold_stats(res["stats"], dist)
     t_e.record(stream)
     torch.cuda.synchronize()
     if dist:
@@ -439,11 +473,13 @@ def run_mine(args):
         w = torch.tensor([ex_div, ex_oth, lit_div, lit_oth], device="cuda", dtype=torch.float64)
         dist.all_reduce(w, op=dist.ReduceOp.MAX)   # per-GPU work of the slowest rank's kind
         ex_div, ex_oth, lit_div, lit_oth = (float(x) for x in w)
-    value = world * n * K / (total_ms / 1e3)
+    value = n_total * K / (total_ms / 1e3)
 
     # end-to-end through the public host-buffer API (copies inside the timed region)
     e2e = None
-    if not args.no_e2e:
+    if devgen:
+        e2e = {"skipped": "device-generated workload: no host inputs (use --host-gen for the host-buffer API)"}
+    elif not args.no_e2e:
         hb = J.HostBuffers(batch, stats=True, n_buckets=n_buckets)
         J.solve_batch_host(hb)
         reps = max(1, min(K, 3))
@@ -461,7 +497,7 @@ def run_mine(args):
             t = torch.tensor([ms], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
-        e2e = {"value": world * n * reps / (ms / 1e3), "unit": "instances/s", "h2d_bytes_per_step": int(h2d),
+        e2e = {"value": n_total * reps / (ms / 1e3), "unit": "instances/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "api": "jdob_solve_batch_host (pinned host buffers)", "reps": reps}
         del hb
         # copy roof: one plain pinned host -> device copy of the same number of bytes (no kernels)
@@ -524,11 +560,12 @@ def run_mine(args):
             "warmup": args.warmup,
             "ms_per_step": total_ms / K,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": args.scaling,
             "vs_baseline": None,
             "dtype": "f64",
-            "data": "synthetic (jdobgen seeded generator, paper-shaped profiles; DESIGN.md §Input recipe)",
-            "config": {"workload": label, "n_inst_per_gpu": n, "global_instances": world * n,
+            "data": ("synthetic, generated on the device (jdob_generate_c5_*, bit-identical to jdobgen)" if devgen
+                     else "synthetic (jdobgen seeded generator, paper-shaped profiles; DESIGN.md §Input recipe)"),
+            "config": {"workload": label, "n_inst_per_gpu": n, "global_instances": n_total,
                        "users_per_gpu": int(batch.n_users), "input_bytes_per_gpu": int(batch.nbytes()),
                        "l2": "inputs larger than L2 (126 MB)" if batch.nbytes() > 126e6 else "inputs fit in L2",
                        "step": "jdob_solve_batch (K0+K1) + jdob_stats (K4) + jdob_eval of every plan (K3)"

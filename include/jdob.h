@@ -139,7 +139,7 @@ typedef struct {
  *                          plans (f_e* > 0: some user offloads, R18; valid for any M),
  *                          [8] #status != OK, [9+n] #instances with n~* = n (n <= 63);
  *                          r = 100 (E_lc - E) / E_lc.  Deterministic for a given
- *                          n_inst (fixed reduction tree).  Default buckets (bucket == NULL):
+ *                          n_inst (fixed reduction tree, see jdob_stats_part).  Default buckets (bucket == NULL):
  *                          bucket M_i - 1; instances with M_i > n_buckets are not counted.
  */
 typedef struct {
@@ -197,6 +197,20 @@ JDOB_API int jdob_solve_batch(const jdob_model *models, int32_t n_models, const 
  * Errors: JDOB_EINVAL (NULL arrays, n_buckets out of range, small workspace), JDOB_ECUDA.
  */
 JDOB_API int jdob_stats(const jdob_batch *b, const jdob_result *res, void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * The statistics of one part of a larger batch, for a multi-GPU fold with the same bits as one call
+ * over the whole batch.  The fixed reduction tree of jdob_stats is defined on the
+ * whole batch of n_total instances: 1024 leaves, leaf w = instances [n_total w / 1024,
+ * n_total (w + 1) / 1024), folded pairwise (a dyadic tree; fields 0-2 and 5-9+ add, 3 max, 4 min).
+ * `b` must hold exactly the instances [n_total part / parts, n_total (part + 1) / parts) with parts a
+ * power of two <= 1024; the call writes the root of that part's subtree to res->stats.  Folding the
+ * parts' roots pairwise in part order (paper_2504_14611_b200.dist.fold_stats) gives the same bits as
+ * jdob_stats over the whole batch.  jdob_stats(b, ...) is jdob_stats_part(b, ..., b->n_inst, 1, 0, ...).
+ * Errors: as jdob_stats, plus JDOB_EINVAL when (n_total, parts, part) does not describe `b`.
+ */
+JDOB_API int jdob_stats_part(const jdob_batch *b, const jdob_result *res, int64_t n_total, int32_t parts,
+                             int32_t part, void *ws, size_t ws_bytes, void *stream);
 
 /*
  * Same computation from HOST buffers (the end-to-end public call): copies the
@@ -321,6 +335,47 @@ JDOB_API size_t jdob_grouped_workspace_bytes(const jdob_model *models, int32_t n
  */
 JDOB_API int jdob_solve_grouped(const jdob_model *models, int32_t n_models, const jdob_batch *b, int32_t mode,
                                 const jdob_grouped_result *out, void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * The C5 Monte Carlo workload generated on the device, so that a rank
+ * solves instances it made itself with no input traffic.  INPUT PLUMBING, not the
+ * method: the device twin of the host generator jdobgen.config_c5, bit-identical to
+ * it (counter-based SplitMix64 draws keyed by (seed, instance id, user, field); per instance M ~
+ * U{1..32}, model ~ U{0,1,2}, deadline regime ~ U{0..4}, rho from rho[3]; per user beta = 2.13 or
+ * 30.25 (regimes 0, 1) or ~ U[4.5, 5.5], U[2, 8], U[0, 10] (regimes 2-4) and T = (1 + beta) lat[model]
+ * (P:361); Table I users, optionally R and kappa scaled by U[0.5, 2]).  The host supplies the recipe's
+ * constants so both generators use the same doubles.
+ */
+typedef struct {
+    uint64_t seed;
+    int64_t inst_begin;      /* global id of the first instance (shards generate their own range) */
+    int32_t hetero;          /* 1: R and kappa scaled by U[0.5, 2] per user                       */
+    double zeta, kappa, f_min, f_max, R, p_u;  /* Table I users                                    */
+    double fe_min, fe_max;   /* edge frequency box                                                  */
+    double rho[3];           /* the three sweep steps                                              */
+    double lat[3];           /* per model: zeta v_N / f_max, the beta denominator of P:361         */
+} jdob_gen_params;
+
+/* Device workspace bytes of the two generator calls for n_inst instances (kept between them). */
+JDOB_API size_t jdob_generate_workspace_bytes(int64_t n_inst);
+
+/*
+ * Generator phase 1: writes b->model_id, user_off [n_inst + 1], t_free, fe_min, fe_max, rho and
+ * bucket (model * 5 + regime) of instances [p->inst_begin, p->inst_begin + b->n_inst) (DEVICE arrays
+ * of `b`, caller-allocated), and the total user count user_off[n_inst] to the HOST *n_users (one
+ * synchronous 8-byte read on `stream`), so the caller can size the user arrays.
+ * Errors: JDOB_EINVAL (NULL arrays or n_users, small workspace), JDOB_ECUDA.
+ */
+JDOB_API int jdob_generate_c5_instances(const jdob_gen_params *p, const jdob_batch *b, int64_t *n_users, void *ws,
+                                        size_t ws_bytes, void *stream);
+
+/*
+ * Generator phase 2: writes the user arrays zeta, kappa, f_min, f_max, R, p_u, T [n_users] of `b`
+ * (DEVICE, caller-allocated), reading the model_id and user_off phase 1 wrote and its workspace.
+ * Asynchronous.  Errors: JDOB_EINVAL (NULL arrays, small workspace), JDOB_ECUDA.
+ */
+JDOB_API int jdob_generate_c5_users(const jdob_gen_params *p, const jdob_batch *b, void *ws, size_t ws_bytes,
+                                    void *stream);
 
 /* Message of the last call-level error on this thread ("" if none). */
 JDOB_API const char *jdob_last_error(void);

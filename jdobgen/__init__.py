@@ -361,6 +361,19 @@ def config_c5(n_inst: int = 10_000_000, seed: int = 5, inst_begin: int = 0, hete
                              inst_base=inst_begin, meta=dict(config="c5", seed=seed, n_buckets=15))
 
 
+def c5_device_inputs(seed: int = 5, inst_begin: int = 0, hetero: bool = False):
+    """(models, params) for the device twin of config_c5 (include/jdob.h jdob_gen_params): the recipe's
+    constants as the doubles config_c5 uses -- Table I users and, per model, the beta denominator
+    zeta v_N / f_max of the homogeneous users (min_local_latency on one user)."""
+    models = [profiles.mobilenetv2(), profiles.vgg16(), profiles.resnet18()]
+    zeta, kappa = profiles.ZETA, profiles.KAPPA
+    lat = [float(min_local_latency(m, np.array([zeta]), np.array([TABLE_I["f_max"]]))[0]) for m in models]
+    params = dict(seed=seed, inst_begin=inst_begin, hetero=int(hetero), zeta=zeta, kappa=kappa,
+                  f_min=TABLE_I["f_min"], f_max=TABLE_I["f_max"], R=R_TABLE_I, p_u=TABLE_I["p_u"],
+                  fe_min=TABLE_I["fe_min"], fe_max=TABLE_I["fe_max"], rho=list(C5_RHOS), lat=lat)
+    return models, params
+
+
 def random_batch(seed: int, n_inst: int, M_lo: int = 1, M_hi: int = 8, N_lo: int = 1, N_hi: int = 6,
                  tfree_frac: float = 0.3, k_max: int = 40, B_extra: int = 2, identical_T_frac: float = 0.3,
                  equal_gamma_frac: float = 0.3) -> Batch:

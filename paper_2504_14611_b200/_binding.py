@@ -43,6 +43,12 @@ class JResult(C.Structure):
                                                                            ("work", C.c_void_p)]
 
 
+class JGenParams(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("inst_begin", C.c_int64), ("hetero", C.c_int32)] + \
+               [(f, C.c_double) for f in ("zeta", "kappa", "f_min", "f_max", "R", "p_u", "fe_min", "fe_max")] + \
+               [("rho", C.c_double * 3), ("lat", C.c_double * 3)]
+
+
 class JGrouped(C.Structure):
     _fields_ = [(f, C.c_void_p) for f in ("E", "t_free_next", "n_groups", "status", "group_of", "partition", "f_user",
                                           "group_fe")]
@@ -75,6 +81,8 @@ def lib():
                                           C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
                                           C.c_void_p]
             L.jdob_stats.argtypes = [_P(JBatch), _P(JResult), C.c_void_p, C.c_size_t, C.c_void_p]
+            L.jdob_stats_part.argtypes = [_P(JBatch), _P(JResult), C.c_int64, C.c_int32, C.c_int32, C.c_void_p,
+                                          C.c_size_t, C.c_void_p]
             L.jdob_bf_space_size.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int64]
             L.jdob_bf_space_size.restype = C.c_uint64
             L.jdob_eval.argtypes = [_P(JModel), C.c_int32, _P(JBatch), C.c_void_p, C.c_void_p, C.c_void_p,
@@ -84,6 +92,11 @@ def lib():
             L.jdob_grouped_workspace_bytes.restype = C.c_size_t
             L.jdob_solve_grouped.argtypes = [_P(JModel), C.c_int32, _P(JBatch), C.c_int32, _P(JGrouped), C.c_void_p,
                                              C.c_size_t, C.c_void_p]
+            L.jdob_generate_workspace_bytes.argtypes = [C.c_int64]
+            L.jdob_generate_workspace_bytes.restype = C.c_size_t
+            L.jdob_generate_c5_instances.argtypes = [_P(JGenParams), _P(JBatch), _P(C.c_int64), C.c_void_p,
+                                                     C.c_size_t, C.c_void_p]
+            L.jdob_generate_c5_users.argtypes = [_P(JGenParams), _P(JBatch), C.c_void_p, C.c_size_t, C.c_void_p]
             L.jdob_last_error.restype = C.c_char_p
             L.jdob_version.restype = C.c_char_p
             L.jdob_release_pool.restype = C.c_int
@@ -93,7 +106,8 @@ def lib():
 
 EXPORTED = ("jdob_workspace_bytes", "jdob_solve_batch", "jdob_solve_batch_host", "jdob_bruteforce",
             "jdob_bf_space_size", "jdob_eval", "jdob_grouped_workspace_bytes", "jdob_solve_grouped",
-            "jdob_last_error", "jdob_version", "jdob_release_pool", "jdob_stats")
+            "jdob_last_error", "jdob_version", "jdob_release_pool", "jdob_stats", "jdob_stats_part",
+            "jdob_generate_workspace_bytes", "jdob_generate_c5_instances", "jdob_generate_c5_users")
 
 
 def _check(rc):
@@ -139,15 +153,7 @@ class DeviceBatch:
             t = torch.from_numpy(np.ascontiguousarray(a)).to(dtype)
             return t.to(dev, non_blocking=non_blocking)
 
-        self.model_tensors = []
-        ms = []
-        for m in batch.models:
-            mt = {f: up(np.asarray(getattr(m, f), np.float64), torch.float64) for f in ("A", "O", "g", "q", "d", "c")}
-            self.model_tensors.append(mt)
-            ms.append(JModel(int(m.N), int(m.B_max), *[mt[f].data_ptr() for f in ("A", "O", "g", "q", "d", "c")]))
-        self.Ns = [int(m.N) for m in batch.models]
-        self.n_models = len(ms)
-        self.jmodels = (JModel * len(ms))(*ms)
+        self._set_models(batch.models, up)
         self.n_inst = int(len(batch.model_id))
         self.user_off_host = np.ascontiguousarray(batch.user_off, np.int64)
         self.n_users = int(self.user_off_host[-1])
@@ -161,6 +167,62 @@ class DeviceBatch:
                                                            ("model_id", "user_off") + self.USER + self.INST +
                                                            ("bucket",)])
         self._ws = {}
+
+    def _set_models(self, models, up):
+        torch = _torch()
+        self.model_tensors = []
+        ms = []
+        for m in models:
+            mt = {f: up(np.asarray(getattr(m, f), np.float64), torch.float64) for f in ("A", "O", "g", "q", "d", "c")}
+            self.model_tensors.append(mt)
+            ms.append(JModel(int(m.N), int(m.B_max), *[mt[f].data_ptr() for f in ("A", "O", "g", "q", "d", "c")]))
+        self.Ns = [int(m.N) for m in models]
+        self.n_models = len(ms)
+        self.jmodels = (JModel * len(ms))(*ms)
+
+    @classmethod
+    def generate_c5(cls, models, params: dict, n_inst: int, device=None, n_buckets: int = 15, stream=None):
+        """The C5 workload generated on the device (jdob_generate_c5_*; input plumbing, bit-identical
+        to jdobgen.config_c5): `models` and `params` (the jdob_gen_params fields) come from the caller,
+        e.g. jdobgen.c5_device_inputs.  No host->device traffic but the model tables."""
+        torch = _torch()
+        self = cls.__new__(cls)
+        self.device = torch.device(device if device is not None else "cuda")
+        dev = self.device
+
+        def up(a, dtype):
+            return torch.from_numpy(np.ascontiguousarray(a)).to(dtype).to(dev)
+
+        self._set_models(models, up)
+        n = int(n_inst)
+        self.n_inst = n
+        gp = JGenParams(int(params["seed"]), int(params.get("inst_begin", 0)), int(params.get("hetero", 0)),
+                        *[float(params[f]) for f in ("zeta", "kappa", "f_min", "f_max", "R", "p_u", "fe_min",
+                                                      "fe_max")],
+                        (C.c_double * 3)(*params["rho"]), (C.c_double * 3)(*params["lat"]))
+        self.t = {"model_id": torch.empty(n, dtype=torch.int32, device=dev),
+                  "user_off": torch.empty(n + 1, dtype=torch.int64, device=dev),
+                  "bucket": torch.empty(n, dtype=torch.int32, device=dev)}
+        for f in self.INST:
+            self.t[f] = torch.empty(n, dtype=torch.float64, device=dev)
+        for f in self.USER:
+            self.t[f] = None
+        ws = torch.empty(int(lib().jdob_generate_workspace_bytes(n)), dtype=torch.uint8, device=dev)
+        jb = JBatch(n, self.n_models, *[_ptr(self.t[f]) for f in ("model_id", "user_off") + self.USER + self.INST +
+                                        ("bucket",)])
+        nu = C.c_int64()
+        sh = _stream_handle(stream)
+        _check(lib().jdob_generate_c5_instances(C.byref(gp), C.byref(jb), C.byref(nu), ws.data_ptr(), ws.numel(), sh))
+        self.n_users = int(nu.value)
+        for f in self.USER:
+            self.t[f] = torch.empty(self.n_users, dtype=torch.float64, device=dev)
+        self.jbatch = JBatch(n, self.n_models, *[_ptr(self.t[f]) for f in
+                                                 ("model_id", "user_off") + self.USER + self.INST + ("bucket",)])
+        _check(lib().jdob_generate_c5_users(C.byref(gp), C.byref(self.jbatch), ws.data_ptr(), ws.numel(), sh))
+        self.user_off_host = None
+        self.n_buckets = n_buckets
+        self._ws = {}
+        return self
 
     def workspace(self, which: int):
         torch = _torch()
@@ -209,9 +271,12 @@ def solve_batch(db: DeviceBatch, mode: int = MODE_FULL, f_user: bool = True, cou
     return out
 
 
-def stats(db: DeviceBatch, res: dict, n_buckets: Optional[int] = None, stream=None, out=None):
+def stats(db: DeviceBatch, res: dict, n_buckets: Optional[int] = None, stream=None, out=None,
+          part: Optional[tuple] = None):
     """jdob_stats: the bucketed energy-saving statistics (a12) of solved instances `res` (the dict
-    solve_batch returned for `db`), as a call of its own; returns the [n_buckets, 80] f64 tensor."""
+    solve_batch returned for `db`), as a call of its own; returns the [n_buckets, 80] f64 tensor.
+    part = (n_total, parts, p): `db` is part p of `parts` of a batch of n_total instances
+    (jdob_stats_part); the result is that part's subtree root, folded by dist.fold_stats."""
     torch = _torch()
     if out is None:
         nb = n_buckets if n_buckets is not None else db.n_buckets
@@ -219,7 +284,12 @@ def stats(db: DeviceBatch, res: dict, n_buckets: Optional[int] = None, stream=No
     r = JResult(*[_ptr(res.get(f)) for f in ("E", "E_lc", "t_free_next", "f_e", "n_tilde", "j", "status", "mask")],
                 None, None, out.data_ptr(), int(out.shape[0]), None, None)
     ws = db.workspace(2)
-    _check(lib().jdob_stats(C.byref(db.jbatch), C.byref(r), ws.data_ptr(), ws.numel(), _stream_handle(stream)))
+    if part is None:
+        _check(lib().jdob_stats(C.byref(db.jbatch), C.byref(r), ws.data_ptr(), ws.numel(), _stream_handle(stream)))
+    else:
+        n_total, parts, p = part
+        _check(lib().jdob_stats_part(C.byref(db.jbatch), C.byref(r), int(n_total), int(parts), int(p),
+                                     ws.data_ptr(), ws.numel(), _stream_handle(stream)))
     return out
 
 

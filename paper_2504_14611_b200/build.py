@@ -14,7 +14,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libjdob.so")
 OBJ = os.path.join(HERE, "build")
-SOURCES = ["aggregates.cu", "solve.cu", "eval.cu", "stats.cu", "bruteforce.cu", "grouping.cu", "solve_large.cu", "api.cu"]
+SOURCES = ["aggregates.cu", "solve.cu", "eval.cu", "stats.cu", "bruteforce.cu", "grouping.cu", "solve_large.cu",
+           "gen.cu", "api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
                      "-Xcompiler", "-fvisibility=hidden"]

@@ -266,13 +266,18 @@ int jdob_solve_batch(const jdob_model *models, int32_t n_models, const jdob_batc
     if ((rc = cuda_check("solve"))) return rc;
     if (out->stats) {
         double *partials = (double *)((char *)ws + models_bytes(models, n_models));
-        launch_stats(db, dr, partials, out->stats, out->n_buckets, s);
+        launch_stats(db, dr, partials, out->stats, out->n_buckets, b->n_inst, 1, 0, s);
         if ((rc = cuda_check("stats"))) return rc;
     }
     return JDOB_OK;
 }
 
 int jdob_stats(const jdob_batch *b, const jdob_result *res, void *ws, size_t ws_bytes, void *stream) {
+    return jdob_stats_part(b, res, b ? b->n_inst : 0, 1, 0, ws, ws_bytes, stream);
+}
+
+int jdob_stats_part(const jdob_batch *b, const jdob_result *res, int64_t n_total, int32_t parts, int32_t part,
+                    void *ws, size_t ws_bytes, void *stream) {
     g_err.clear();
     if (!b || !res) return fail(JDOB_EINVAL, "stats: NULL batch or result");
     if (b->n_inst < 0) return fail(JDOB_EINVAL, "n_inst < 0");
@@ -296,8 +301,67 @@ int jdob_stats(const jdob_batch *b, const jdob_result *res, void *ws, size_t ws_
     dr.counts = nullptr;
     dr.partition = nullptr;
     dr.work = nullptr;
-    launch_stats(to_dev(b), dr, (double *)ws, res->stats, res->n_buckets, (cudaStream_t)stream);
+    if (!launch_stats(to_dev(b), dr, (double *)ws, res->stats, res->n_buckets, n_total, parts, part,
+                      (cudaStream_t)stream))
+        return fail(JDOB_EINVAL, "stats: the batch (%lld instances) is not part %d of %d of %lld instances (parts a "
+                    "power of two <= %d)", (long long)b->n_inst, part, parts, (long long)n_total, kStatsBlocks);
     return cuda_check("stats");
+}
+
+static GenParams gen_params(const jdob_gen_params *p) {
+    GenParams g;
+    g.seed = p->seed;
+    g.inst_begin = p->inst_begin;
+    g.hetero = p->hetero;
+    g.zeta = p->zeta;
+    g.kappa = p->kappa;
+    g.f_min = p->f_min;
+    g.f_max = p->f_max;
+    g.R = p->R;
+    g.p_u = p->p_u;
+    g.fe_min = p->fe_min;
+    g.fe_max = p->fe_max;
+    for (int i = 0; i < 3; i++) {
+        g.rho[i] = p->rho[i];
+        g.lat[i] = p->lat[i];
+    }
+    return g;
+}
+
+size_t jdob_generate_workspace_bytes(int64_t n_inst) { return n_inst < 0 ? 0 : gen_workspace_bytes(n_inst); }
+
+int jdob_generate_c5_instances(const jdob_gen_params *p, const jdob_batch *b, int64_t *n_users, void *ws,
+                               size_t ws_bytes, void *stream) {
+    g_err.clear();
+    if (!p || !b || !n_users) return fail(JDOB_EINVAL, "generate: NULL argument");
+    if (b->n_inst < 0) return fail(JDOB_EINVAL, "n_inst < 0");
+    if (b->n_inst > 0 && (!b->model_id || !b->user_off || !b->t_free || !b->fe_min || !b->fe_max || !b->rho ||
+                          !b->bucket))
+        return fail(JDOB_EINVAL, "generate: NULL instance array");
+    if (!ws || ws_bytes < gen_workspace_bytes(b->n_inst)) return fail(JDOB_EINVAL, "generate: small workspace");
+    cudaStream_t s = (cudaStream_t)stream;
+    *n_users = 0;
+    if (b->n_inst == 0) return JDOB_OK;
+    launch_gen_inst(gen_params(p), b->n_inst, (int *)b->model_id, (long long *)b->user_off, (double *)b->t_free,
+                    (double *)b->fe_min, (double *)b->fe_max, (double *)b->rho, (int *)b->bucket, ws, s);
+    long long nu = 0;
+    cudaMemcpyAsync(&nu, b->user_off + b->n_inst, sizeof(nu), cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_check("generate: read n_users");
+    *n_users = nu;
+    return cuda_check("generate instances");
+}
+
+int jdob_generate_c5_users(const jdob_gen_params *p, const jdob_batch *b, void *ws, size_t ws_bytes, void *stream) {
+    g_err.clear();
+    if (!p || !b) return fail(JDOB_EINVAL, "generate: NULL argument");
+    if (b->n_inst > 0 && (!b->model_id || !b->user_off || !b->zeta || !b->kappa || !b->f_min || !b->f_max ||
+                          !b->R || !b->p_u || !b->T))
+        return fail(JDOB_EINVAL, "generate: NULL user array");
+    if (!ws || ws_bytes < gen_workspace_bytes(b->n_inst)) return fail(JDOB_EINVAL, "generate: small workspace");
+    launch_gen_users(gen_params(p), b->n_inst, b->model_id, (const long long *)b->user_off, (double *)b->zeta,
+                     (double *)b->kappa, (double *)b->f_min, (double *)b->f_max, (double *)b->R, (double *)b->p_u,
+                     (double *)b->T, ws, (cudaStream_t)stream);
+    return cuda_check("generate users");
 }
 
 static size_t og_work_bytes(int64_t n, int64_t nu) {
@@ -651,7 +715,7 @@ int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob
         r2.counts = (long long *)dr.counts;
         r2.partition = dr.partition;
         double *partials = (double *)((char *)ws[0] + models_bytes(models, n_models));
-        launch_stats(to_dev(&db), r2, partials, dr.stats, out->n_buckets, s);
+        launch_stats(to_dev(&db), r2, partials, dr.stats, out->n_buckets, n, 1, 0, s);
         cudaMemcpyAsync(out->stats, dr.stats, (size_t)out->n_buckets * JDOB_STATS_FIELDS * 8,
                         cudaMemcpyDeviceToHost, s);
         d2h += (long long)out->n_buckets * JDOB_STATS_FIELDS * 8;

@@ -17,7 +17,7 @@ struct ModelChunk {
 
 // Launch geometry of the solve kernel (one warp per instance, persistent grid).
 constexpr int kSolveWarps = 4;
-constexpr int kStatsBlocks = 1184;   // fixed => deterministic statistics tree
+constexpr int kStatsBlocks = 1024;   // leaves of the fixed dyadic statistics tree (power of two)
 constexpr int kBfBlocks = 148 * 8;   // persistent brute-force grid
 constexpr int kBfWarps = 4;
 
@@ -52,11 +52,29 @@ void launch_solve(const DevModel *models, const DevBatch &b, const DevResult &r,
                   int num_sms);
 void launch_solve_large(const DevModel *models, const DevBatch &b, const DevResult &r, int mode, cudaStream_t s,
                         int num_sms);
-void launch_stats(const DevBatch &b, const DevResult &r, double *partials, double *stats, int n_buckets,
-                  cudaStream_t s);
+// Statistics of the local batch b = part `part` of `parts` (a power of two <= kStatsBlocks) of a batch
+// of n_total instances, i.e. its instances [n_total part / parts, n_total (part + 1) / parts): the
+// leaves [part W / parts, (part + 1) W / parts) of the global dyadic tree folded into their subtree
+// root.  Returns false (nothing launched) when the arguments do not describe such a part.
+bool launch_stats(const DevBatch &b, const DevResult &r, double *partials, double *stats, int n_buckets,
+                  long long n_total, int parts, int part, cudaStream_t s);
 void launch_eval(const DevModel *models, const DevBatch &b, const int *partition, const int *plan_nt,
                  const unsigned *plan_mask, const double *f_e, double slack,
                  double *E, double *tf, double *f_user, unsigned *viol, int *status, cudaStream_t s);
+// K6 (gen.cu): the C5 workload generated on the device -- input plumbing (jdobgen's device twin)
+struct GenParams {
+    unsigned long long seed;
+    long long inst_begin;
+    int hetero;
+    double zeta, kappa, f_min, f_max, R, p_u, fe_min, fe_max;
+    double rho[3], lat[3];
+};
+size_t gen_workspace_bytes(long long n);
+void launch_gen_inst(const GenParams &p, long long n, int *model_id, long long *user_off, double *t_free,
+                     double *fe_min, double *fe_max, double *rho, int *bucket, void *ws, cudaStream_t s);
+void launch_gen_users(const GenParams &p, long long n, const int *model_id, const long long *user_off, double *zeta,
+                      double *kappa, double *f_min, double *f_max, double *R, double *p_u, double *T, void *ws,
+                      cudaStream_t s);
 void launch_bruteforce(const DevModel *models, const DevBatch &b, int space, unsigned long long idx_begin,
                        unsigned long long idx_end, double *part_E, long long *part_idx, double *E_min,
                        long long *idx_min, int *status, cudaStream_t s);

@@ -1,10 +1,12 @@
 // K4: energy-saving statistics (row a12; "average energy consumption per user",
-// P:407; reduction vs LC; R16), bucketed, with a FIXED reduction tree:
-// block w of the fixed grid (one warp) owns the contiguous instance range
-// [w n / W, (w+1) n / W); each lane accumulates its fixed subsequence of it into
-// lane-private shared memory, the lanes are folded in lane order, and a final kernel
-// folds the per-block partials in a fixed tree.  Counts are exact integers.  Results are
-// therefore identical run to run for a given n_inst.
+// P:407; reduction vs LC; R16), bucketed, with a FIXED reduction tree
+// defined on the GLOBAL batch of n_total instances: leaf w of W = 1024 (one warp) owns the
+// contiguous instance range [w n / W, (w+1) n / W); each lane accumulates its fixed
+// subsequence of it into lane-private shared memory, the lanes are folded in lane order,
+// and the leaves are folded by the dyadic (pairwise) tree over w.  Counts are exact
+// integers.  A shard [r n / P, (r+1) n / P) of a power-of-two P is a subtree, so the
+// per-rank roots folded pairwise over r (paper_2504_14611_b200.dist.fold_stats) give the
+// same bits as one GPU over the whole batch.
 #include "jdob_dev.cuh"
 #include "kernels.h"
 
@@ -33,7 +35,9 @@ __device__ __forceinline__ int lane_slot(int f) {  // field -> per-lane slot, -1
 // range and accumulates them IN THAT ORDER into its own shared-memory slots (no shuffles, no atomics on
 // floating point); integer counters use shared-memory integer atomics (exact, order-free).  The lanes
 // are then folded in lane order, so the result is identical run to run.
-__global__ void __launch_bounds__(32) k_stats_partial(DevBatch b, DevResult r, double *partials, int n_buckets) {
+__global__ void __launch_bounds__(32) k_stats_partial(DevBatch b, DevResult r, double *partials, int n_buckets,
+                                                      long long n_total, long long begin, long long w0) {
+    // leaf w of the global tree = instances [n_total w / W, n_total (w + 1) / W); this block is w0 + blockIdx.x
     extern __shared__ double sh[];
     double *fs = sh;                                                        // [n_buckets][kLaneF][32]
     int *cnt = (int *)(sh + (size_t)n_buckets * kLaneF * 32);               // [n_buckets][kStatsF]
@@ -44,9 +48,9 @@ __global__ void __launch_bounds__(32) k_stats_partial(DevBatch b, DevResult r, d
     }
     for (int x = lane; x < n_buckets * kStatsF; x += 32) cnt[x] = 0;
     __syncwarp();
-    const long long W = gridDim.x;
-    const long long gw = blockIdx.x;
-    const long long i0 = b.n_inst * gw / W, i1 = b.n_inst * (gw + 1) / W;
+    const long long W = kStatsBlocks;
+    const long long gw = w0 + blockIdx.x;  // global leaf
+    const long long i0 = n_total * gw / W - begin, i1 = n_total * (gw + 1) / W - begin;
     // the lane's instances i0 + lane, + 32, ... in that order, four per step: the loads of the four are
     // issued together (latency overlap), the accumulation keeps the order (same bits)
     constexpr int U = 4;
@@ -111,29 +115,46 @@ __global__ void __launch_bounds__(32) k_stats_partial(DevBatch b, DevResult r, d
     }
 }
 
-// one warp per output element: lane l folds partials l, l+32, ... in order, then a fixed
-// xor-butterfly combines the lanes -- a fixed tree, so the result is run-to-run identical
-__global__ void k_stats_final(const double *partials, int n_blocks, int n_buckets, double *stats) {
+// One warp per output element: the dyadic tree over the nl (a power of two) leaves.  Lane l folds
+// its consecutive block of s = max(nl / 32, 1) leaves pairwise (a binary-counter stack: the same tree),
+// then an xor butterfly with d = 1, 2, 4, ... combines neighbouring blocks -- combine() is commutative
+// bit for bit, so lane l and lane l ^ d hold the same subtree value at every level.
+__global__ void k_stats_final(const double *partials, int nl, int n_buckets, double *stats) {
     const int lane = threadIdx.x & 31;
     const int x = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (x >= n_buckets * kStatsF) return;
     const int f = x % kStatsF;
+    const int s = nl >= 32 ? nl / 32 : 1;
+    double stack[11];
     double v = field_init(f);
-#pragma unroll 8
-    for (int blk = lane; blk < n_blocks; blk += 32) v = combine(f, v, partials[(size_t)blk * n_buckets * kStatsF + x]);
-#pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) v = combine(f, v, __shfl_xor_sync(0xffffffffu, v, d));
+    if (lane < nl) {
+        for (int i = 0; i < s; i++) {
+            double y = partials[(size_t)(lane * s + i) * n_buckets * kStatsF + x];
+            int lev = 0;
+            for (; (i >> lev) & 1; lev++) y = combine(f, stack[lev], y);
+            stack[lev] = y;
+        }
+        v = stack[__ffs(s) - 1];  // s is a power of two: the root of the lane's block
+    }
+    const int lanes = nl >= 32 ? 32 : nl;
+    for (int d = 1; d < lanes; d <<= 1) v = combine(f, v, __shfl_xor_sync(0xffffffffu, v, d));
     if (lane == 0) stats[x] = v;
 }
 
-void launch_stats(const DevBatch &b, const DevResult &r, double *partials, double *stats, int n_buckets,
-                  cudaStream_t s) {
+bool launch_stats(const DevBatch &b, const DevResult &r, double *partials, double *stats, int n_buckets,
+                  long long n_total, int parts, int part, cudaStream_t s) {
+    const long long W = kStatsBlocks;
+    if (parts < 1 || parts > W || (parts & (parts - 1)) || part < 0 || part >= parts || n_total < 0) return false;
+    const long long begin = n_total * part / parts, end = n_total * (part + 1) / parts;
+    if (b.n_inst != end - begin) return false;
+    const long long nl = W / parts, w0 = nl * part;  // leaf w0 starts at n_total w0 / W = begin
     const size_t smem = (size_t)n_buckets * kLaneF * 32 * sizeof(double) + (size_t)n_buckets * kStatsF * sizeof(int);
     cudaFuncSetAttribute(k_stats_partial, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)((size_t)JDOB_MAX_BUCKETS * (kLaneF * 32 * sizeof(double) + kStatsF * sizeof(int))));
-    k_stats_partial<<<kStatsBlocks, 32, smem, s>>>(b, r, partials, n_buckets);
+    k_stats_partial<<<(unsigned)nl, 32, smem, s>>>(b, r, partials, n_buckets, n_total, begin, w0);
     const int warps = n_buckets * kStatsF;
-    k_stats_final<<<(warps * 32 + 255) / 256, 256, 0, s>>>(partials, kStatsBlocks, n_buckets, stats);
+    k_stats_final<<<(warps * 32 + 255) / 256, 256, 0, s>>>(partials, (int)nl, n_buckets, stats);
+    return true;
 }
 
 }  // namespace jdob

@@ -44,6 +44,39 @@ def allreduce_stats(stats, dist):
     return red
 
 
+def fold_parts(parts):
+    """Fold statistics roots [P, n_buckets, 80] (P a power of two, part order) pairwise -- the top of the
+    dyadic tree of jdob_stats (include/jdob.h jdob_stats_part): fields add, except 3 (max) and 4 (min)."""
+    import torch
+    t = parts
+    while t.shape[0] > 1:
+        a, b = t[0::2], t[1::2]
+        s = a + b
+        s[:, :, STATS_MAX_FIELD] = torch.where(b[:, :, STATS_MAX_FIELD] > a[:, :, STATS_MAX_FIELD],
+                                               b[:, :, STATS_MAX_FIELD], a[:, :, STATS_MAX_FIELD])
+        s[:, :, STATS_MIN_FIELD] = torch.where(b[:, :, STATS_MIN_FIELD] < a[:, :, STATS_MIN_FIELD],
+                                               b[:, :, STATS_MIN_FIELD], a[:, :, STATS_MIN_FIELD])
+        t = s
+    return t[0]
+
+
+def fold_stats(stats, dist):
+    """Global statistics from per-rank roots of jdob_stats_part (rank r = part r of world): all_gather
+    of the [n_buckets, 80] roots (P x 40 KB at most) and the pairwise fold in rank order, on every rank.
+    The same bits as one jdob_stats call over the whole batch when the world size is a power of two;
+    otherwise the NCCL SUM/MAX/MIN fold (allreduce_stats), whose float sums are equal within 1e-9."""
+    import torch
+    world = dist.get_world_size()
+    if world & (world - 1):
+        return allreduce_stats(stats, dist)
+    x = stats.contiguous()
+    if dist.get_backend() == "gloo" and x.is_cuda:   # test-only backend: gather on the host
+        x = x.cpu()
+    parts = [torch.empty_like(x) for _ in range(world)]
+    dist.all_gather(parts, x)
+    return fold_parts(torch.stack(parts)).to(stats.device)
+
+
 def allreduce_argmin(E, idx, dist):
     """Global (E, idx) lexicographic minimum of per-rank partial argmins (1-element tensors).
 

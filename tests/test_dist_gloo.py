@@ -120,3 +120,27 @@ def test_shard_ranges_cover():
     size, k = 12 ** 8 * 64, 64
     rs = [D.bf_shard(size, k, 8, r) for r in range(8)]
     assert rs[0][0] == 0 and rs[-1][1] == size and all(a % k == 0 for a, _ in rs)
+
+
+def _fold_fn(rank, world):
+    # per-rank roots (random, with the max/min fields) folded over gloo: every rank gets the pairwise fold
+    rng = np.random.default_rng(100 + rank)
+    st = torch.from_numpy(rng.random((3, 80)) * 10.0 ** rng.integers(-3, 4, (3, 80)))
+    return D.fold_stats(st, dist).numpy(), st.numpy()
+
+
+def test_fold_stats_is_the_pairwise_tree():
+    out = run_world(_fold_fn)
+    roots = np.stack([out[0][1], out[1][1]])
+    want = roots[0] + roots[1]
+    want[:, 3] = np.maximum(roots[0][:, 3], roots[1][:, 3])
+    want[:, 4] = np.minimum(roots[0][:, 4], roots[1][:, 4])
+    for r in (0, 1):
+        assert np.array_equal(out[r][0], want)
+    # four parts: ((p0 + p1) + (p2 + p3)), field by field
+    rng = np.random.default_rng(5)
+    p = rng.random((4, 2, 80))
+    f = D.fold_parts(torch.from_numpy(p)).numpy()
+    s = (p[0] + p[1]) + (p[2] + p[3])
+    assert np.array_equal(f[:, 5], s[:, 5])
+    assert np.array_equal(f[:, 3], p[:, :, 3].max(0)) and np.array_equal(f[:, 4], p[:, :, 4].min(0))
