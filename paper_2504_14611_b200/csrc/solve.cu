@@ -68,7 +68,15 @@ struct SolveSmem {
     GridKCache kc;                       // k of the last (f_e,min, f_e,max, rho)
     double rinv[kMaxM];                  // RD(1 / R_m): lower-bound upload term
     double lb[64];                       // per n~: lower bound of every configuration's energy
+    // uniform users (UNI kernel, N <= kUniCache): the per-n~ values that depend only on the model and
+    // the users' shared (R, zeta, f_max, kappa, f_min, p_u) -- O/R, zeta v, gamma and the lower-bound
+    // member term -- formed once per warp for consecutive instances with the same key (Table I: all)
+    long long ukey[8];
+    double uOR[32], uZV[32], uG[32], uEM[32];
 };
+#ifndef JDOB_NO_UNI_CACHE
+constexpr int kUniCache = 32;
+#endif
 
 // Ranks under the key (gamma desc, T asc, index asc) (R2), then order[] and the
 // suffix-min deadlines L_i = min_{i' >= i} T_order[i'] (Eq. fth's min, R1).
@@ -113,13 +121,14 @@ __device__ __noinline__ void sort_users_T(int M, double T, SolveSmem &s, int lan
 
 // Alg. 1 lines 4-6 for partition point nt.  Returns i^ (M if none).
 __device__ __forceinline__ int setup_nt(const DevModel &md, int nt, int M, bool homog, bool uni, double t_free,
-                                        SolveSmem &s, int lane) {
+                                        SolveSmem &s, int lane, bool uc = false) {
     const double v_nt = md.v[nt], u_nt = md.u[nt], O_nt = md.O[nt];
     double gam = 0.0;
     if (lane < M) {
-        const double OR = O_nt / s.R[lane];  // Eq. (3)
-        const double zv = s.z[lane] * v_nt;
-        gam = OR + div_z(zv, s.f1[lane]);   // gamma
+        // uc: the same expressions, formed once per warp for this key (uniform users)
+        const double OR = uc ? s.uOR[nt] : O_nt / s.R[lane];  // Eq. (3)
+        const double zv = uc ? s.uZV[nt] : s.z[lane] * v_nt;
+        gam = uc ? s.uG[nt] : OR + div_z(zv, s.f1[lane]);      // gamma
         if (!uni || lane == 0) {             // uniform users: one copy serves every member
             s.orzv[lane] = make_double2(OR, zv);
             s.kuup[lane] = make_double2(s.kap[lane] * u_nt, OR * s.pu[lane]);  // Eq. (4)
@@ -283,6 +292,34 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     __syncwarp();
 
     const int B1 = md.B1;
+    bool uc = false;  // per-warp cache of the uniform users' per-n~ values
+#ifndef JDOB_NO_UNI_CACHE
+    if (UNI && N <= kUniCache) {
+        const long long key[7] = {(long long)mid, __double_as_longlong(R0), __double_as_longlong(z0),
+                                  __double_as_longlong(f10), __double_as_longlong(k0), __double_as_longlong(f00),
+                                  __double_as_longlong(p0)};
+        bool same = true;
+#pragma unroll
+        for (int q = 0; q < 7; q++) same = same && s.ukey[q] == key[q];
+        if (!__all_sync(0xffffffffu, same)) {  // every lane has read the key before lane 0 rewrites it
+            __syncwarp();
+            if (lane < N) {
+                const double O_nt = md.O[lane], v_nt = md.v[lane];
+                const double OR = O_nt / R0, zv = z0 * v_nt;  // the expressions of setup_nt and the bound
+                s.uOR[lane] = OR;
+                s.uZV[lane] = zv;
+                s.uG[lane] = OR + div_z(zv, f10);
+                s.uEM[lane] = (((k0 * md.u[lane]) * f00) * f00) + __dmul_rd(O_nt, recip_rd(R0)) * p0;
+            }
+            if (lane == 0) {
+#pragma unroll
+                for (int q = 0; q < 7; q++) s.ukey[q] = key[q];
+            }
+            __syncwarp();
+        }
+        uc = true;
+    }
+#endif
     const bool use_lb = PRUNE && mode != JDOB_MODE_BINARY;
     if (use_lb) {
         // Lower bound of E over every configuration at n~: a member's term
@@ -290,9 +327,9 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
         // monotone), a non-member's term is e_loc, so each term >= the min of the two; the user-order
         // RN sum of the minima is <= the sum of the terms, and the edge term (psi f_e) f_e >= 0.
         if (UNI) {  // every user has user 0's kappa, f_min, p_u and R: one bound term per n~
-            const double rv = recip_rd(R0), kv = k0, fv = f00, pv = p0;  // user 0's values
+            const double rv = uc ? 0.0 : recip_rd(R0), kv = k0, fv = f00, pv = p0;  // user 0's values
             for (int nt = lane; nt < N; nt += 32) {
-                const double em = (((kv * md.u[nt]) * fv) * fv) + __dmul_rd(md.O[nt], rv) * pv;
+                const double em = uc ? s.uEM[nt] : (((kv * md.u[nt]) * fv) * fv) + __dmul_rd(md.O[nt], rv) * pv;
                 double S = 0.0;
                 for (int m = 0; m < M; m++) {
                     const double el = s.et[m].x;
@@ -387,7 +424,7 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
             }
             if (COUNTS) c_setup += 1;
             last_nt = nt;
-            const int ihat = setup_nt(md, nt, M, homog, uni, t_free, s, lane);
+            const int ihat = setup_nt(md, nt, M, homog, uni, t_free, s, lane, uc);
             // two grid points per lane (j0 + lane and j0 + 32 + lane): the two energy chains are
             // independent, which doubles the instruction-level parallelism of the sweep and lets both
             // share each user's shared-memory loads
@@ -563,7 +600,7 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     // so the winner's are formed directly (same expressions as setup_nt) instead of a new set-up
     const bool win_direct = homog;
 #endif
-    if (!win_direct && bN != last_nt) setup_nt(md, bN, M, homog, uni, t_free, s, lane);
+    if (!win_direct && bN != last_nt) setup_nt(md, bN, M, homog, uni, t_free, s, lane, uc);
     const int Bo = M - bP;
     const double lo_ = s.Lg[bP].x;
     const double fe = grid_fe(fe_max, rho, bJ);
@@ -572,7 +609,8 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     const bool member = (lane < M) && (s.rank[lane] >= bP);
     double f = floc, arr = t_free;
     if (member) {
-        const double2 a = win_direct ? make_double2(md.O[bN] / s.R[lane], s.z[lane] * md.v[bN])
+        const double2 a = (win_direct && uc) ? make_double2(s.uOR[bN], s.uZV[bN])
+                          : win_direct ? make_double2(md.O[bN] / s.R[lane], s.z[lane] * md.v[bN])
                                      : s.orzv[uni ? 0 : lane];  // (O/R, zv)
         const double2 t = s.fmm[lane];                          // (f_min, f_max)
         const double budget = (lo_ - a.x) - te;
@@ -615,6 +653,7 @@ __global__ void __launch_bounds__(kSolveWarps * 32, UNI ? JDOB_SOLVE_MINB_U : JD
         s.inv_key = make_double2(0.0, 0.0);  // rho > 0 in every valid instance: no false hit
         s.inv_n = 0;
         s.kc = GridKCache{0.0, 0.0, 0.0, 0};  // rho > 0 in every valid instance: no false hit
+        s.ukey[0] = -1;                       // no model id -1: no false hit
     }
     __syncwarp();
     const long long gw = (long long)blockIdx.x * kSolveWarps + (threadIdx.x >> 5);
