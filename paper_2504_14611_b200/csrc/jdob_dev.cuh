@@ -163,20 +163,25 @@ struct InstRegs {  // lane-resident user parameters (lane = user)
 // (off, M64, mid) = user_off[i], the user count and model_id[i], loaded by the caller (K1 loads
 // the next instance's while it solves the current one).  The user loads are issued before the
 // model checks so that their latency overlaps the model-table loads.
+// The per-user predicates (box check, local feasibility P:127, T < t_free for Require P:259) and, when
+// `flags` is given, the instance flags (users differ from user 0 in (R, zeta, f_max) -> kNotHomog, in
+// (f_min, kappa, p_u) -> kNotUni, in T -> kNotSameT) are combined by ONE warp OR-reduction; the
+// statuses are then decided in the oracle's precedence order.
+constexpr unsigned kVBad = 1u, kVInfeas = 2u, kVRequire = 4u, kNotHomog = 8u, kNotUni = 16u, kNotSameT = 32u;
+
 __device__ __forceinline__ int warp_validate_pre(const DevModel *models, const DevBatch &b, long long i, int lane,
                                                  long long off, long long M64, int mid, InstRegs &x, int &M,
-                                                 long long &k, const DevModel *&mdp, GridKCache *kc = nullptr) {
+                                                 long long &k, const DevModel *&mdp, GridKCache *kc = nullptr,
+                                                 unsigned *flags = nullptr) {
     M = (M64 >= 1 && M64 <= kMaxM) ? (int)M64 : 0;
     k = 0;
     x.z = x.k = x.f0 = x.f1 = x.R = x.p = 0.0;
     x.T = dinf();
-#ifndef JDOB_LATE_SCALARS
     // the instance scalars are loaded with the users' values, so that both latencies overlap
     x.t_free = b.t_free[i];
     x.fe_min = b.fe_min[i];
     x.fe_max = b.fe_max[i];
     x.rho = b.rho[i];
-#endif
 #ifndef JDOB_LATE_USERS
     if (lane < M) {  // users of an instance rejected below are loaded but not used
         const long long u = off + lane;
@@ -198,6 +203,7 @@ __device__ __forceinline__ int warp_validate_pre(const DevModel *models, const D
     if (M64 < 1 || M64 > kMaxMLarge || M64 > mdp->B1 - 1) return JDOB_ST_BADPARAM;
     if (M64 > kMaxM) return kStDefer;  // more users than lanes: the block-per-instance path
     bool ok = true;
+    unsigned bits = 0u;
     if (lane < M) {
 #ifdef JDOB_LATE_USERS
         const long long u = off + lane;
@@ -213,14 +219,31 @@ __device__ __forceinline__ int warp_validate_pre(const DevModel *models, const D
              dfinite(x.T);
         ok = ok && (x.z >= 0.0) && (x.k >= 0.0) && (x.f0 > 0.0) && (x.f0 <= x.f1) && (x.R > 0.0) &&
              (x.p >= 0.0) && (x.T > 0.0);
+        bits |= ok ? 0u : kVBad;
     }
-    if (__any_sync(0xffffffffu, !ok)) return JDOB_ST_BADPARAM;
-#ifdef JDOB_LATE_SCALARS
-    x.t_free = b.t_free[i];
-    x.fe_min = b.fe_min[i];
-    x.fe_max = b.fe_max[i];
-    x.rho = b.rho[i];
-#endif
+    const double vN = mdp->v[mdp->N];
+    if (lane < M) {
+        // P:127 literally RN(zeta v_N / f_max) > T; when T f_max - zeta v_N > 0 exactly (the fma's sign)
+        // the quotient is < T, so RN(.) <= T and the test fails without the division
+        const double zvN = x.z * vN;
+        if (!(__fma_rn(x.T, x.f1, -zvN) > 0.0) && (zvN / x.f1 > x.T)) bits |= kVInfeas;
+        if (x.T < x.t_free) bits |= kVRequire;  // min_m T_m < t_free <=> some T_m < t_free
+    }
+    if (flags) {
+        auto sb = [](double a, double c) { return __double_as_longlong(a) == __double_as_longlong(c); };
+        const double R0 = __shfl_sync(0xffffffffu, x.R, 0), z0 = __shfl_sync(0xffffffffu, x.z, 0),
+                     f10 = __shfl_sync(0xffffffffu, x.f1, 0), f00 = __shfl_sync(0xffffffffu, x.f0, 0),
+                     k0 = __shfl_sync(0xffffffffu, x.k, 0), p0 = __shfl_sync(0xffffffffu, x.p, 0),
+                     T0 = __shfl_sync(0xffffffffu, x.T, 0);
+        if (lane < M) {
+            if (!(sb(x.R, R0) && sb(x.z, z0) && sb(x.f1, f10))) bits |= kNotHomog;
+            if (!(sb(x.f0, f00) && sb(x.k, k0) && sb(x.p, p0))) bits |= kNotUni;
+            if (!(x.T == T0)) bits |= kNotSameT;
+        }
+    }
+    bits = __reduce_or_sync(0xffffffffu, bits);
+    if (flags) *flags = bits;
+    if (bits & kVBad) return JDOB_ST_BADPARAM;
     const double t_free = x.t_free, fe_min = x.fe_min, fe_max = x.fe_max, rho = x.rho;
     if (!(dfinite(t_free) && dfinite(fe_min) && dfinite(fe_max) && dfinite(rho) && (t_free >= 0.0) &&
           (fe_min > 0.0) && (fe_min <= fe_max) && (rho > 0.0)))
@@ -238,14 +261,8 @@ __device__ __forceinline__ int warp_validate_pre(const DevModel *models, const D
         k = grid_k(fe_min, fe_max, rho);
     }
     if (k > kMaxK) return JDOB_ST_BADPARAM;
-    const double vN = mdp->v[mdp->N];
-    // P:127 literally RN(zeta v_N / f_max) > T; when T f_max - zeta v_N > 0 exactly (the fma's sign)
-    // the quotient is < T, so RN(.) <= T and the test fails without the division
-    const double zvN = x.z * vN;
-    const bool infeas = (lane < M) && !(__fma_rn(x.T, x.f1, -zvN) > 0.0) && (zvN / x.f1 > x.T);
-    if (__any_sync(0xffffffffu, infeas)) return JDOB_ST_LOCAL_INFEASIBLE;
-    const double Tmin = warp_min_nonneg(x.T);  // T > 0 (checked above), +inf beyond M
-    if (Tmin < t_free) return JDOB_ST_REQUIRE;
+    if (bits & kVInfeas) return JDOB_ST_LOCAL_INFEASIBLE;
+    if (bits & kVRequire) return JDOB_ST_REQUIRE;
     return JDOB_ST_OK;
 }
 

@@ -218,7 +218,8 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     int M;
     const DevModel *mdp;
     InstRegs x;
-    const int st = warp_validate_pre(models, b, i, lane, off, M64, mid, x, M, k, mdp, &s.kc);
+    unsigned vflags = 0u;
+    const int st = warp_validate_pre(models, b, i, lane, off, M64, mid, x, M, k, mdp, &s.kc, &vflags);
     if (st == kStDefer) return;  // M > 32: solved by k_solve_large (solve_large.cu)
     const double t_free = x.t_free, fe_max = x.fe_max, rho = x.rho;
     if (st == JDOB_ST_BADPARAM || st == JDOB_ST_BADMODEL) {
@@ -268,17 +269,16 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     }
     // instance-level flags (warp-uniform)
     const double R0 = s.R[0], z0 = s.z[0], f10 = s.f1[0];  // user 0's values
-    auto sb = [](double a, double c) { return __double_as_longlong(a) == __double_as_longlong(c); };
-    const bool homog_ = __all_sync(0xffffffffu, lane >= M || (sb(x.R, R0) && sb(x.z, z0) && sb(x.f1, f10)));
+    // (from the validation's single warp reduction)
+    const bool homog_ = !(vflags & kNotHomog);
     const double f00 = s.fmm[0].x, k0 = s.kap[0], p0 = s.pu[0];
-    const bool uni_ = homog_ && __all_sync(0xffffffffu, lane >= M || (sb(x.f0, f00) && sb(x.k, k0) && sb(x.p, p0)));
+    const bool uni_ = homog_ && !(vflags & kNotUni);
     if (UNI && !uni_) {  // left to the general kernel
         if (lane == 0) r.status[i] = kStDefer;
         return;
     }
     const bool homog = UNI ? true : homog_, uni = UNI ? true : uni_;
-    const double T0 = s.T[0];
-    if (homog && __all_sync(0xffffffffu, lane >= M || x.T == T0)) {
+    if (homog && !(vflags & kNotSameT)) {
         // equal gamma and equal deadlines (Table I identical-deadline setting): the key (T asc,
         // index asc) is the index order and every suffix minimum is T
         if (lane < M) {
