@@ -68,6 +68,8 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
+    p.add_argument("--eval-step", action="store_true",
+                   help="re-verify the plans with jdob_eval (K3) inside the step instead of the solver's epilogue")
     p.add_argument("--host-gen", action="store_true",
                    help="c5: generate on the host and copy (default: generated on the device, no input H2D)")
     return p.parse_args()
@@ -417,7 +419,8 @@ def run_mine(args):
     setup_frac = float(wk[:, 0].sum()) / float(np.array([m.N for m in batch.models])[np.asarray(batch.model_id)].sum())
     del res_c
 
-    res = J.solve_batch(db, f_user=False)
+    fused = not args.eval_step   # a11: the plans re-verified in K1's epilogue (jdob_eval's bits)
+    res = J.solve_batch(db, f_user=False, verify=fused)
     # this rank's root of the statistics tree over the whole job's batch (jdob_stats_part); the
     # pairwise fold over ranks (dist.fold_stats) has the bits of one GPU over the whole batch
     part = (n_total, world, rank)
@@ -429,9 +432,10 @@ def run_mine(args):
     stream = torch.cuda.current_stream()
 
     def step():
-        J.solve_batch(db, f_user=False, out=res)
+        J.solve_batch(db, f_user=False, out=res, verify=fused)
         J.stats(db, res, out=res["stats"], part=part)
-        J.eval_plans(db, plans=res, f_user=False, out=ev)
+        if not fused:
+            J.eval_plans(db, plans=res, f_user=False, out=ev)
         if dist:
             res["stats_global"] = fold_stats(res["stats"], dist)
 
@@ -451,10 +455,11 @@ def run_mine(args):
     t_s.record(stream)
     for i in range(K):
         ev_s[i].record(stream)
-        J.solve_batch(db, f_user=False, out=res)           # K0 + K1 (K0: one tiny block per model)
+        J.solve_batch(db, f_user=False, out=res, verify=fused)  # K0 + K1 (+ a11 in K1's epilogue)
         ev_e[i].record(stream)
         J.stats(db, res, out=res["stats"], part=part)      # K4
-        J.eval_plans(db, plans=res, f_user=False, out=ev)  # K3
+        if not fused:
+            J.eval_plans(db, plans=res, f_user=False, out=ev)  # K3
         if dist:
             res["stats_global"] = fold_stats(res["stats"], dist)
     t_e.record(stream)
@@ -465,7 +470,20 @@ def run_mine(args):
     clk = clocks.stop()
     total_ms = t_s.elapsed_time(t_e)
     solve_ms = float(np.mean([a.elapsed_time(b) for a, b in zip(ev_s, ev_e)]))
-    viol = int((ev["violations"] != 0).sum().item())
+    if fused:   # bit 31 alone marks an unverified M > 32 instance (none in these workloads)
+        viol = int((res["violations"] != 0).sum().item())
+    else:
+        viol = int((ev["violations"] != 0).sum().item())
+    # K3 (jdob_eval) over the same plans, timed on its own: the standalone a11 entry point, and the
+    # check that its bits equal the epilogue's
+    s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s_.record(stream)
+    for _ in range(3):
+        J.eval_plans(db, plans=res, f_user=False, out=ev)
+    e_.record(stream)
+    torch.cuda.synchronize()
+    eval_leg = {"kernel": "k_eval (K3, jdob_eval)", "ms": s_.elapsed_time(e_) / 3,
+                "bits_equal_epilogue": bool(torch.equal(ev["violations"], res["violations"])) if fused else None}
     if dist:
         t = torch.tensor([total_ms, solve_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -568,7 +586,9 @@ def run_mine(args):
             "config": {"workload": label, "n_inst_per_gpu": n, "global_instances": n_total,
                        "users_per_gpu": int(batch.n_users), "input_bytes_per_gpu": int(batch.nbytes()),
                        "l2": "inputs larger than L2 (126 MB)" if batch.nbytes() > 126e6 else "inputs fit in L2",
-                       "step": "jdob_solve_batch (K0+K1) + jdob_stats (K4) + jdob_eval of every plan (K3)"
+                       "step": ("jdob_solve_batch (K0 + K1, every plan re-verified in K1's epilogue with "
+                                "jdob_eval's formulas, row a11) + jdob_stats (K4)" if fused else
+                                "jdob_solve_batch (K0+K1) + jdob_stats (K4) + jdob_eval of every plan (K3)")
                                + (" + NCCL stats allreduce" if dist else ""),
                        "parallelism": f"dp{world}"},
             "roofline": {"bound": "alu", "kernel": "k_solve (K1)", "unit": "G FP64-pipe instr/s",
@@ -592,10 +612,11 @@ def run_mine(args):
                                       "this launch (profiles/) over the live time"},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": 6 * K,
+            "gpu_launches": (5 if fused else 6) * K,
             "clocks": clk,
             "bruteforce": bf,
             "plan_violations": viol,
+            "eval_leg": eval_leg,
             "parity": parity,
         }
         print(json.dumps(line), flush=True)

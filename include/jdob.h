@@ -154,6 +154,13 @@ typedef struct {
     int64_t *work;      /* optional [4*n_inst], ignored when counts != NULL and by the host API:
                            work the pruned sweep executed per instance -- n~ set-ups, visited
                            pairs, evaluated pairs, member evaluations */
+    uint32_t *violations; /* optional [n_inst] (NULL = skip; ignored by the host API): the plan
+                           re-verified in the solver's epilogue with jdob_eval's formulas and
+                           bits at relative slack `slack` (row a11: D6 bit 0, D7 bit 1, D8 bit 2,
+                           non-positive budget bit 3, Require bit 4, f_e box bit 5) -- the same
+                           bits jdob_eval returns for the (n_tilde, mask, f_e) outputs; 0 for
+                           BADPARAM/BADMODEL; bit 31 only ("not verified") for M_i > 32 */
+    double slack;
 } jdob_result;
 
 /*

@@ -40,7 +40,9 @@ class JResult(C.Structure):
     _fields_ = [(f, C.c_void_p) for f in ("E", "E_lc", "t_free_next", "f_e", "n_tilde", "j", "status", "mask",
                                           "f_user", "counts", "stats")] + [("n_buckets", C.c_int32),
                                                                            ("partition", C.c_void_p),
-                                                                           ("work", C.c_void_p)]
+                                                                           ("work", C.c_void_p),
+                                                                           ("violations", C.c_void_p),
+                                                                           ("slack", C.c_double)]
 
 
 class JGenParams(C.Structure):
@@ -236,8 +238,10 @@ class DeviceBatch:
 
 def solve_batch(db: DeviceBatch, mode: int = MODE_FULL, f_user: bool = True, counts: bool = False,
                 stats: bool = False, n_buckets: Optional[int] = None, stream=None, out: Optional[dict] = None,
-                partition: bool = False, work: bool = False) -> dict:
-    """jdob_solve_batch: J-DOB (Alg. 1/2) over every instance of `db`; outputs are device tensors."""
+                partition: bool = False, work: bool = False, verify: bool = False, slack: float = 1e-9) -> dict:
+    """jdob_solve_batch: J-DOB (Alg. 1/2) over every instance of `db`; outputs are device tensors.
+    verify: the plans re-verified in the solver's epilogue with jdob_eval's formulas (row a11) ->
+    out["violations"] (uint32 bits as int32), the bits jdob_eval returns for the same plans."""
     torch = _torch()
     dev = db.device
     n, nu = db.n_inst, db.n_users
@@ -261,10 +265,12 @@ def solve_batch(db: DeviceBatch, mode: int = MODE_FULL, f_user: bool = True, cou
             out["partition"] = torch.empty(nu, dtype=torch.int32, device=dev)
         if work:
             out["work"] = torch.empty((n, 4), dtype=torch.int64, device=dev)
+        if verify:
+            out["violations"] = torch.empty(n, dtype=torch.int32, device=dev)
     r = JResult(*[_ptr(out.get(f)) for f in ("E", "E_lc", "t_free_next", "f_e", "n_tilde", "j", "status", "mask",
                                              "f_user", "counts", "stats")],
                 int(out["stats"].shape[0]) if out.get("stats") is not None else 0, _ptr(out.get("partition")),
-                _ptr(out.get("work")))
+                _ptr(out.get("work")), _ptr(out.get("violations")), float(slack))
     ws = db.workspace(0)
     _check(lib().jdob_solve_batch(db.jmodels, db.n_models, C.byref(db.jbatch), int(mode), C.byref(r),
                                   ws.data_ptr(), ws.numel(), _stream_handle(stream)))

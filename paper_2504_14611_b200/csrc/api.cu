@@ -257,6 +257,8 @@ int jdob_solve_batch(const jdob_model *models, int32_t n_models, const jdob_batc
     dr.counts = (long long *)out->counts;
     dr.partition = out->partition;
     dr.work = (long long *)out->work;
+    dr.viol = out->violations;
+    dr.slack = out->slack;
     launch_solve(dm, db, dr, mode, s, num_sms());
     // instances with 32 < M <= B_max (block per instance); M > B_max is BADPARAM, so the launch is
     // needed only when some model admits batches wider than a warp
@@ -600,6 +602,7 @@ int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob
     dr.stats = out->stats ? (double *)take((size_t)out->n_buckets * JDOB_STATS_FIELDS * 8) : nullptr;
     dr.partition = out->partition ? (int32_t *)take(nu * 4) : nullptr;
     dr.work = nullptr;  // device-API diagnostic only
+    dr.violations = nullptr;
     void *ws[NS];
     for (int k = 0; k < NS; k++) ws[k] = take(wsb);
 

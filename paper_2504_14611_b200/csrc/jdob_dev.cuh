@@ -51,6 +51,8 @@ struct DevResult {
     long long *counts;
     int *partition = nullptr;   // per user n~* or N, or NULL
     long long *work = nullptr;  // [4 n_inst] executed-work counters of the pruned sweep, or NULL
+    unsigned *viol = nullptr;   // [n_inst] the plan re-verified in the epilogue (jdob_eval bits), or NULL
+    double slack = 0.0;
 };
 
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }

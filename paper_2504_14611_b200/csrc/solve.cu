@@ -174,9 +174,19 @@ __device__ __forceinline__ void write_bad(const DevResult &r, long long i, long 
             r.counts[3 * i + 2] = 0;
         }
         if (r.work) r.work[4 * i] = r.work[4 * i + 1] = r.work[4 * i + 2] = r.work[4 * i + 3] = 0;
+        if (r.viol) r.viol[i] = 0u;  // jdob_eval reports no bits for a malformed instance
     }
     if (r.f_user && M >= 1 && M <= kMaxM && lane < M) r.f_user[off + lane] = dnan();
     if (r.partition && M >= 1 && M <= kMaxM && lane < M) r.partition[off + lane] = N;
+}
+
+// The all-local plan re-verified with jdob_eval's formulas (row a11): Require (bit 4) and each
+// local user's D8 at relative slack (bit 2); the eval call's own status does not enter the bits.
+__device__ __forceinline__ unsigned verify_local(const InstRegs &x, double vN, double floc, int M, unsigned vflags,
+                                                 double slack, int lane) {
+    unsigned vb = (vflags & kVRequire) ? 16u : 0u;
+    if (lane < M && (x.z * vN) / floc > x.T + slack * fabs(x.T)) vb |= 4u;
+    return __reduce_or_sync(0xffffffffu, vb);
 }
 
 __device__ __forceinline__ void write_local(const DevResult &r, long long i, long long off, int M, int N,
@@ -251,6 +261,10 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     for (int t = 0; t < M; t++) E_lc = E_lc + s.et[t].x;  // user-index order
     if (st != JDOB_ST_OK || mode == JDOB_MODE_LC) {
         write_local(r, i, off, M, N, E_lc, t_free, floc, st, lane, true);
+        if (r.viol) {
+            const unsigned vb = verify_local(x, vN, floc, M, vflags, r.slack, lane);
+            if (lane == 0) r.viol[i] = vb;
+        }
         return;
     }
 
@@ -590,6 +604,10 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     const bool offload_wins = (bE < E_lc) || (bE == E_lc && (bN < aN || (bN == aN && bJ < aJ)));
     if (!offload_wins) {
         write_local(r, i, off, M, N, E_lc, t_free, floc, st, lane, false);
+        if (r.viol) {
+            const unsigned vb = verify_local(x, vN, floc, M, vflags, r.slack, lane);
+            if (lane == 0) r.viol[i] = vb;
+        }
         return;
     }
     // winner: recompute D20 and D22 lane = user (same arithmetic as the sweep)
@@ -608,6 +626,14 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     const double te = md.phi[bN * B1 + Bo] * inv;
     const bool member = (lane < M) && (s.rank[lane] >= bP);
     double f = floc, arr = t_free;
+    unsigned vbits = 0u;  // the plan re-verified with jdob_eval's formulas (row a11), when r.viol
+    if (r.viol) {
+        if (lane == 0) {
+            if (!(fe >= x.fe_min && fe <= fe_max)) vbits |= 32u;
+            if (t_free + te > lo_ + r.slack * fabs(lo_)) vbits |= 1u;  // D6: the ASAP start of batch n~ + 1
+        }
+        if (!member && lane < M && (x.z * vN) / floc > x.T + r.slack * fabs(x.T)) vbits |= 4u;  // D8
+    }
     if (member) {
         const double2 a = (win_direct && uc) ? make_double2(s.uOR[bN], s.uZV[bN])
                           : win_direct ? make_double2(md.O[bN] / s.R[lane], s.z[lane] * md.v[bN])
@@ -617,10 +643,26 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
         const bool low = (a.y == 0.0) || (__fma_rn(t.x, budget, -a.y) > 0.0);
         f = low ? t.x : clampf(a.y / budget, t.x, t.y);
         arr = div_z(a.y, f) + a.x;
+        if (r.viol) {
+            // jdob_eval's D20 branches (bit 3 and the f of an infeasible budget) and its D7 finish test
+            double fev = f;
+            if (a.y == 0.0) {
+                if (budget < 0.0) vbits |= 8u;
+            } else if (!(__fma_rn(t.x, budget, -a.y) > 0.0) && !(budget > 0.0)) {
+                vbits |= 8u;
+                fev = t.y;
+            }
+            const double fin = (div_z(a.y, fev) + a.x) + te;
+            if (fin > lo_ + r.slack * fabs(lo_)) vbits |= 2u;
+        }
         if (arr < t_free) arr = t_free;
     }
     arr = warp_max_nonneg(arr);  // arrivals >= t_free >= 0
     const unsigned mask = __ballot_sync(0xffffffffu, member);
+    if (r.viol) {
+        vbits = __reduce_or_sync(0xffffffffu, vbits);
+        if (lane == 0) r.viol[i] = vbits;
+    }
     if (lane == 0) {
         r.E[i] = bE;
         r.E_lc[i] = E_lc;

@@ -178,6 +178,8 @@ __device__ void large_instance(long long i, const DevModel *models, const DevBat
             r.n_tilde[i] = N;
             r.j[i] = 0;
             r.status[i] = st;
+            // jdob_eval gives no bits for a malformed instance; the others are not verified here
+            if (r.viol) r.viol[i] = (st == JDOB_ST_BADPARAM || st == JDOB_ST_BADMODEL) ? 0u : 0x80000000u;
             r.mask[i] = 0u;
             if (r.counts) r.counts[3 * i] = r.counts[3 * i + 1] = r.counts[3 * i + 2] = 0;
             if (r.work) r.work[4 * i] = r.work[4 * i + 1] = r.work[4 * i + 2] = r.work[4 * i + 3] = 0;
@@ -214,6 +216,8 @@ __device__ void large_instance(long long i, const DevModel *models, const DevBat
             r.n_tilde[i] = N;
             r.j[i] = 0;
             r.status[i] = st;
+            // jdob_eval gives no bits for a malformed instance; the others are not verified here
+            if (r.viol) r.viol[i] = (st == JDOB_ST_BADPARAM || st == JDOB_ST_BADMODEL) ? 0u : 0x80000000u;
             r.mask[i] = 0u;
             if (r.counts && zero_counts) r.counts[3 * i] = r.counts[3 * i + 1] = r.counts[3 * i + 2] = 0;
             if (r.work && zero_counts) r.work[4 * i] = r.work[4 * i + 1] = r.work[4 * i + 2] = r.work[4 * i + 3] = 0;
@@ -406,6 +410,7 @@ __device__ void large_instance(long long i, const DevModel *models, const DevBat
         r.n_tilde[i] = bN;
         r.j[i] = bJ;
         r.status[i] = st;
+        if (r.viol) r.viol[i] = 0x80000000u;  // not verified in this kernel (include/jdob.h)
         r.mask[i] = 0u;  // M > 32: see partition
     }
     __syncthreads();

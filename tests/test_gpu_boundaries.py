@@ -147,3 +147,15 @@ def test_boundaries_stats(J):
         assert np.array_equal(np.isnan(a), np.isnan(b))
         ok = ~np.isnan(a)
         assert np.all(np.abs(a[ok] - b[ok]) <= 1e-9 * np.maximum(np.abs(a[ok]), np.abs(b[ok])))
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_boundaries_fused_verify(J, case):
+    """The solver's epilogue verification (row a11) on the boundary instances: the bits of jdob_eval,
+    at slack 0 and 1e-9 (the R10 clamp cases sit exactly on D7)."""
+    for b in (build(case), twin(case)):
+        db = J.DeviceBatch(b)
+        for slack in (0.0, 1e-9):
+            res = J.solve_batch(db, verify=True, slack=slack)
+            ev = to_np(J.eval_plans(db, plans=res, slack=slack))
+            assert_bits_equal(res["violations"].cpu().numpy().view(np.uint32), ev["violations"], case)

@@ -642,3 +642,27 @@ def test_bf_work_counters(J):
         Eo, Io, So = O.bf(t, space)
         assert (float(E.item()), int(I.item())) == (Eo, Io)
         assert int(W[0].item()) == O.bf_space_size(t, space) // O.grid_k(t)
+
+
+def _verify_batches():
+    yield "random-t_free", g.random_batch(seed=160, n_inst=3000, M_hi=32, N_hi=12, k_max=80, tfree_frac=0.5)
+    yield "random-small", g.random_batch(seed=161, n_inst=3000, M_hi=6, N_hi=4, k_max=20, identical_T_frac=0.7)
+    yield "c2", g.config_batch("c2", n_inst=20000)
+    yield "c3", g.config_batch("c3", n_inst=20000)
+    yield "c5", g.config_batch("c5", n_inst=20000)
+
+
+@pytest.mark.parametrize("slack", [0.0, 1e-9])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
+def test_fused_verify_equals_eval(J, mode, slack):
+    """Row a11 in the solver's epilogue: the violation bits of every plan equal jdob_eval's for the
+    (n_tilde, mask, f_e) outputs at the same slack; the other outputs are unchanged."""
+    for name, b in _verify_batches():
+        db = J.DeviceBatch(b)
+        plain = to_np(J.solve_batch(db, mode=mode))
+        res = J.solve_batch(db, mode=mode, verify=True, slack=slack)
+        ev = to_np(J.eval_plans(db, plans=res, slack=slack))
+        out = to_np(res)
+        for f in PRODUCT_FIELDS:
+            assert_bits_equal(out[f], plain[f], f"{name} {f}")
+        assert_bits_equal(out["violations"].view(np.uint32), ev["violations"], f"{name} violations")
