@@ -45,14 +45,35 @@ def users_batch(model, T_lists, seed_tag=""):
     return G._batch_from_lists([model], np.zeros(n, np.int32), Ms, cols, inst)
 
 
-def fig4(J, out_dir):
-    import torch
+def fig4_batches():
+    """(beta, T, Ms, batch): one instance per M = 1..32 at the identical deadline of beta."""
     m = G.profiles.mobilenetv2()
-    rows = []
+    out = []
     for beta in (2.13, 30.25):
         T = float(G.deadline_from_beta(m, G.profiles.ZETA, 2.6e9, beta))
         Ms = list(range(1, 33))
-        b = users_batch(m, [[T] * M for M in Ms])
+        out.append((beta, T, Ms, users_batch(m, [[T] * M for M in Ms])))
+    return out
+
+
+def fig5_batches(trials, seed=55):
+    """(M, lo, hi, batch): `trials` instances of M users with beta ~ U[lo, hi] i.i.d.."""
+    m = G.profiles.mobilenetv2()
+    lat = float(G.min_local_latency(m, np.array([G.profiles.ZETA]), np.array([2.6e9]))[0])
+    out = []
+    for M in (10, 20):
+        for (lo, hi) in ((4.5, 5.5), (2.0, 8.0), (0.0, 10.0)):
+            ids = np.arange(trials)
+            beta = G.uniform(G.draw(seed, np.repeat(ids, M), np.tile(np.arange(M), trials), G.F_BETA_USER), lo, hi)
+            T = (1.0 + beta) * lat
+            out.append((M, lo, hi, users_batch(m, [list(T[t * M:(t + 1) * M]) for t in range(trials)])))
+    return out
+
+
+def fig4(J, out_dir):
+    import torch
+    rows = []
+    for beta, T, Ms, b in fig4_batches():
         db = J.DeviceBatch(b)
         res = {}
         for name, mode in METHODS:
@@ -74,25 +95,18 @@ def fig4(J, out_dir):
 
 def fig5(J, out_dir, trials, seed=55):
     import torch
-    m = G.profiles.mobilenetv2()
-    lat = float(G.min_local_latency(m, np.array([G.profiles.ZETA]), np.array([2.6e9]))[0])
     rows = []
-    for M in (10, 20):
-        for (lo, hi) in ((4.5, 5.5), (2.0, 8.0), (0.0, 10.0)):
-            ids = np.arange(trials)
-            beta = G.uniform(G.draw(seed, np.repeat(ids, M), np.tile(np.arange(M), trials), G.F_BETA_USER), lo, hi)
-            T = (1.0 + beta) * lat
-            b = users_batch(m, [list(T[t * M:(t + 1) * M]) for t in range(trials)])
-            db = J.DeviceBatch(b)
-            row = dict(M=M, beta_lo=lo, beta_hi=hi, trials=trials)
-            for name, mode in METHODS:
-                r = J.solve_grouped(db, mode=mode, f_user=False)
-                torch.cuda.synchronize()
-                row[name] = float(r["E"].cpu().numpy().mean() / M)
-                if name == "J-DOB":
-                    row["mean_groups"] = float(r["n_groups"].cpu().numpy().mean())
-            row["reduction_%"] = 100 * (1 - row["J-DOB"] / row["LC"])
-            rows.append(row)
+    for M, lo, hi, b in fig5_batches(trials, seed):
+        db = J.DeviceBatch(b)
+        row = dict(M=M, beta_lo=lo, beta_hi=hi, trials=trials)
+        for name, mode in METHODS:
+            r = J.solve_grouped(db, mode=mode, f_user=False)
+            torch.cuda.synchronize()
+            row[name] = float(r["E"].cpu().numpy().mean() / M)
+            if name == "J-DOB":
+                row["mean_groups"] = float(r["n_groups"].cpu().numpy().mean())
+        row["reduction_%"] = 100 * (1 - row["J-DOB"] / row["LC"])
+        rows.append(row)
     with open(os.path.join(out_dir, "fig5.csv"), "w", newline="") as f:
         w = csv.DictWriter(f, fieldnames=list(rows[0].keys()))
         w.writeheader()

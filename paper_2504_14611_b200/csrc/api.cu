@@ -9,6 +9,7 @@
 
 #include "jdob_dev.cuh"
 #include "kernels.h"
+#include <nvtx3/nvToolsExt.h>
 
 namespace jdob {
 void launch_bruteforce_impl(const DevModel *models, const DevBatch &b, int model_id, int N, int M, int space,
@@ -187,6 +188,12 @@ static int num_sms() {
     return n > 0 ? n : 148;
 }
 
+// NVTX range around each entry point (header-only NVTX v3: a no-op unless a profiler is attached)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 extern "C" {
 
 const char *jdob_last_error(void) { return g_err.c_str(); }
@@ -227,6 +234,7 @@ uint64_t jdob_bf_space_size(int32_t space, int32_t N, int32_t M, int64_t k) {
 
 int jdob_solve_batch(const jdob_model *models, int32_t n_models, const jdob_batch *b, int32_t mode,
                      const jdob_result *out, void *ws, size_t ws_bytes, void *stream) {
+    NvtxRange nvtx_("jdob_solve_batch");
     g_err.clear();
     int rc = check_models(models, n_models);
     if (rc) return rc;
@@ -280,6 +288,7 @@ int jdob_stats(const jdob_batch *b, const jdob_result *res, void *ws, size_t ws_
 
 int jdob_stats_part(const jdob_batch *b, const jdob_result *res, int64_t n_total, int32_t parts, int32_t part,
                     void *ws, size_t ws_bytes, void *stream) {
+    NvtxRange nvtx_("jdob_stats_part");
     g_err.clear();
     if (!b || !res) return fail(JDOB_EINVAL, "stats: NULL batch or result");
     if (b->n_inst < 0) return fail(JDOB_EINVAL, "n_inst < 0");
@@ -334,6 +343,7 @@ size_t jdob_generate_workspace_bytes(int64_t n_inst) { return n_inst < 0 ? 0 : g
 
 int jdob_generate_c5_instances(const jdob_gen_params *p, const jdob_batch *b, int64_t *n_users, void *ws,
                                size_t ws_bytes, void *stream) {
+    NvtxRange nvtx_("jdob_generate_c5_instances");
     g_err.clear();
     if (!p || !b || !n_users) return fail(JDOB_EINVAL, "generate: NULL argument");
     if (b->n_inst < 0) return fail(JDOB_EINVAL, "n_inst < 0");
@@ -354,6 +364,7 @@ int jdob_generate_c5_instances(const jdob_gen_params *p, const jdob_batch *b, in
 }
 
 int jdob_generate_c5_users(const jdob_gen_params *p, const jdob_batch *b, void *ws, size_t ws_bytes, void *stream) {
+    NvtxRange nvtx_("jdob_generate_c5_users");
     g_err.clear();
     if (!p || !b) return fail(JDOB_EINVAL, "generate: NULL argument");
     if (b->n_inst > 0 && (!b->model_id || !b->user_off || !b->zeta || !b->kappa || !b->f_min || !b->f_max ||
@@ -380,6 +391,7 @@ size_t jdob_grouped_workspace_bytes(const jdob_model *models, int32_t n_models, 
 
 int jdob_solve_grouped(const jdob_model *models, int32_t n_models, const jdob_batch *b, int32_t mode,
                        const jdob_grouped_result *out, void *ws, size_t ws_bytes, void *stream) {
+    NvtxRange nvtx_("jdob_solve_grouped");
     g_err.clear();
     int rc = check_models(models, n_models);
     if (rc) return rc;
@@ -455,6 +467,7 @@ int jdob_eval(const jdob_model *models, int32_t n_models, const jdob_batch *b, c
               const int32_t *plan_n_tilde, const uint32_t *plan_mask, const double *f_e, double slack, double *E,
               double *t_free_next, double *f_user, uint32_t *violations, int32_t *status, void *ws, size_t ws_bytes,
               void *stream) {
+    NvtxRange nvtx_("jdob_eval");
     g_err.clear();
     int rc = check_models(models, n_models);
     if (rc) return rc;
@@ -475,6 +488,7 @@ int jdob_eval(const jdob_model *models, int32_t n_models, const jdob_batch *b, c
 int jdob_bruteforce(const jdob_model *models, int32_t n_models, const jdob_batch *b, int32_t space,
                     uint64_t idx_begin, uint64_t idx_end, double *E_min, int64_t *idx_min, int32_t *status,
                     int64_t *work, void *ws, size_t ws_bytes, void *stream) {
+    NvtxRange nvtx_("jdob_bruteforce");
     g_err.clear();
     int rc = check_models(models, n_models);
     if (rc) return rc;
@@ -504,6 +518,7 @@ int jdob_bruteforce(const jdob_model *models, int32_t n_models, const jdob_batch
 
 int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob_batch *b, int32_t mode,
                           const jdob_result *out, void *stream, int64_t *h2d_bytes, int64_t *d2h_bytes) {
+    NvtxRange nvtx_("jdob_solve_batch_host");
     g_err.clear();
     if (!models || n_models < 1) return fail(JDOB_EINVAL, "models");
     for (int i = 0; i < n_models; i++) {
