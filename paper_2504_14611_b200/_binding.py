@@ -64,6 +64,19 @@ class JdobError(RuntimeError):
     pass
 
 
+def _sig(L, name, argtypes, restype=None):
+    """Declare a C-ABI signature.  A library chosen by JDOB_LIB (an older build for an A/B timing) may
+    lack entry points added later: those are skipped there; the in-tree library must export all."""
+    if not hasattr(L, name):
+        if os.environ.get("JDOB_LIB"):
+            return
+        raise ImportError(f"{LIB_PATH} does not export {name}")
+    f = getattr(L, name)
+    f.argtypes = argtypes
+    if restype is not None:
+        f.restype = restype
+
+
 def lib():
     """Load libjdob.so (built in-tree by paper_2504_14611_b200.build)."""
     global _lib
@@ -73,32 +86,19 @@ def lib():
                 raise ImportError(f"libjdob.so not built ({LIB_PATH}); run __graft_entry__.build() "
                                   "or python -m paper_2504_14611_b200.build")
             L = C.CDLL(LIB_PATH)
-            L.jdob_workspace_bytes.argtypes = [_P(JModel), C.c_int32, C.c_int32]
-            L.jdob_workspace_bytes.restype = C.c_size_t
-            L.jdob_solve_batch.argtypes = [_P(JModel), C.c_int32, _P(JBatch), C.c_int32, _P(JResult), C.c_void_p,
-                                           C.c_size_t, C.c_void_p]
-            L.jdob_solve_batch_host.argtypes = [_P(JModel), C.c_int32, _P(JBatch), C.c_int32, _P(JResult),
-                                                C.c_void_p, _P(C.c_int64), _P(C.c_int64)]
-            L.jdob_bruteforce.argtypes = [_P(JModel), C.c_int32, _P(JBatch), C.c_int32, C.c_uint64, C.c_uint64,
-                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
-                                          C.c_void_p]
-            L.jdob_stats.argtypes = [_P(JBatch), _P(JResult), C.c_void_p, C.c_size_t, C.c_void_p]
-            L.jdob_stats_part.argtypes = [_P(JBatch), _P(JResult), C.c_int64, C.c_int32, C.c_int32, C.c_void_p,
-                                          C.c_size_t, C.c_void_p]
-            L.jdob_bf_space_size.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int64]
-            L.jdob_bf_space_size.restype = C.c_uint64
-            L.jdob_eval.argtypes = [_P(JModel), C.c_int32, _P(JBatch), C.c_void_p, C.c_void_p, C.c_void_p,
-                                    C.c_void_p, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
-                                    C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
-            L.jdob_grouped_workspace_bytes.argtypes = [_P(JModel), C.c_int32, C.c_int64, C.c_int64]
-            L.jdob_grouped_workspace_bytes.restype = C.c_size_t
-            L.jdob_solve_grouped.argtypes = [_P(JModel), C.c_int32, _P(JBatch), C.c_int32, _P(JGrouped), C.c_void_p,
-                                             C.c_size_t, C.c_void_p]
-            L.jdob_generate_workspace_bytes.argtypes = [C.c_int64]
-            L.jdob_generate_workspace_bytes.restype = C.c_size_t
-            L.jdob_generate_c5_instances.argtypes = [_P(JGenParams), _P(JBatch), _P(C.c_int64), C.c_void_p,
-                                                     C.c_size_t, C.c_void_p]
-            L.jdob_generate_c5_users.argtypes = [_P(JGenParams), _P(JBatch), C.c_void_p, C.c_size_t, C.c_void_p]
+            _sig(L, "jdob_workspace_bytes", [_P(JModel), C.c_int32, C.c_int32], C.c_size_t)
+            _sig(L, "jdob_solve_batch", [_P(JModel), C.c_int32, _P(JBatch), C.c_int32, _P(JResult), C.c_void_p, C.c_size_t, C.c_void_p])
+            _sig(L, "jdob_solve_batch_host", [_P(JModel), C.c_int32, _P(JBatch), C.c_int32, _P(JResult), C.c_void_p, _P(C.c_int64), _P(C.c_int64)])
+            _sig(L, "jdob_bruteforce", [_P(JModel), C.c_int32, _P(JBatch), C.c_int32, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p])
+            _sig(L, "jdob_stats", [_P(JBatch), _P(JResult), C.c_void_p, C.c_size_t, C.c_void_p])
+            _sig(L, "jdob_stats_part", [_P(JBatch), _P(JResult), C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t, C.c_void_p])
+            _sig(L, "jdob_bf_space_size", [C.c_int32, C.c_int32, C.c_int32, C.c_int64], C.c_uint64)
+            _sig(L, "jdob_eval", [_P(JModel), C.c_int32, _P(JBatch), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p])
+            _sig(L, "jdob_grouped_workspace_bytes", [_P(JModel), C.c_int32, C.c_int64, C.c_int64], C.c_size_t)
+            _sig(L, "jdob_solve_grouped", [_P(JModel), C.c_int32, _P(JBatch), C.c_int32, _P(JGrouped), C.c_void_p, C.c_size_t, C.c_void_p])
+            _sig(L, "jdob_generate_workspace_bytes", [C.c_int64], C.c_size_t)
+            _sig(L, "jdob_generate_c5_instances", [_P(JGenParams), _P(JBatch), _P(C.c_int64), C.c_void_p, C.c_size_t, C.c_void_p])
+            _sig(L, "jdob_generate_c5_users", [_P(JGenParams), _P(JBatch), C.c_void_p, C.c_size_t, C.c_void_p])
             L.jdob_last_error.restype = C.c_char_p
             L.jdob_version.restype = C.c_char_p
             L.jdob_release_pool.restype = C.c_int
