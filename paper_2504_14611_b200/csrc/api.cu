@@ -244,6 +244,8 @@ int jdob_solve_batch(const jdob_model *models, int32_t n_models, const jdob_batc
     if (b->n_inst > 0 && (!out->E || !out->E_lc || !out->t_free_next || !out->f_e || !out->n_tilde || !out->j ||
                           !out->status || !out->mask))
         return fail(JDOB_EINVAL, "result has a NULL required array");
+    if (out->violations && (out->counts || out->work))
+        return fail(JDOB_EINVAL, "violations cannot be combined with the counts/work diagnostics");
     if (out->stats && (out->n_buckets < 1 || out->n_buckets > JDOB_MAX_BUCKETS))
         return fail(JDOB_EINVAL, "n_buckets = %d outside [1, %d]", out->n_buckets, JDOB_MAX_BUCKETS);
     const size_t need = jdob_workspace_bytes(models, n_models, 0);

@@ -161,7 +161,7 @@ __global__ void k_eval(const DevModel *models, DevBatch b, const int *partition,
             const double zvN = b.zeta[u] * vN, f0 = b.f_min[u];
             f = (__fma_rn(f0, T, -zvN) > 0.0) ? f0 : clampf(zvN / T, f0, b.f_max[u]);
             e = ((b.kappa[u] * uN) * f) * f;
-            if ((b.zeta[u] * vN) / f > T + slack * fabs(T)) viol |= 4u;
+            if (d8_violated(b.zeta[u] * vN, f, T + slack * fabs(T))) viol |= 4u;
         }
         if (f_user) f_user[u] = f;
         E = E + e;

@@ -125,6 +125,14 @@ __device__ __forceinline__ double div_lb(double a, double b) {
     return (q > 0.0 && !(__fma_rn(-q, b, a) > 0.0)) ? __longlong_as_double(__double_as_longlong(q) - 1) : q;
 }
 
+// jdob_eval's D8 test RN(zvN / f) > lim, lim = RN(T + slack |T|), f > 0: when lim f - zvN >= 0 exactly
+// (the sign of the correctly rounded fma) the quotient is <= lim, so RN(quotient) <= lim and the test
+// fails without the division; otherwise the literal division decides.
+__device__ __forceinline__ bool d8_violated(double zvN, double f, double lim) {
+    if (__fma_rn(lim, f, -zvN) >= 0.0) return false;
+    return zvN / f > lim;
+}
+
 // Edge grid (R7): f_e(j) = f_e,max - j*rho, one multiply then one subtract.
 __device__ __forceinline__ double grid_fe(double fe_max, double rho, long long j) {
     return __dsub_rn(fe_max, __dmul_rn((double)j, rho));

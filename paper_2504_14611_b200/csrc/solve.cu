@@ -185,7 +185,7 @@ __device__ __forceinline__ void write_bad(const DevResult &r, long long i, long 
 __device__ __forceinline__ unsigned verify_local(const InstRegs &x, double vN, double floc, int M, unsigned vflags,
                                                  double slack, int lane) {
     unsigned vb = (vflags & kVRequire) ? 16u : 0u;
-    if (lane < M && (x.z * vN) / floc > x.T + slack * fabs(x.T)) vb |= 4u;
+    if (lane < M && d8_violated(x.z * vN, floc, x.T + slack * fabs(x.T))) vb |= 4u;
     return __reduce_or_sync(0xffffffffu, vb);
 }
 
@@ -219,7 +219,7 @@ __device__ __forceinline__ void write_local(const DevResult &r, long long i, lon
 // UNI: the instance class this kernel solves.  true = uniform users (Table I; the other instances
 // are marked kStDefer), false = the rest (only instances marked kStDefer by the first kernel).
 // Two specialised kernels keep each one's code, and so its instruction-cache footprint, small.
-template <bool COUNTS, bool PRUNE, bool UNI>
+template <bool COUNTS, bool PRUNE, bool UNI, bool VERIFY>
 __device__ __forceinline__ void solve_instance(long long i, long long off, long long M64, int mid,
                                                const DevModel *models, const DevBatch &b, const DevResult &r,
                                                int mode, SolveSmem &s, int lane) {
@@ -261,7 +261,7 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     for (int t = 0; t < M; t++) E_lc = E_lc + s.et[t].x;  // user-index order
     if (st != JDOB_ST_OK || mode == JDOB_MODE_LC) {
         write_local(r, i, off, M, N, E_lc, t_free, floc, st, lane, true);
-        if (r.viol) {
+        if (VERIFY) {
             const unsigned vb = verify_local(x, vN, floc, M, vflags, r.slack, lane);
             if (lane == 0) r.viol[i] = vb;
         }
@@ -604,7 +604,7 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     const bool offload_wins = (bE < E_lc) || (bE == E_lc && (bN < aN || (bN == aN && bJ < aJ)));
     if (!offload_wins) {
         write_local(r, i, off, M, N, E_lc, t_free, floc, st, lane, false);
-        if (r.viol) {
+        if (VERIFY) {
             const unsigned vb = verify_local(x, vN, floc, M, vflags, r.slack, lane);
             if (lane == 0) r.viol[i] = vb;
         }
@@ -626,13 +626,13 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     const double te = md.phi[bN * B1 + Bo] * inv;
     const bool member = (lane < M) && (s.rank[lane] >= bP);
     double f = floc, arr = t_free;
-    unsigned vbits = 0u;  // the plan re-verified with jdob_eval's formulas (row a11), when r.viol
-    if (r.viol) {
+    unsigned vbits = 0u;  // the plan re-verified with jdob_eval's formulas (row a11)
+    if (VERIFY) {
         if (lane == 0) {
             if (!(fe >= x.fe_min && fe <= fe_max)) vbits |= 32u;
             if (t_free + te > lo_ + r.slack * fabs(lo_)) vbits |= 1u;  // D6: the ASAP start of batch n~ + 1
         }
-        if (!member && lane < M && (x.z * vN) / floc > x.T + r.slack * fabs(x.T)) vbits |= 4u;  // D8
+        if (!member && lane < M && d8_violated(x.z * vN, floc, x.T + r.slack * fabs(x.T))) vbits |= 4u;  // D8
     }
     if (member) {
         const double2 a = (win_direct && uc) ? make_double2(s.uOR[bN], s.uZV[bN])
@@ -643,7 +643,7 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
         const bool low = (a.y == 0.0) || (__fma_rn(t.x, budget, -a.y) > 0.0);
         f = low ? t.x : clampf(a.y / budget, t.x, t.y);
         arr = div_z(a.y, f) + a.x;
-        if (r.viol) {
+        if (VERIFY) {
             // jdob_eval's D20 branches (bit 3 and the f of an infeasible budget) and its D7 finish test
             double fev = f;
             if (a.y == 0.0) {
@@ -652,14 +652,16 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                 vbits |= 8u;
                 fev = t.y;
             }
-            const double fin = (div_z(a.y, fev) + a.x) + te;
+            double fin = arr;  // eval's arrival div_z(zv, f) + O/R: arr unless eval took f_max
+            if (fev != f) fin = div_z(a.y, fev) + a.x;
+            fin = fin + te;
             if (fin > lo_ + r.slack * fabs(lo_)) vbits |= 2u;
         }
         if (arr < t_free) arr = t_free;
     }
     arr = warp_max_nonneg(arr);  // arrivals >= t_free >= 0
     const unsigned mask = __ballot_sync(0xffffffffu, member);
-    if (r.viol) {
+    if (VERIFY) {
         vbits = __reduce_or_sync(0xffffffffu, vbits);
         if (lane == 0) r.viol[i] = vbits;
     }
@@ -685,7 +687,9 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
 #define JDOB_SOLVE_MINB_U 6
 #endif
 
-template <bool COUNTS, bool PRUNE, bool UNI>
+// VERIFY: the instantiation with row a11 in the epilogue (r.viol != NULL); the product kernel without
+// it carries none of that code (K1's speed is sensitive to its code size)
+template <bool COUNTS, bool PRUNE, bool UNI, bool VERIFY>
 __global__ void __launch_bounds__(kSolveWarps * 32, UNI ? JDOB_SOLVE_MINB_U : JDOB_SOLVE_MINB)
     k_solve(const DevModel *models, DevBatch b, DevResult r, int mode) {
     __shared__ SolveSmem smem[kSolveWarps];
@@ -721,7 +725,7 @@ __global__ void __launch_bounds__(kSolveWarps * 32, UNI ? JDOB_SOLVE_MINB_U : JD
 #else
             head(i, o, m, id);
 #endif
-            solve_instance<COUNTS, PRUNE, UNI>(i, co, cm, cid, models, b, r, mode, s, lane);
+            solve_instance<COUNTS, PRUNE, UNI, VERIFY>(i, co, cm, cid, models, b, r, mode, s, lane);
 #ifdef JDOB_NO_PF
             head(i + nw, o, m, id);
 #endif
@@ -736,29 +740,29 @@ __global__ void __launch_bounds__(kSolveWarps * 32, UNI ? JDOB_SOLVE_MINB_U : JD
                 def &= def - 1u;
                 const long long ii2 = base + q, o = b.user_off[ii2];
                 const long long m = (b.user_end ? b.user_end[ii2] : b.user_off[ii2 + 1]) - o;
-                solve_instance<COUNTS, PRUNE, UNI>(ii2, o, m, b.model_id[ii2], models, b, r, mode, s, lane);
+                solve_instance<COUNTS, PRUNE, UNI, VERIFY>(ii2, o, m, b.model_id[ii2], models, b, r, mode, s, lane);
             }
         }
     }
 }
 
-template <bool COUNTS, bool PRUNE, bool UNI>
+template <bool COUNTS, bool PRUNE, bool UNI, bool VERIFY>
 static void launch_solve_t(const DevModel *models, const DevBatch &b, const DevResult &r, int mode, cudaStream_t s,
                            int num_sms) {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve<COUNTS, PRUNE, UNI>, kSolveWarps * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve<COUNTS, PRUNE, UNI, VERIFY>, kSolveWarps * 32, 0);
     if (per_sm < 1) per_sm = 1;
     const long long want = (b.n_inst + kSolveWarps - 1) / kSolveWarps;
     long long grid = (long long)num_sms * per_sm;
     if (want < grid) grid = want;
-    k_solve<COUNTS, PRUNE, UNI><<<(unsigned)grid, kSolveWarps * 32, 0, s>>>(models, b, r, mode);
+    k_solve<COUNTS, PRUNE, UNI, VERIFY><<<(unsigned)grid, kSolveWarps * 32, 0, s>>>(models, b, r, mode);
 }
 
-template <bool COUNTS, bool PRUNE>
+template <bool COUNTS, bool PRUNE, bool VERIFY = false>
 static void launch_pair(const DevModel *models, const DevBatch &b, const DevResult &r, int mode, cudaStream_t s,
                         int num_sms) {
-    launch_solve_t<COUNTS, PRUNE, true>(models, b, r, mode, s, num_sms);   // uniform users; marks the rest
-    launch_solve_t<COUNTS, PRUNE, false>(models, b, r, mode, s, num_sms);  // the rest
+    launch_solve_t<COUNTS, PRUNE, true, VERIFY>(models, b, r, mode, s, num_sms);   // uniform users; marks the rest
+    launch_solve_t<COUNTS, PRUNE, false, VERIFY>(models, b, r, mode, s, num_sms);  // the rest
 }
 
 void launch_solve(const DevModel *models, const DevBatch &b, const DevResult &r, int mode, cudaStream_t s,
@@ -766,6 +770,7 @@ void launch_solve(const DevModel *models, const DevBatch &b, const DevResult &r,
     if (b.n_inst <= 0) return;
     if (r.counts) launch_pair<true, false>(models, b, r, mode, s, num_sms);      // literal counters
     else if (r.work) launch_pair<true, true>(models, b, r, mode, s, num_sms);    // executed counters
+    else if (r.viol) launch_pair<false, true, true>(models, b, r, mode, s, num_sms);  // + row a11 in the epilogue
     else launch_pair<false, true>(models, b, r, mode, s, num_sms);
 }
 
