@@ -1,21 +1,37 @@
 #!/bin/bash
-# Round-2 profiling pass (one B200 under gpurun): bench lines, launch list, ncu --set full of the
-# product kernels with the FP64 instruction counters.  Outputs in $OUT (default gpurun_out/r02p).
+# Round-2 profiling pass (one B200 under gpurun): bench lines (C2 default, C3, C5 device-generated,
+# C3 strong N=2 over gloo), launch list, ncu --set full of K1/K2/K3/K4 with the FP64 instruction
+# counters, compute-sanitizer over tools/sanitize_run.py.  Outputs in $OUT (default gpurun_out/r02p).
 set -x
 OUT=${OUT:-gpurun_out/r02p}
 mkdir -p $OUT
-X="--metrics smsp__sass_thread_inst_executed_op_dadd_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,smsp__sass_thread_inst_executed_op_fp64_pred_on.sum,sm__sass_thread_inst_executed_op_fp64_pred_on.sum,smsp__inst_executed_pipe_fp64.sum,sm__inst_executed_pipe_fp64.sum"
+X="--metrics smsp__sass_thread_inst_executed_op_fp64_pred_on.sum,smsp__inst_executed_pipe_fp64.sum"
 python __graft_entry__.py > $OUT/build.log 2>&1
-[ -z "$NOBENCH" ] && python bench.py > $OUT/bench_default.jsonl 2> $OUT/bench_default.err
-[ -n "$C5" ] && python bench.py --workload c5 --no-bf > $OUT/bench_c5.jsonl 2> $OUT/bench_c5.err
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/gpu.txt
+lscpu > $OUT/cpu.txt
+python bench.py > $OUT/bench_c2.jsonl 2> $OUT/bench_c2.err
+python bench.py --workload c3 --no-bf > $OUT/bench_c3.jsonl 2> $OUT/bench_c3.err
+python bench.py --workload c5 --scaling strong --no-bf > $OUT/bench_c5.jsonl 2> $OUT/bench_c5.err
+JDOB_BENCH_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
+    --master-port 29517 bench.py --gpus 2 --no-cpu > $OUT/bench_c2_n2_gloo.jsonl 2> $OUT/bench_c2_n2_gloo.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
     python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --bf-reps 1 > $OUT/launches_bench.log 2>&1
 timeout 900 ncu --set full $X --clock-control none --import-source on --kernel-name-base mangled \
-    -k regex:k_solveILb0ELb1ELb1E -c 1 -o $OUT/prof_solve -f \
+    -k regex:k_solveILb0ELb1ELb1ELb0E -c 1 -o $OUT/prof_solve -f \
     python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-bf > $OUT/prof_solve.log 2>&1
+timeout 900 ncu --set full $X --clock-control none --import-source on --kernel-name-base mangled \
+    -k regex:k_solveILb0ELb1ELb1ELb0E -c 1 -o $OUT/prof_solve_c5 -f \
+    python bench.py --workload c5 --n-inst 1000000 --steps 1 --warmup 1 --no-e2e --no-cpu --no-bf > $OUT/prof_solve_c5.log 2>&1
 timeout 900 ncu --set full $X --clock-control none --import-source on --kernel-name-base mangled \
     -k regex:k_bf_mainILi8ELb1ELb0E -c 1 -o $OUT/prof_bf -f \
     python tools/profile_bf.py 1.0 > $OUT/prof_bf.log 2>&1
-[ -n "$EVAL" ] && timeout 600 ncu --set full $X --clock-control none --import-source on -k regex:k_eval -c 1 -o $OUT/prof_eval -f \
+timeout 600 ncu --set full $X --clock-control none --import-source on -k regex:k_eval -c 1 -o $OUT/prof_eval -f \
     python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --no-bf > $OUT/prof_eval.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_stats_partial -c 1 -o $OUT/prof_stats -f \
+    python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --no-bf > $OUT/prof_stats.log 2>&1
+if [ -z "$NOSAN" ]; then
+for tool in memcheck racecheck synccheck initcheck; do
+    timeout 900 compute-sanitizer --tool $tool python tools/sanitize_run.py > $OUT/sanitize_$tool.txt 2>&1
+done
+fi
 ls -la $OUT

@@ -32,6 +32,18 @@ J.solve_batch(J.DeviceBatch(lb), partition=True)
 J.solve_batch(J.DeviceBatch(lb), counts=True, partition=True)
 r5 = G.random_batch(seed=21, n_inst=1, M_lo=5, M_hi=5, N_lo=3, N_hi=3, k_max=20)
 J.bruteforce(J.DeviceBatch(r5), 0)
+J.solve_batch(db, verify=True, slack=1e-9)           # row a11 in K1's epilogue
+J.bruteforce(J.DeviceBatch(r5), 0, work=True)        # K2 counting instantiation
+dc = J.DeviceBatch(c)
+rc = J.solve_batch(dc)
+for P in (1, 2, 4):                                  # statistics subtrees (jdob_stats_part)
+    for r in range(P):
+        lo, hi = r * 64 // P, (r + 1) * 64 // P
+        part = J.DeviceBatch(G.config_batch("c3", n_inst=hi - lo, inst_begin=lo))
+        J.stats(part, J.solve_batch(part), n_buckets=3, part=(64, P, r))
+models, params = G.c5_device_inputs(inst_begin=1000)  # K6 device generator
+g5 = J.DeviceBatch.generate_c5(models, params, 3000)
+J.solve_batch(g5, stats=True, n_buckets=15)
 hb = J.HostBuffers(c, stats=True, n_buckets=3)
 J.solve_batch_host(hb)
 torch.cuda.synchronize()
