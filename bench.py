@@ -403,7 +403,7 @@ def run_mine(args):
     if devgen:   # each rank generates its own instances on the device: no input traffic
         models, params = G.c5_device_inputs(inst_begin=lo)
         db = J.DeviceBatch.generate_c5(models, params, n)
-        batch = DevGenView(db, models, lo, dict(config="c5", n_buckets=15))
+        batch = DevGenView(db, models, lo, dict(config="c5", n_buckets=480))
     else:
         batch = G.config_batch(args.workload, n_inst=n, inst_begin=lo)
         db = J.DeviceBatch(batch)
@@ -500,7 +500,10 @@ def run_mine(args):
     if devgen:
         e2e = {"skipped": "device-generated workload: no host inputs (use --host-gen for the host-buffer API)"}
     elif not args.no_e2e:
-        hb = J.HostBuffers(batch, stats=True, n_buckets=n_buckets)
+        # users sharing their device parameters within an instance (Table I; all of C2/C3/C5) go through
+        # jdob_solve_shared_host, the others through jdob_solve_batch_host
+        shared = J.shared_params(batch) is not None
+        hb = J.HostBuffers(batch, stats=True, n_buckets=n_buckets, shared=shared)
         J.solve_batch_host(hb)
         reps = max(1, min(K, 3))
         if dist:
@@ -518,7 +521,9 @@ def run_mine(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         e2e = {"value": n_total * reps / (ms / 1e3), "unit": "instances/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "api": "jdob_solve_batch_host (pinned host buffers)", "reps": reps}
+               "d2h_bytes_per_step": int(d2h), "reps": reps,
+               "api": ("jdob_solve_shared_host (pinned host buffers; users' shared device parameters once per "
+                       "instance, expanded on the device)" if shared else "jdob_solve_batch_host (pinned host buffers)")}
         del hb
         # copy roof: one plain pinned host -> device copy of the same number of bytes (no kernels)
         hx = torch.empty(int(h2d), dtype=torch.uint8).pin_memory()

@@ -46,7 +46,7 @@ extern "C" {
 #define JDOB_MAX_N 63          /* sub-tasks per DNN (N)                        */
 #define JDOB_MAX_K 65536       /* edge-frequency grid points per instance (k) */
 #define JDOB_STATS_FIELDS 80   /* doubles per statistics bucket (a12)               */
-#define JDOB_MAX_BUCKETS 64
+#define JDOB_MAX_BUCKETS 512   /* (M, regime, model) of C5: 32 x 5 x 3 = 480 */
 
 /* call-level return codes */
 enum { JDOB_OK = 0, JDOB_EINVAL = 1, JDOB_ETOOBIG = 2, JDOB_ECUDA = 3 };
@@ -239,6 +239,33 @@ JDOB_API int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, c
                           const jdob_result *out, void *stream, int64_t *h2d_bytes, int64_t *d2h_bytes);
 
 /*
+ * A batch whose users share their device parameters within each instance -- identical devices, the
+ * setting of every experiment of the paper (Table I), where only the deadlines differ --
+ * given with one copy of (zeta, kappa, f_min, f_max, R, p_u) per INSTANCE and T per user.  HOST
+ * pointers (jdob_solve_shared_host).  Same meaning as jdob_batch otherwise.
+ */
+typedef struct {
+    int64_t n_inst;
+    int32_t n_models;
+    const int32_t *model_id;
+    const int64_t *user_off;
+    const double *zeta, *kappa, *f_min, *f_max, *R, *p_u;  /* [n_inst]: the instance's users' values */
+    const double *T;                                        /* [user_off[n_inst]] */
+    const double *t_free, *fe_min, *fe_max, *rho;           /* [n_inst] */
+    const int32_t *bucket;
+} jdob_shared_batch;
+
+/*
+ * jdob_solve_batch_host for a jdob_shared_batch: the same computation and outputs (bit-identical to
+ * jdob_solve_batch_host on the equivalent per-user arrays); a chunk's users are expanded on the device
+ * from the instances' values (one small kernel), so the host->device traffic is 8 B per user + 48 B per
+ * instance for the user parameters instead of 56 B per user.  Errors: as jdob_solve_batch_host.
+ */
+JDOB_API int jdob_solve_shared_host(const jdob_model *models, int32_t n_models, const jdob_shared_batch *b,
+                                    int32_t mode, const jdob_result *out, void *stream, int64_t *h2d_bytes,
+                                    int64_t *d2h_bytes);
+
+/*
  * Release the device memory the library's private pool keeps between jdob_solve_batch_host
  * calls (cudaMemPoolTrimTo(pool, 0) on every device the library has used).  Host call; safe
  * when no jdob_solve_batch_host call is in flight.  Returns JDOB_OK or JDOB_ECUDA.
@@ -369,7 +396,7 @@ JDOB_API size_t jdob_generate_workspace_bytes(int64_t n_inst);
 /*
  * Generator phase 1: writes b->model_id, user_off [n_inst + 1], t_free, fe_min, fe_max, rho and
  * bucket (model * 5 + regime) of instances [p->inst_begin, p->inst_begin + b->n_inst) (DEVICE arrays
- * of `b`, caller-allocated), and the total user count user_off[n_inst] to the HOST *n_users (one
+ * of `b`, caller-allocated; bucket = (model * 5 + regime) * 32 + M - 1), and the total user count user_off[n_inst] to the HOST *n_users (one
  * synchronous 8-byte read on `stream`), so the caller can size the user arrays.
  * Errors: JDOB_EINVAL (NULL arrays or n_users, small workspace), JDOB_ECUDA.
  */

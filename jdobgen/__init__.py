@@ -356,9 +356,10 @@ def config_c5(n_inst: int = 10_000_000, seed: int = 5, inst_begin: int = 0, hete
     users["T"] = (1.0 + beta) * lat
     inst = dict(t_free=np.zeros(n_inst), fe_min=np.full(n_inst, TABLE_I["fe_min"]),
                 fe_max=np.full(n_inst, TABLE_I["fe_max"]), rho=rho)
-    bucket = (mid * 5 + regime).astype(np.int32)
+    # statistics buckets by (model, deadline regime, M) -- SURVEY §8(a) a12: 3 x 5 x 32 = 480
+    bucket = ((mid * 5 + regime) * 32 + (Ms - 1)).astype(np.int32)
     return _batch_from_lists(models, mid.astype(np.int32), Ms, users, inst, bucket=bucket,
-                             inst_base=inst_begin, meta=dict(config="c5", seed=seed, n_buckets=15))
+                             inst_base=inst_begin, meta=dict(config="c5", seed=seed, n_buckets=480))
 
 
 def c5_device_inputs(seed: int = 5, inst_begin: int = 0, hetero: bool = False):

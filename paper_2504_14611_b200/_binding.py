@@ -51,6 +51,12 @@ class JGenParams(C.Structure):
                [("rho", C.c_double * 3), ("lat", C.c_double * 3)]
 
 
+class JSharedBatch(C.Structure):
+    _fields_ = [("n_inst", C.c_int64), ("n_models", C.c_int32), ("model_id", C.c_void_p), ("user_off", C.c_void_p)] + \
+               [(f, C.c_void_p) for f in ("zeta", "kappa", "f_min", "f_max", "R", "p_u", "T",
+                                          "t_free", "fe_min", "fe_max", "rho", "bucket")]
+
+
 class JGrouped(C.Structure):
     _fields_ = [(f, C.c_void_p) for f in ("E", "t_free_next", "n_groups", "status", "group_of", "partition", "f_user",
                                           "group_fe")]
@@ -96,6 +102,8 @@ def lib():
             _sig(L, "jdob_eval", [_P(JModel), C.c_int32, _P(JBatch), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p])
             _sig(L, "jdob_grouped_workspace_bytes", [_P(JModel), C.c_int32, C.c_int64, C.c_int64], C.c_size_t)
             _sig(L, "jdob_solve_grouped", [_P(JModel), C.c_int32, _P(JBatch), C.c_int32, _P(JGrouped), C.c_void_p, C.c_size_t, C.c_void_p])
+            _sig(L, "jdob_solve_shared_host", [_P(JModel), C.c_int32, _P(JSharedBatch), C.c_int32, _P(JResult),
+                                               C.c_void_p, _P(C.c_int64), _P(C.c_int64)])
             _sig(L, "jdob_generate_workspace_bytes", [C.c_int64], C.c_size_t)
             _sig(L, "jdob_generate_c5_instances", [_P(JGenParams), _P(JBatch), _P(C.c_int64), C.c_void_p, C.c_size_t, C.c_void_p])
             _sig(L, "jdob_generate_c5_users", [_P(JGenParams), _P(JBatch), C.c_void_p, C.c_size_t, C.c_void_p])
@@ -109,7 +117,8 @@ def lib():
 EXPORTED = ("jdob_workspace_bytes", "jdob_solve_batch", "jdob_solve_batch_host", "jdob_bruteforce",
             "jdob_bf_space_size", "jdob_eval", "jdob_grouped_workspace_bytes", "jdob_solve_grouped",
             "jdob_last_error", "jdob_version", "jdob_release_pool", "jdob_stats", "jdob_stats_part",
-            "jdob_generate_workspace_bytes", "jdob_generate_c5_instances", "jdob_generate_c5_users")
+            "jdob_generate_workspace_bytes", "jdob_generate_c5_instances", "jdob_generate_c5_users",
+            "jdob_solve_shared_host")
 
 
 def _check(rc):
@@ -183,7 +192,7 @@ class DeviceBatch:
         self.jmodels = (JModel * len(ms))(*ms)
 
     @classmethod
-    def generate_c5(cls, models, params: dict, n_inst: int, device=None, n_buckets: int = 15, stream=None):
+    def generate_c5(cls, models, params: dict, n_inst: int, device=None, n_buckets: int = 480, stream=None):
         """The C5 workload generated on the device (jdob_generate_c5_*; input plumbing, bit-identical
         to jdobgen.config_c5): `models` and `params` (the jdob_gen_params fields) come from the caller,
         e.g. jdobgen.c5_device_inputs.  No host->device traffic but the model tables."""
@@ -368,10 +377,29 @@ def bruteforce(db: DeviceBatch, space: int, idx_begin: int = 0, idx_end: Optiona
     return (E, I, S, W) if work else (E, I, S)
 
 
-class HostBuffers:
-    """Pinned host copies of a batch and its outputs for the end-to-end call."""
+def shared_params(batch):
+    """Per-instance (zeta, kappa, f_min, f_max, R, p_u) when every instance's users share them bit for bit
+    (jdob_shared_batch), else None."""
+    off = np.asarray(batch.user_off, np.int64)
+    first = off[:-1]
+    M = np.diff(off)
+    if len(first) == 0 or (M < 1).any():
+        return None
+    out = {}
+    for f in ("zeta", "kappa", "f_min", "f_max", "R", "p_u"):
+        a = np.asarray(getattr(batch, f), np.float64)
+        v = a[first]
+        if not np.array_equal(a.view(np.int64), np.repeat(v, M).view(np.int64)):
+            return None
+        out[f] = v
+    return out
 
-    def __init__(self, batch, f_user=False, stats=False, n_buckets=None, partition=False):
+
+class HostBuffers:
+    """Pinned host copies of a batch and its outputs for the end-to-end call.  shared=True stores the
+    users' device parameters once per instance (jdob_shared_batch; the batch's users must share them)."""
+
+    def __init__(self, batch, f_user=False, stats=False, n_buckets=None, partition=False, shared=False):
         torch = _torch()
 
         def pin(a, dtype):
@@ -387,13 +415,18 @@ class HostBuffers:
         n = len(batch.model_id)
         self.n_inst = n
         self.t = {"model_id": pin(batch.model_id, np.int32), "user_off": pin(batch.user_off, np.int64)}
+        self.shared = bool(shared)
+        sp = shared_params(batch) if shared else None
+        if shared and sp is None:
+            raise ValueError("shared=True needs users that share their parameters within each instance")
         for f in DeviceBatch.USER + DeviceBatch.INST:
-            self.t[f] = pin(getattr(batch, f), np.float64)
+            self.t[f] = pin(sp[f] if (sp is not None and f in sp) else getattr(batch, f), np.float64)
         bucket = getattr(batch, "bucket", None)
         self.t["bucket"] = None if bucket is None else pin(bucket, np.int32)
-        self.jbatch = JBatch(n, self.n_models, *[_ptr(self.t[f]) for f in
-                                                  ("model_id", "user_off") + DeviceBatch.USER + DeviceBatch.INST +
-                                                  ("bucket",)])
+        cls = JSharedBatch if shared else JBatch
+        self.jbatch = cls(n, self.n_models, *[_ptr(self.t[f]) for f in
+                                               ("model_id", "user_off") + DeviceBatch.USER + DeviceBatch.INST +
+                                               ("bucket",)])
         nu = int(batch.user_off[-1])
         z = lambda k, dt: torch.empty(k, dtype=dt).pin_memory()
         self.out = dict(E=z(n, torch.float64), E_lc=z(n, torch.float64), t_free_next=z(n, torch.float64),
@@ -406,7 +439,8 @@ class HostBuffers:
 
 
 def solve_batch_host(hb: HostBuffers, mode: int = MODE_FULL, stream=None):
-    """jdob_solve_batch_host: host buffers in, host buffers out (copies inside the call).
+    """jdob_solve_batch_host (jdob_solve_shared_host for shared HostBuffers): host buffers in, host buffers
+    out (copies inside the call).
 
     Returns (h2d_bytes, d2h_bytes)."""
     o = hb.out
@@ -414,8 +448,9 @@ def solve_batch_host(hb: HostBuffers, mode: int = MODE_FULL, stream=None):
                                            "f_user", "counts", "stats")], hb.n_buckets, _ptr(o.get("partition")), None)
     h2d = C.c_int64()
     d2h = C.c_int64()
-    _check(lib().jdob_solve_batch_host(hb.jmodels, hb.n_models, C.byref(hb.jbatch), int(mode), C.byref(r),
-                                       _stream_handle(stream), C.byref(h2d), C.byref(d2h)))
+    fn = lib().jdob_solve_shared_host if hb.shared else lib().jdob_solve_batch_host
+    _check(fn(hb.jmodels, hb.n_models, C.byref(hb.jbatch), int(mode), C.byref(r), _stream_handle(stream),
+              C.byref(h2d), C.byref(d2h)))
     return h2d.value, d2h.value
 
 

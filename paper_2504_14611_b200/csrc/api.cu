@@ -46,7 +46,7 @@ static size_t model_table_bytes(const jdob_model &m) {
 }
 
 static size_t stats_partial_bytes() {
-    return al((size_t)kStatsBlocks * JDOB_MAX_BUCKETS * kStatsF * sizeof(double));
+    return al((size_t)kStatsBlocks * 64 * kStatsF * sizeof(double));  // one group of 64 buckets (stats.cu)
 }
 
 static int check_models(const jdob_model *models, int32_t n_models) {
@@ -518,10 +518,51 @@ int jdob_bruteforce(const jdob_model *models, int32_t n_models, const jdob_batch
     return cuda_check("bruteforce");
 }
 
-int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob_batch *b, int32_t mode,
-                          const jdob_result *out, void *stream, int64_t *h2d_bytes, int64_t *d2h_bytes) {
-    NvtxRange nvtx_("jdob_solve_batch_host");
-    g_err.clear();
+}  // extern "C"
+
+// Users of one instance given with shared device parameters (jdob_shared_batch): expanded, per chunk,
+// into the struct-of-arrays layout the kernels read (one warp per instance, lane = user).
+__global__ void k_expand_shared(long long n, const long long *user_off, const double *z, const double *k,
+                                const double *f0, const double *f1, const double *R, const double *p, double *uz,
+                                double *uk, double *uf0, double *uf1, double *uR, double *up) {
+    const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    const long long o = user_off[i], e = user_off[i + 1];
+    for (long long u = o + lane; u < e; u += 32) {
+        uz[u] = z[i];
+        uk[u] = k[i];
+        uf0[u] = f0[i];
+        uf1[u] = f1[i];
+        uR[u] = R[i];
+        up[u] = p[i];
+    }
+}
+
+// jdob_solve_batch_host and jdob_solve_shared_host: exactly one of b (users as arrays) and sb (users
+// sharing their device parameters within an instance) is given
+static int solve_host_impl(const jdob_model *models, int32_t n_models, const jdob_batch *b_full,
+                           const jdob_shared_batch *sb, int32_t mode, const jdob_result *out, void *stream,
+                           int64_t *h2d_bytes, int64_t *d2h_bytes) {
+    // the instance-level fields of either form, in a jdob_batch (user arrays: T only for sb)
+    jdob_batch bv;
+    if (b_full) {
+        bv = *b_full;
+    } else {
+        bv.n_inst = sb->n_inst;
+        bv.n_models = sb->n_models;
+        bv.model_id = sb->model_id;
+        bv.user_off = sb->user_off;
+        bv.zeta = bv.kappa = bv.f_min = bv.f_max = bv.R = bv.p_u = sb->T;  // placeholders: not copied
+        bv.T = sb->T;
+        bv.t_free = sb->t_free;
+        bv.fe_min = sb->fe_min;
+        bv.fe_max = sb->fe_max;
+        bv.rho = sb->rho;
+        bv.bucket = sb->bucket;
+    }
+    const jdob_batch *b = &bv;
+    const bool shared = (sb != nullptr);
     if (!models || n_models < 1) return fail(JDOB_EINVAL, "models");
     for (int i = 0; i < n_models; i++) {
         if (models[i].N < 1 || models[i].N > JDOB_MAX_N || models[i].B_max < 1 ||
@@ -532,6 +573,8 @@ int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob
     }
     int rc = check_batch(b, n_models);
     if (rc) return rc;
+    if (shared && b->n_inst > 0 && (!sb->zeta || !sb->kappa || !sb->f_min || !sb->f_max || !sb->R || !sb->p_u))
+        return fail(JDOB_EINVAL, "shared batch has a NULL parameter array");
     if (!out || !out->E || !out->E_lc || !out->t_free_next || !out->f_e || !out->n_tilde || !out->j ||
         !out->status || !out->mask)
         return fail(JDOB_EINVAL, "result has a NULL required array");
@@ -554,7 +597,7 @@ int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob
         bytes += 4 * al(n1 * 8) + 2 * al(n1 * b1 * 8);
     }
     const size_t in_inst = al(n * 4) + al((n + 1) * 8) + 4 * al(n * 8) + (b->bucket ? al(n * 4) : 0);
-    const size_t in_user = 7 * al(nu * 8);
+    const size_t in_user = 7 * al(nu * 8) + (shared ? 6 * al(n * 8) : 0);
     const size_t outb = 4 * al(n * 8) + 4 * al(n * 4) + (out->f_user ? al(nu * 8) : 0) +
                         (out->partition ? al(nu * 4) : 0) +
                         (out->counts ? al(n * 3 * 8) : 0) +
@@ -605,6 +648,15 @@ int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob
     const double *ih[4] = {b->t_free, b->fe_min, b->fe_max, b->rho};
     for (int t = 0; t < 4; t++) *inf[t] = (const double *)take(n * 8);
     db.bucket = b->bucket ? (const int32_t *)take(n * 4) : nullptr;
+    double *sh_dev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // shared parameters [n]
+    const double *sh_host[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    if (shared) {
+        const double *hs[6] = {sb->zeta, sb->kappa, sb->f_min, sb->f_max, sb->R, sb->p_u};
+        for (int t = 0; t < 6; t++) {
+            sh_dev[t] = (double *)take(n * 8);
+            sh_host[t] = hs[t];
+        }
+    }
     jdob_result dr = *out;
     dr.E = (double *)take(n * 8);
     dr.E_lc = (double *)take(n * 8);
@@ -676,9 +728,19 @@ int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob
         h2(db.model_id + i0, b->model_id + i0, (i1 - i0) * 4);
         // user_off[i0..i1] (the shared boundary element is written with identical bytes by both chunks)
         h2(db.user_off + i0, b->user_off + i0, (i1 - i0 + 1) * 8);
-        for (int t = 0; t < 7; t++) h2(*uf[t] + u0, uh[t] + u0, (u1 - u0) * 8);
+        if (!shared) {
+            for (int t = 0; t < 7; t++) h2(*uf[t] + u0, uh[t] + u0, (u1 - u0) * 8);
+        } else {
+            h2(db.T + u0, b->T + u0, (u1 - u0) * 8);
+            for (int t = 0; t < 6; t++) h2(sh_dev[t] + i0, sh_host[t] + i0, (i1 - i0) * 8);
+        }
         for (int t = 0; t < 4; t++) h2(*inf[t] + i0, ih[t] + i0, (i1 - i0) * 8);
         if (b->bucket) h2(db.bucket + i0, b->bucket + i0, (i1 - i0) * 4);
+        if (shared)  // the users' arrays of this chunk from the instances' shared values
+            k_expand_shared<<<(unsigned)(((i1 - i0) * 32 + 255) / 256), 256, 0, ss>>>(
+                i1 - i0, (const long long *)db.user_off + i0, sh_dev[0] + i0, sh_dev[1] + i0, sh_dev[2] + i0,
+                sh_dev[3] + i0, sh_dev[4] + i0, sh_dev[5] + i0, (double *)db.zeta, (double *)db.kappa,
+                (double *)db.f_min, (double *)db.f_max, (double *)db.R, (double *)db.p_u);
         jdob_batch cb = db;
         cb.n_inst = i1 - i0;
         cb.model_id = db.model_id + i0;
@@ -753,6 +815,24 @@ int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob
     if (h2d_bytes) *h2d_bytes = h2d;
     if (d2h_bytes) *d2h_bytes = d2h;
     return JDOB_OK;
+}
+
+extern "C" {
+
+int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob_batch *b, int32_t mode,
+                          const jdob_result *out, void *stream, int64_t *h2d_bytes, int64_t *d2h_bytes) {
+    NvtxRange nvtx_("jdob_solve_batch_host");
+    g_err.clear();
+    if (!b) return fail(JDOB_EINVAL, "batch is NULL");
+    return solve_host_impl(models, n_models, b, nullptr, mode, out, stream, h2d_bytes, d2h_bytes);
+}
+
+int jdob_solve_shared_host(const jdob_model *models, int32_t n_models, const jdob_shared_batch *b, int32_t mode,
+                           const jdob_result *out, void *stream, int64_t *h2d_bytes, int64_t *d2h_bytes) {
+    NvtxRange nvtx_("jdob_solve_shared_host");
+    g_err.clear();
+    if (!b) return fail(JDOB_EINVAL, "batch is NULL");
+    return solve_host_impl(models, n_models, nullptr, b, mode, out, stream, h2d_bytes, d2h_bytes);
 }
 
 }  // extern "C"

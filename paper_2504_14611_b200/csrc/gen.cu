@@ -52,7 +52,7 @@ __global__ void k_gen_inst(GenParams p, long long n, int *model_id, long long *u
     fe_min[i] = p.fe_min;
     fe_max[i] = p.fe_max;
     rho[i] = p.rho[rc];
-    bucket[i] = mid * 5 + reg;
+    bucket[i] = (mid * 5 + reg) * 32 + (int)(M - 1);  // (model, regime, M): 480 buckets
     regime[i] = reg;
 }
 

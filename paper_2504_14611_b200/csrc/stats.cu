@@ -35,8 +35,13 @@ __device__ __forceinline__ int lane_slot(int f) {  // field -> per-lane slot, -1
 // range and accumulates them IN THAT ORDER into its own shared-memory slots (no shuffles, no atomics on
 // floating point); integer counters use shared-memory integer atomics (exact, order-free).  The lanes
 // are then folded in lane order, so the result is identical run to run.
+// One pass accumulates the buckets [b_lo, b_lo + n_buckets) of n_all (at most kBucketGroup, the shared
+// memory of one warp); more buckets take one pass per group over the same instances.
+constexpr int kBucketGroup = 64;
+
 __global__ void __launch_bounds__(32) k_stats_partial(DevBatch b, DevResult r, double *partials, int n_buckets,
-                                                      long long n_total, long long begin, long long w0) {
+                                                      long long n_total, long long begin, long long w0, int b_lo,
+                                                      int n_all) {
     // leaf w of the global tree = instances [n_total w / W, n_total (w + 1) / W); this block is w0 + blockIdx.x
     extern __shared__ double sh[];
     double *fs = sh;                                                        // [n_buckets][kLaneF][32]
@@ -64,8 +69,9 @@ __global__ void __launch_bounds__(32) k_stats_partial(DevBatch b, DevResult r, d
             bq[q] = -1;
             if (ii < i1) {
                 Mq[q] = (int)(b.user_off[ii + 1] - b.user_off[ii]);
-                // default bucket M - 1; instances with M > n_buckets are not counted
-                bq[q] = b.bucket ? b.bucket[ii] : ((Mq[q] >= 1 && Mq[q] <= n_buckets) ? Mq[q] - 1 : -1);
+                // default bucket M - 1; instances with M > n_all are not counted; local index in the group
+                const int bg = b.bucket ? b.bucket[ii] : ((Mq[q] >= 1 && Mq[q] <= n_all) ? Mq[q] - 1 : -1);
+                bq[q] = (bg >= 0 && bg < n_all) ? bg - b_lo : -1;
                 sq[q] = r.status[ii];
                 Eq[q] = r.E[ii];
                 Lq[q] = r.E_lc[ii];
@@ -148,12 +154,15 @@ bool launch_stats(const DevBatch &b, const DevResult &r, double *partials, doubl
     const long long begin = n_total * part / parts, end = n_total * (part + 1) / parts;
     if (b.n_inst != end - begin) return false;
     const long long nl = W / parts, w0 = nl * part;  // leaf w0 starts at n_total w0 / W = begin
-    const size_t smem = (size_t)n_buckets * kLaneF * 32 * sizeof(double) + (size_t)n_buckets * kStatsF * sizeof(int);
     cudaFuncSetAttribute(k_stats_partial, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)((size_t)JDOB_MAX_BUCKETS * (kLaneF * 32 * sizeof(double) + kStatsF * sizeof(int))));
-    k_stats_partial<<<(unsigned)nl, 32, smem, s>>>(b, r, partials, n_buckets, n_total, begin, w0);
-    const int warps = n_buckets * kStatsF;
-    k_stats_final<<<(warps * 32 + 255) / 256, 256, 0, s>>>(partials, (int)nl, n_buckets, stats);
+                         (int)((size_t)kBucketGroup * (kLaneF * 32 * sizeof(double) + kStatsF * sizeof(int))));
+    for (int b_lo = 0; b_lo < n_buckets; b_lo += kBucketGroup) {  // partials reused group after group
+        const int nb = (n_buckets - b_lo < kBucketGroup) ? n_buckets - b_lo : kBucketGroup;
+        const size_t smem = (size_t)nb * kLaneF * 32 * sizeof(double) + (size_t)nb * kStatsF * sizeof(int);
+        k_stats_partial<<<(unsigned)nl, 32, smem, s>>>(b, r, partials, nb, n_total, begin, w0, b_lo, n_buckets);
+        const int warps = nb * kStatsF;
+        k_stats_final<<<(warps * 32 + 255) / 256, 256, 0, s>>>(partials, (int)nl, nb, stats + (size_t)b_lo * kStatsF);
+    }
     return true;
 }
 

@@ -25,7 +25,7 @@ def declared_symbols():
 
 def test_header_symbols_exported(L):
     syms = declared_symbols()
-    assert len(syms) == 16, syms
+    assert len(syms) == 17, syms
     assert set(syms) == set(__import__("paper_2504_14611_b200").EXPORTED), syms
     for s in syms:
         assert hasattr(L, s), s
@@ -97,7 +97,8 @@ def test_struct_layouts_match_header(tmp_path):
     if cc is None:
         pytest.skip("no C compiler")
     structs = {"jdob_model": B.JModel, "jdob_batch": B.JBatch, "jdob_result": B.JResult,
-               "jdob_grouped_result": B.JGrouped, "jdob_gen_params": B.JGenParams}
+               "jdob_grouped_result": B.JGrouped, "jdob_gen_params": B.JGenParams,
+               "jdob_shared_batch": B.JSharedBatch}
     lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "jdob.h"', "int main(void) {"]
     for cname, py in structs.items():
         lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')

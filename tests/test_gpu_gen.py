@@ -38,7 +38,7 @@ def test_c5_device_generated_prefix_vs_oracle(J):
     models, params = g.c5_device_inputs()
     db = J.DeviceBatch.generate_c5(models, params, n)
     res = J.solve_batch(db, f_user=False)
-    st = J.stats(db, res, n_buckets=15)
+    st = J.stats(db, res, n_buckets=480)
     gpu = to_np({k: v[:pre] for k, v in res.items() if k in ("E", "E_lc", "t_free_next", "f_e", "n_tilde", "j",
                                                                "status", "mask")})
     host = g.config_c5(n_inst=pre)

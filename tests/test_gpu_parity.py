@@ -339,6 +339,24 @@ def test_host_api_chunked_pipeline(J):
     assert_bits_equal(host["stats"].reshape(3, -1), gpu["stats"], "stats")
 
 
+@pytest.mark.parametrize("cfg,n", [("c2", 300_000), ("c3", 50_000), ("c5", 40_000)])
+def test_shared_host_api_equals_full(J, cfg, n):
+    """jdob_solve_shared_host (users' device parameters once per instance, expanded on the device)
+    returns the bits of jdob_solve_batch_host on the per-user arrays, with fewer bytes copied in."""
+    b = g.config_batch(cfg, n_inst=n)
+    nb = int(b.meta.get("n_buckets", 32))
+    full = J.HostBuffers(b, f_user=True, stats=True, n_buckets=nb)
+    h_full, _ = J.solve_batch_host(full)
+    sh = J.HostBuffers(b, f_user=True, stats=True, n_buckets=nb, shared=True)
+    h_sh, _ = J.solve_batch_host(sh)
+    assert h_sh < h_full
+    for f in ("E", "E_lc", "t_free_next", "f_e", "n_tilde", "j", "status", "mask", "f_user", "stats"):
+        assert_bits_equal(sh.out[f].numpy().reshape(-1), full.out[f].numpy().reshape(-1), f)
+    het = g.random_batch(seed=143, n_inst=50, M_lo=2, M_hi=8, N_hi=5, k_max=20, equal_gamma_frac=0.0)
+    with pytest.raises(ValueError):
+        J.HostBuffers(het, shared=True)
+
+
 # ------------------------------- brute force -------------------------------------
 @pytest.mark.parametrize("toy", ["toy-1", "toy-2", "toy-2-m1", "toy-2-tfree", "toy-4"])
 @pytest.mark.parametrize("space", [0, 1])

@@ -43,7 +43,7 @@ for P in (1, 2, 4):                                  # statistics subtrees (jdob
         J.stats(part, J.solve_batch(part), n_buckets=3, part=(64, P, r))
 models, params = G.c5_device_inputs(inst_begin=1000)  # K6 device generator
 g5 = J.DeviceBatch.generate_c5(models, params, 3000)
-J.solve_batch(g5, stats=True, n_buckets=15)
+J.solve_batch(g5, stats=True, n_buckets=480)
 hb = J.HostBuffers(c, stats=True, n_buckets=3)
 J.solve_batch_host(hb)
 torch.cuda.synchronize()
