@@ -333,8 +333,14 @@ def bf_leg(J, torch, world, rank, reps, dist, peak_gops, with_cpu, cpu_seconds):
             "peak_note": PEAK_NOTE + "; literal = SURVEY §8(d) per-candidate work over all candidates / "
                          "the kernel's time (> 1 is the pruning's signature); executed = the work the "
                          "pruned scan ran, from its counters (bench.py bf_executed_ops)"}
-    roof["achieved"] = roof["executed"]["achieved"]
-    roof["frac"] = roof["executed"]["frac"]
+    if hw and hw.get("fp64_thread_inst"):   # the FP64 lane instructions ncu counted for this launch
+        a_ = hw["fp64_thread_inst"] / (km / 1e3) / 1e9
+        roof["ncu_executed"] = {"fp64_lane_instructions_per_launch": hw["fp64_thread_inst"], "achieved": a_,
+                                "frac": a_ / peak_gops}
+    src = roof.get("ncu_executed") or roof["executed"]
+    roof["achieved"] = src["achieved"]
+    roof["frac"] = src["frac"]
+    roof["frac_source"] = "ncu_executed" if roof.get("ncu_executed") else "executed (op-count model)"
     out = {"metric": "brute-force candidates/s", "value": size / (ms / 1e3), "unit": "candidates/s",
            "workload": "c4_resnet18_m8_12pp_k64_general", "candidates": size, "ms": ms, "reps": reps,
            "scaling": "strong", "E_min": res[0], "idx_min": res[1], "status": res[2],
@@ -599,7 +605,10 @@ def run_mine(args):
                                + (" + NCCL stats allreduce" if dist else ""),
                        "parallelism": f"dp{world}"},
             "roofline": {"bound": "alu", "kernel": "k_solve (K1)", "unit": "G FP64-pipe instr/s",
-                         "achieved": executed["achieved"], "peak": peak, "frac": executed["frac"],
+                         # the measured executed rate when the committed ncu record of this launch exists
+                         "achieved": (ncu_exec or executed)["achieved"], "peak": peak,
+                         "frac": (ncu_exec or executed)["frac"],
+                         "frac_source": "ncu_executed" if ncu_exec else "executed (op-count model)",
                          "w_div": W_DIV,
                          "executed": executed, "literal": literal, "ncu_executed": ncu_exec,
                          "traffic": ncu_record("k_solve") if default_c2 else None,

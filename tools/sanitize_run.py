@@ -10,7 +10,7 @@ import paper_2504_14611_b200 as J  # noqa: E402
 
 b = G.random_batch(seed=5, n_inst=64, M_lo=1, M_hi=32, N_lo=1, N_hi=12, k_max=70, tfree_frac=0.4)
 db = J.DeviceBatch(b)
-res = J.solve_batch(db, counts=True, stats=True, n_buckets=32)
+res = J.solve_batch(db, counts=True, stats=True, n_buckets=32, partition=True)
 J.solve_batch(db, stats=True, n_buckets=32)          # pruned product path
 J.solve_batch(db, work=True, partition=True)         # executed-work counters
 J.eval_plans(db, plans=res)
