@@ -587,7 +587,7 @@ static int solve_host_impl(const jdob_model *models, int32_t n_models, const jdo
     if (n > 0 && b->user_off[0] < 0) return fail(JDOB_EINVAL, "user_off[0] = %lld < 0", (long long)b->user_off[0]);
     const long long nu = n > 0 ? (long long)b->user_off[n] : 0;
 #ifndef JDOB_HOST_NS
-#define JDOB_HOST_NS 2
+#define JDOB_HOST_NS 4
 #endif
     constexpr int NS = JDOB_HOST_NS;  // copy/compute pipeline depth
     // device layout: model tables | batch | outputs | NS workspaces

@@ -16,11 +16,11 @@ __device__ __forceinline__ int part_of(const int *partition, const int *plan_nt,
     return ((plan_mask[i] >> m) & 1u) ? plan_nt[i] : N;
 }
 
-__global__ void k_eval(const DevModel *models, DevBatch b, const int *partition, const int *plan_nt,
-                       const unsigned *plan_mask, const double *f_e, double slack, double *E_out, double *tf_out,
-                       double *f_user, unsigned *viol_out, int *status_out) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= b.n_inst) return;
+// One configuration (instance i), one thread: the reference form of the evaluator.
+__device__ __forceinline__ void eval_one(long long i, const DevModel *models, const DevBatch &b, const int *partition,
+                                         const int *plan_nt, const unsigned *plan_mask, const double *f_e,
+                                         double slack, double *E_out, double *tf_out, double *f_user,
+                                         unsigned *viol_out, int *status_out) {
     const long long off = b.user_off[i];
     const long long M64 = b.user_off[i + 1] - off;
     const int mid = b.model_id[i];
@@ -171,6 +171,16 @@ __global__ void k_eval(const DevModel *models, DevBatch b, const int *partition,
     tf_out[i] = tf;
     viol_out[i] = viol;
     status_out[i] = st;
+}
+
+__global__ void __launch_bounds__(128) k_eval(const DevModel *models, DevBatch b, const int *partition,
+                                              const int *plan_nt, const unsigned *plan_mask, const double *f_e,
+                                              double slack, double *E_out, double *tf_out, double *f_user,
+                                              unsigned *viol_out, int *status_out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < b.n_inst)
+        eval_one(i, models, b, partition, plan_nt, plan_mask, f_e, slack, E_out, tf_out, f_user, viol_out,
+                 status_out);
 }
 
 void launch_eval(const DevModel *models, const DevBatch &b, const int *partition, const int *plan_nt,

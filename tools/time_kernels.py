@@ -50,10 +50,10 @@ def t_stats(cfg, n):
     return {"cfg": cfg + "_stats", "n": n, "ms": out[True] - out[False], "solve_ms": out[False]}
 
 
-def t_e2e(cfg, n):
-    """jdob_solve_batch_host from pinned host buffers (copies inside), median of 5."""
+def t_e2e(cfg, n, shared=False):
+    """jdob_solve_batch_host (jdob_solve_shared_host) from pinned host buffers (copies inside), median of 5."""
     b = G.config_batch(cfg, n_inst=n)
-    hb = J.HostBuffers(b, stats=True, n_buckets=int(b.meta.get("n_buckets", 32)))
+    hb = J.HostBuffers(b, stats=True, n_buckets=int(b.meta.get("n_buckets", 32)), shared=shared)
     J.solve_batch_host(hb)
     ts = []
     for _ in range(5):
@@ -65,7 +65,7 @@ def t_e2e(cfg, n):
         torch.cuda.synchronize()
         ts.append(s.elapsed_time(e))
     ms = float(np.median(ts))
-    return {"cfg": cfg + "_e2e", "n": n, "ms": ms, "inst_per_s": n / ms * 1e3}
+    return {"cfg": cfg + ("_e2e_shared" if shared else "_e2e"), "n": n, "ms": ms, "inst_per_s": n / ms * 1e3}
 
 
 def t_eval(cfg, n):
@@ -123,7 +123,7 @@ if __name__ == "__main__":
     todo = {"c2": lambda: t_solve("c2", 1 << 20), "c3": lambda: t_solve("c3", 100_000),
             "c5": lambda: t_solve("c5", 1_000_000), "bf": lambda: t_bf(0.25),
             "og": lambda: t_grouped("c3", 100_000), "eval": lambda: t_eval("c2", 1 << 20),
-            "stats": lambda: t_stats("c2", 1 << 20), "e2e": lambda: t_e2e("c2", 1 << 20), "c2lc": lambda: t_solve("c2", 1 << 20, J.MODE_LC),
+            "stats": lambda: t_stats("c2", 1 << 20), "e2e": lambda: t_e2e("c2", 1 << 20), "e2es": lambda: t_e2e("c2", 1 << 20, True), "c2lc": lambda: t_solve("c2", 1 << 20, J.MODE_LC),
             "c2noedge": lambda: t_solve("c2", 1 << 20, J.MODE_NO_EDGE_DVFS), "stats5": lambda: t_stats("c5", 1_000_000)}
     for r in (todo[w]() for w in which):
         r["lib"] = os.path.basename(lib)
