@@ -130,7 +130,9 @@ __global__ void k_bf_setup(const DevModel *models, DevBatch b, int space, BfHead
 //   including the one that ends a scan)  [5] Gamma divisions executed  [6] candidates skipped by
 //   the edge-only j skip  [7] vectors whose D6' fails at the first grid point  [8] offloaders
 //   summed over the evaluated candidates
-template <int MAXM, bool EXACT, bool WORK>
+// GEN: the general space (blocks of N + 1 vectors per lane) or the identical space (one vector per
+// lane), a compile-time choice so that each kernel carries only its own space's code.
+template <int MAXM, bool EXACT, bool WORK, bool GEN>
 #ifndef JDOB_BF_MINB
 #define JDOB_BF_MINB 4
 #endif
@@ -249,7 +251,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
             // mixed-radix add of the stride's digits (64-bit division only here).  Identical space:
             // one vector per lane and step.  Either way a lane visits its vectors in increasing order.
             const int radix = N + 1;
-            const bool blk = (space == 0);
+            constexpr bool blk = GEN;
             const int L = blk ? radix : 1;
             const unsigned long long ubeg = blk ? vb / (unsigned long long)radix : vb;
             const unsigned long long uend = blk ? (ve + radix - 1) / (unsigned long long)radix : ve;
@@ -726,15 +728,18 @@ template <int MAXM, bool EXACT = false>
 static void launch_main(const DevModel *models, int model_id, int space, unsigned long long ib, unsigned long long ie,
                         BfHeader *hdr, const double *tab, const double *user, const double *inv,
                         double *part_E, long long *part_idx, unsigned long long *work, size_t smem, cudaStream_t s) {
-    if (work) {
-        cudaMemsetAsync(work, 0, 9 * sizeof(unsigned long long), s);
-        cudaFuncSetAttribute(k_bf_main<MAXM, EXACT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_bf_main<MAXM, EXACT, true><<<kBfBlocks, kBfWarps * 32, smem, s>>>(models, model_id, space, ib, ie, hdr, tab,
-                                                                            user, inv, part_E, part_idx, work);
+    if (work) cudaMemsetAsync(work, 0, 9 * sizeof(unsigned long long), s);
+    auto go = [&](auto kern, unsigned long long *w) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<kBfBlocks, kBfWarps * 32, smem, s>>>(models, model_id, space, ib, ie, hdr, tab, user, inv, part_E,
+                                                    part_idx, w);
+    };
+    if (space == 0) {
+        if (work) go(k_bf_main<MAXM, EXACT, true, true>, work);
+        else go(k_bf_main<MAXM, EXACT, false, true>, nullptr);
     } else {
-        cudaFuncSetAttribute(k_bf_main<MAXM, EXACT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_bf_main<MAXM, EXACT, false><<<kBfBlocks, kBfWarps * 32, smem, s>>>(models, model_id, space, ib, ie, hdr, tab,
-                                                                             user, inv, part_E, part_idx, nullptr);
+        if (work) go(k_bf_main<MAXM, EXACT, true, false>, work);
+        else go(k_bf_main<MAXM, EXACT, false, false>, nullptr);
     }
 }
 
