@@ -161,6 +161,15 @@ def fp64_frac(div, oth, ms, peak_gops):
             "frac": ach / peak_gops}
 
 
+def issue_roof(warp_instructions, ms, clk_mhz):
+    """The kernel against the instruction-issue peak (148 SMs x 4 schedulers x 1 warp instruction per
+    clock): what bounds K1 and K2, whose FP64 pipe is mostly idle (ncu warp instructions of the launch)."""
+    peak = N_SMS * 4 * clk_mhz * 1e6 / 1e9   # G warp instructions/s
+    a = warp_instructions / (ms / 1e3) / 1e9
+    return {"warp_instructions_per_launch": warp_instructions, "achieved": a, "peak": peak, "unit": "G warp instr/s",
+            "frac": a / peak}
+
+
 def cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -320,6 +329,7 @@ def bf_leg(J, torch, world, rank, reps, dist, peak_gops, with_cpu, cpu_seconds):
     ldiv, loth = bf_literal_ops(N, M, k)
     ediv, eoth = bf_executed_ops(wk, N, M)
     hw = ncu_record("k_bf_main_hw") if world == 1 else None
+    clk_mhz = peak_gops * 1e3 / (N_SMS * PEAK_FP64_SM_PER_CLK)
     roof = {"bound": "alu", "kernel": "k_bf_main (K2)", "unit": "G FP64-pipe instr/s", "peak": peak_gops,
             "launch_ms": km, "w_div": W_DIV,
             "literal": fp64_frac(ldiv / world, loth / world, km, peak_gops),
@@ -337,6 +347,7 @@ def bf_leg(J, torch, world, rank, reps, dist, peak_gops, with_cpu, cpu_seconds):
         a_ = hw["fp64_thread_inst"] / (km / 1e3) / 1e9
         roof["ncu_executed"] = {"fp64_lane_instructions_per_launch": hw["fp64_thread_inst"], "achieved": a_,
                                 "frac": a_ / peak_gops}
+        roof["issue"] = issue_roof(hw["warp_instructions"], km, clk_mhz)
     src = roof.get("ncu_executed") or roof["executed"]
     roof["achieved"] = src["achieved"]
     roof["frac"] = src["frac"]
@@ -577,11 +588,12 @@ def run_mine(args):
         hw = ncu_record("k_solve_hw") if default_c2 else None
         # hardware count of the FP64-pipe lane instructions one launch executes (committed ncu capture
         # of this exact launch), over the live K1 time: the measured executed fraction
-        ncu_exec = None
+        ncu_exec = issue = None
         if hw and hw.get("fp64_thread_inst"):
             a_ = hw["fp64_thread_inst"] / (solve_ms / 1e3) / 1e9
             ncu_exec = {"fp64_lane_instructions_per_launch": hw["fp64_thread_inst"], "achieved": a_,
                         "frac": a_ / peak}
+            issue = issue_roof(hw["warp_instructions"], solve_ms, peak_clk)
         line = {
             "metric": "J-DOB instances solved/s",
             "value": value,
@@ -611,6 +623,7 @@ def run_mine(args):
                          "frac_source": "ncu_executed" if ncu_exec else "executed (op-count model)",
                          "w_div": W_DIV,
                          "executed": executed, "literal": literal, "ncu_executed": ncu_exec,
+                         "issue": issue,
                          "traffic": ncu_record("k_solve") if default_c2 else None,
                          "ncu_hw": hw,
                          "algorithmic_bytes": int(batch.nbytes()),
