@@ -33,11 +33,9 @@ struct BfHeader {
 
 // Per-(n, user) tables are stored user-major, element m (N + 1) + n: the brute force gathers them with
 // a lane-dependent n for a fixed user, so consecutive n must fall in distinct shared-memory banks.
-#ifndef JDOB_BF_NO_TRANS
-__device__ __forceinline__ int tix(int n, int m, int N, int M) { return m * (N + 1) + n; }
-#else
-__device__ __forceinline__ int tix(int n, int m, int N, int M) { return n * M + m; }
-#endif
+// NP = the row length: N + 1, or 16 when the kernel is specialised for N <= 15 (PAD: every shared-memory
+// offset is then a compile-time constant of the M = 8 kernel, so no registers hold table pointers).
+__device__ __forceinline__ int tix(int n, int m, int NP) { return m * NP + n; }
 
 // Base-(N+1) digits of a lane's block index (users 0 .. M-2).  (Packing them as 6-bit fields of one
 // 64-bit word frees registers but costs more instructions than the spills it removes: measured.)
@@ -48,7 +46,7 @@ struct Digits {
     __device__ __forceinline__ void set(int m, int v) { a[m] = v; }
 };
 
-__global__ void k_bf_setup(const DevModel *models, DevBatch b, int space, BfHeader *hdr, double *tab /*[5][M][N+1]*/,
+__global__ void k_bf_setup(const DevModel *models, DevBatch b, int space, int NP, BfHeader *hdr, double *tab /*[5][M][NP]*/,
                            double *user /*[4][32]: eloc fmin fmax T*/, double *invtab) {
     const int lane = threadIdx.x & 31;
     long long off, k;
@@ -105,10 +103,10 @@ __global__ void k_bf_setup(const DevModel *models, DevBatch b, int space, BfHead
         user[1 * 32 + lane] = x.f0;
         user[2 * 32 + lane] = x.f1;
         user[3 * 32 + lane] = x.T;
-        const int NM = (N + 1) * M;
+        const int NM = NP * M;
         for (int n = 0; n <= N; n++) {
             const double OR = md.O[n] / x.R;
-            const int t = tix(n, lane, N, M);
+            const int t = tix(n, lane, NP);
             tab[0 * NM + t] = OR;                  // O_n / R_m
             tab[1 * NM + t] = x.z * md.v[n];       // zeta_m v_n
             tab[2 * NM + t] = x.k * md.u[n];       // kappa_m u_n
@@ -132,7 +130,7 @@ __global__ void k_bf_setup(const DevModel *models, DevBatch b, int space, BfHead
 //   summed over the evaluated candidates
 // GEN: the general space (blocks of N + 1 vectors per lane) or the identical space (one vector per
 // lane), a compile-time choice so that each kernel carries only its own space's code.
-template <int MAXM, bool EXACT, bool WORK, bool GEN>
+template <int MAXM, bool EXACT, bool WORK, bool GEN, bool PAD>
 #ifndef JDOB_BF_MINB
 #define JDOB_BF_MINB 4
 #endif
@@ -156,7 +154,8 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
         const unsigned long long size = hdr->size;
         const double t_free = hdr->t_free, fe_max = hdr->fe_max, rho = hdr->rho;
         const DevModel &md = models[model_id];
-        const int NM = (N + 1) * M;
+        const int NP = PAD ? 16 : N + 1, NR = PAD ? 16 : N + 1;  // table row length, d/c table rows
+        const int NM = NP * M;
         double *sOR = sm, *sZV = sm + NM, *sKU = sm + 2 * NM, *sUP = sm + 3 * NM;
         double *sLB = sm + 4 * NM;  // [M][N+1] per-user bound terms (tix)
         double *sEl = sm + 5 * NM, *sFmin = sEl + 32, *sFmax = sEl + 64, *sT = sEl + 96;
@@ -166,7 +165,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
         double *sG = sPlb + 64;  // [M][N+1] lower bound of user m's arrival O/R + zv/f* when offloading at n
         // d_n(b) A_n and c_n(b) A_n for b = 0..M (row stride M + 1): the batch sums gather them with a
         // lane-dependent b, consecutive b in distinct banks
-        double *sDA = sG + (N + 1) * M, *sCA = sDA + (N + 1) * (M + 1);
+        double *sDA = sG + NP * M, *sCA = sDA + NR * (M + 1);
         const long long kt = k < kInvTab ? k : kInvTab;
         for (int x = threadIdx.x; x < 5 * NM; x += blockDim.x) sm[x] = tab[x];
         for (int x = threadIdx.x; x < 128; x += blockDim.x) sEl[x] = user[x];
@@ -201,7 +200,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
         // G = RN(O/R + RN(zv RD(1/f_max))) (1 - 2^-46) <= (O/R + zv/f_max)(1 - 2^-47) and the margins
         // of X below, S / X <= f_e for every feasible candidate.
         for (int y = threadIdx.x; y < N * M; y += blockDim.x) {
-            const int m = y % M, x = tix(y / M, m, N, M);
+            const int m = y % M, x = tix(y / M, m, NP);
 #ifndef JDOB_BF_NO_D7_FE
             sG[x] = (sOR[x] + sZV[x] * recip_rd(sFmax[m])) * (1.0 - 0x1p-46);
 #else
@@ -220,7 +219,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
         {
             const double inv_max = sInv[0];  // RN(1 / f_e(0)) = RN(1 / f_e,max)
             for (int y = threadIdx.x; y < N * M; y += blockDim.x) {
-                const int n = y / M, m = y % M, x = tix(n, m, N, M);
+                const int n = y / M, m = y % M, x = tix(n, m, NP);
                 const double zv = sZV[x];
                 if (zv == 0.0) continue;  // f* = f_min (R9): the f_min term stands
                 const double X = (sT[m] - sOR[x]) - sSlb[n] * inv_max;
@@ -298,7 +297,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                     for (int m = 0; m < MAXM; m++)
                         if (m < M - 1) {
 #if JDOB_BF_PRUNE
-                            lbu_hi = lbu_hi + sLB[tix(dig.get(m), m, N, M)];
+                            lbu_hi = lbu_hi + sLB[tix(dig.get(m), m, NP)];
 #endif
                             const int dm = dig.get(m);
                             if (dm < N) {
@@ -313,7 +312,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
 #pragma unroll
                         for (int m = 0; m < MAXM; m++)
                             if (m < M - 1 && dig.get(m) == nmin_hi) {
-                                const double g = sG[tix(nmin_hi, m, N, M)];
+                                const double g = sG[tix(nmin_hi, m, NP)];
                                 gmax_hi = (g > gmax_hi) ? g : gmax_hi;
                             }
                     }
@@ -343,11 +342,11 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                 // stop here
                 double lbu = 0.0;
                 if (blk) {
-                    lbu = lbu_hi + sLB[tix(t, M - 1, N, M)];
+                    lbu = lbu_hi + sLB[tix(t, M - 1, NP)];
                 } else {
 #pragma unroll
                     for (int m = 0; m < MAXM; m++)
-                        if (m < M) lbu = lbu + sLB[tix(nv[m], m, N, M)];
+                        if (m < M) lbu = lbu + sLB[tix(nv[m], m, NP)];
                 }
                 if (lbu >= bestE || lbu > inc) continue;  // the edge term only adds (>= 0)
                 if constexpr (WORK) wk[1]++;
@@ -388,7 +387,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                         if (blk) {
                             gmax = (t < nmin_hi) ? t_free : gmax_hi;  // t < nmin_hi: only the last user at nmin = t
                             if (t == nmin) {
-                                const double g = sG[tix(t, M - 1, N, M)];
+                                const double g = sG[tix(t, M - 1, NP)];
                                 gmax = (g > gmax) ? g : gmax;
                             }
                         } else
@@ -397,7 +396,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
 #pragma unroll
                             for (int m = 0; m < MAXM; m++)
                                 if (m < M && nv[m] == nmin)
-                                    gmax = (sG[tix(nmin, m, N, M)] > gmax) ? sG[tix(nmin, m, N, M)] : gmax;
+                                    gmax = (sG[tix(nmin, m, NP)] > gmax) ? sG[tix(nmin, m, NP)] : gmax;
                         }
                         Xd7 = __dmul_ru(__dadd_ru(__dmul_ru(l_o, 1.0 + 0x1p-48), -gmax), 1.0 + 0x1p-48);
                         const double fd = div_lb(Slo, Xd7);  // <= S_{nmin+1} / X
@@ -502,7 +501,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                     if (m < M && nv[m] < N) {
                         offm |= 1u << m;
                         if constexpr (REG) {
-                            const int x = tix(nv[m], m, N, M);
+                            const int x = tix(nv[m], m, NP);
                             lo[m] = l_o - sOR[x];
                             zvr[m] = sZV[x];
                             kur[m] = sKU[x];
@@ -613,7 +612,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                                     ku = kur[m];
                                     up = upr[m];
                                 } else {
-                                    const int x = tix(nv[m], m, N, M);
+                                    const int x = tix(nv[m], m, NP);
                                     lom = l_o - sOR[x];
                                     zv = sZV[x];
                                     ku = sKU[x];
@@ -724,22 +723,22 @@ size_t bf_workspace_bytes() {
            1024;
 }
 
-template <int MAXM, bool EXACT = false>
+template <int MAXM, bool EXACT = false, bool PAD = false>
 static void launch_main(const DevModel *models, int model_id, int space, unsigned long long ib, unsigned long long ie,
                         BfHeader *hdr, const double *tab, const double *user, const double *inv,
                         double *part_E, long long *part_idx, unsigned long long *work, size_t smem, cudaStream_t s) {
     if (work) cudaMemsetAsync(work, 0, 9 * sizeof(unsigned long long), s);
-    auto go = [&](auto kern, unsigned long long *w) {
+    auto go = [&](auto kern, unsigned long long *w) {  // (the PAD choice is the caller's template argument)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<kBfBlocks, kBfWarps * 32, smem, s>>>(models, model_id, space, ib, ie, hdr, tab, user, inv, part_E,
                                                     part_idx, w);
     };
     if (space == 0) {
-        if (work) go(k_bf_main<MAXM, EXACT, true, true>, work);
-        else go(k_bf_main<MAXM, EXACT, false, true>, nullptr);
+        if (work) go(k_bf_main<MAXM, EXACT, true, true, PAD>, work);
+        else go(k_bf_main<MAXM, EXACT, false, true, PAD>, nullptr);
     } else {
-        if (work) go(k_bf_main<MAXM, EXACT, true, false>, work);
-        else go(k_bf_main<MAXM, EXACT, false, false>, nullptr);
+        if (work) go(k_bf_main<MAXM, EXACT, true, false, PAD>, work);
+        else go(k_bf_main<MAXM, EXACT, false, false, PAD>, nullptr);
     }
 }
 
@@ -758,11 +757,20 @@ void launch_bruteforce_impl(const DevModel *models, const DevBatch &b, int model
     double *part_E = (double *)p;
     p += sizeof(double) * kBfBlocks;
     long long *part_idx = (long long *)p;
-    k_bf_setup<<<1, 32, 0, s>>>(models, b, space, hdr, tab, user, inv);
     const int Mc = (M >= 1 && M <= kMaxM) ? M : 1;
-    const size_t smem = sizeof(double) * (5 * (size_t)(N + 1) * Mc + 128 + kInvTab + 17 * kBfThreads + 128 +
-                                          (size_t)(N + 1) * Mc + 2 * (size_t)(N + 1) * (Mc + 1));
-    if (Mc == 8)
+#ifndef JDOB_BF_NO_PAD
+    const bool pad = (Mc == 8 && N <= 15);  // M = 8, N <= 15: the constant-layout kernel (C4: N = 11)
+#else
+    const bool pad = false;
+#endif
+    const size_t NP = pad ? 16 : (size_t)N + 1;
+    k_bf_setup<<<1, 32, 0, s>>>(models, b, space, (int)NP, hdr, tab, user, inv);
+    const size_t smem = sizeof(double) * (5 * NP * Mc + 128 + kInvTab + 17 * kBfThreads + 128 + NP * Mc +
+                                          2 * NP * (Mc + 1));
+    if (pad)
+        launch_main<8, true, true>(models, model_id, space, idx_begin, idx_end, hdr, tab, user, inv, part_E, part_idx,
+                                   work, smem, s);
+    else if (Mc == 8)
         launch_main<8, true>(models, model_id, space, idx_begin, idx_end, hdr, tab, user, inv, part_E, part_idx, work, smem,
                              s);
     else if (Mc <= 8)
