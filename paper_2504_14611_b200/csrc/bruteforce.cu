@@ -292,6 +292,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                 // users 0 .. M-2 of the block (general space): bound terms in user order, n_min, l_o
                 double lbu_hi = 0.0, lo_hi = dinf(), gmax_hi = t_free;
                 int nmin_hi = N;
+                unsigned long long hist_hi = 0ull;  // digit histogram of users 0 .. M-2 (4-bit fields)
                 if (blk) {
 #pragma unroll
                     for (int m = 0; m < MAXM; m++)
@@ -300,6 +301,7 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                             lbu_hi = lbu_hi + sLB[tix(dig.get(m), m, NP)];
 #endif
                             const int dm = dig.get(m);
+                            if (M <= 15 && N <= 15) hist_hi += 1ull << (4 * dm);
                             if (dm < N) {
                                 if (dm < nmin_hi) nmin_hi = dm;
                                 lo_hi = (sT[m] < lo_hi) ? sT[m] : lo_hi;
@@ -419,9 +421,13 @@ __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const D
                     // descends.  Below n_min + 1 every b_n is 0 and the literal loop adds +0.0, which
                     // leaves S and Psi unchanged, so the sums stop there: S = Psi's partner S_{nmin+1}.
                     // The per-user S_{n_m+1} are formed only for vectors that pass the bound below.
+                    if (blk) {
+                        hist = hist_hi + (1ull << (4 * t));  // the block's histogram plus the last user
+                    } else {
 #pragma unroll
-                    for (int m = 0; m < MAXM; m++)
-                        if (m < M) hist += 1ull << (4 * nv[m]);
+                        for (int m = 0; m < MAXM; m++)
+                            if (m < M) hist += 1ull << (4 * nv[m]);
+                    }
                     int ge = 0;
                     for (int n = N; n > nmin; n--) {
                         ge += (int)((hist >> (4 * n)) & 0xfull);
