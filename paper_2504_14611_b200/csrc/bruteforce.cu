@@ -132,7 +132,7 @@ __global__ void k_bf_setup(const DevModel *models, DevBatch b, int space, int NP
 // lane), a compile-time choice so that each kernel carries only its own space's code.
 template <int MAXM, bool EXACT, bool WORK, bool GEN, bool PAD>
 #ifndef JDOB_BF_MINB
-#define JDOB_BF_MINB 4
+#define JDOB_BF_MINB 3
 #endif
 __global__ void __launch_bounds__(kBfWarps * 32, JDOB_BF_MINB) k_bf_main(const DevModel *models, int model_id, int space,
                                                            unsigned long long idx_begin, unsigned long long idx_end,
@@ -729,6 +729,22 @@ size_t bf_workspace_bytes() {
            1024;
 }
 
+// one wave of the persistent grid: JDOB_BF_GRID blocks per SM (at most kBfBlocks in all)
+#ifndef JDOB_BF_GRID
+#define JDOB_BF_GRID 3
+#endif
+static int bf_grid() {
+    static const int g = [] {
+        int dev = 0, n = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+        const long long want = (long long)n * JDOB_BF_GRID;
+        return (int)(want < kBfBlocks ? want : kBfBlocks);
+    }();
+    return g;
+}
+
 template <int MAXM, bool EXACT = false, bool PAD = false>
 static void launch_main(const DevModel *models, int model_id, int space, unsigned long long ib, unsigned long long ie,
                         BfHeader *hdr, const double *tab, const double *user, const double *inv,
@@ -736,7 +752,7 @@ static void launch_main(const DevModel *models, int model_id, int space, unsigne
     if (work) cudaMemsetAsync(work, 0, 9 * sizeof(unsigned long long), s);
     auto go = [&](auto kern, unsigned long long *w) {  // (the PAD choice is the caller's template argument)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<kBfBlocks, kBfWarps * 32, smem, s>>>(models, model_id, space, ib, ie, hdr, tab, user, inv, part_E,
+        kern<<<bf_grid(), kBfWarps * 32, smem, s>>>(models, model_id, space, ib, ie, hdr, tab, user, inv, part_E,
                                                     part_idx, w);
     };
     if (space == 0) {
@@ -785,7 +801,7 @@ void launch_bruteforce_impl(const DevModel *models, const DevBatch &b, int model
         launch_main<16>(models, model_id, space, idx_begin, idx_end, hdr, tab, user, inv, part_E, part_idx, work, smem, s);
     else
         launch_main<32>(models, model_id, space, idx_begin, idx_end, hdr, tab, user, inv, part_E, part_idx, work, smem, s);
-    k_bf_final<<<1, 32, 0, s>>>(hdr, part_E, part_idx, kBfBlocks, E_min, idx_min, status);
+    k_bf_final<<<1, 32, 0, s>>>(hdr, part_E, part_idx, bf_grid(), E_min, idx_min, status);
 }
 
 }  // namespace jdob
