@@ -684,7 +684,7 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
 #endif
 
 #ifndef JDOB_SOLVE_MINB_U
-#define JDOB_SOLVE_MINB_U 6
+#define JDOB_SOLVE_MINB_U 5
 #endif
 
 // VERIFY: the instantiation with row a11 in the epilogue (r.viol != NULL); the product kernel without
