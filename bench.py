@@ -684,7 +684,7 @@ def run_reference(args):
             "data": "synthetic", "impl": "reference",
             "config": {"workload": label, "n_inst_per_step": per_step, "parallelism": f"host x{cores} threads"},
             "cpu_baseline": {"value": value, "unit": "instances/s", "cores": cores, "kind": "oracle",
-                             "sample": f"{per_step} instances of {label} per step"},
+                             "cpu_model": cpu_model(), "sample": f"{per_step} instances of {label} per step"},
             "e2e": {"value": value, "unit": "instances/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
