@@ -12,6 +12,7 @@ GPUs and over gloo on CPU (tests/test_dist_gloo.py).
 """
 from __future__ import annotations
 
+import contextlib
 from typing import Tuple
 
 STATS_MAX_FIELD, STATS_MIN_FIELD = 3, 4
@@ -30,18 +31,26 @@ def bf_shard(size: int, k: int, world: int, rank: int) -> Tuple[int, int]:
     return v0 * k, v1 * k
 
 
+def _nvtx(name):
+    """NVTX range around a collective (SURVEY §5 tracing) when CUDA is present."""
+    import torch
+    if torch.cuda.is_available():
+        return torch.cuda.nvtx.range(name)
+    return contextlib.nullcontext()
+
+
 def allreduce_stats(stats, dist):
     """Fold per-rank statistics [n_buckets, 80]: SUM, except field 3 MAX and field 4 MIN."""
-    import torch
-    red = stats.clone()
-    dist.all_reduce(red, op=dist.ReduceOp.SUM)
-    mx = stats[:, STATS_MAX_FIELD].contiguous().clone()
-    mn = stats[:, STATS_MIN_FIELD].contiguous().clone()
-    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-    dist.all_reduce(mn, op=dist.ReduceOp.MIN)
-    red[:, STATS_MAX_FIELD] = mx
-    red[:, STATS_MIN_FIELD] = mn
-    return red
+    with _nvtx("jdob.allreduce_stats"):
+        red = stats.clone()
+        dist.all_reduce(red, op=dist.ReduceOp.SUM)
+        mx = stats[:, STATS_MAX_FIELD].contiguous().clone()
+        mn = stats[:, STATS_MIN_FIELD].contiguous().clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(mn, op=dist.ReduceOp.MIN)
+        red[:, STATS_MAX_FIELD] = mx
+        red[:, STATS_MIN_FIELD] = mn
+        return red
 
 
 def fold_parts(parts):
@@ -69,12 +78,13 @@ def fold_stats(stats, dist):
     world = dist.get_world_size()
     if world & (world - 1):
         return allreduce_stats(stats, dist)
-    x = stats.contiguous()
-    if dist.get_backend() == "gloo" and x.is_cuda:   # test-only backend: gather on the host
-        x = x.cpu()
-    parts = [torch.empty_like(x) for _ in range(world)]
-    dist.all_gather(parts, x)
-    return fold_parts(torch.stack(parts)).to(stats.device)
+    with _nvtx("jdob.fold_stats"):
+        x = stats.contiguous()
+        if dist.get_backend() == "gloo" and x.is_cuda:   # test-only backend: gather on the host
+            x = x.cpu()
+        parts = [torch.empty_like(x) for _ in range(world)]
+        dist.all_gather(parts, x)
+        return fold_parts(torch.stack(parts)).to(stats.device)
 
 
 def allreduce_argmin(E, idx, dist):
@@ -82,9 +92,10 @@ def allreduce_argmin(E, idx, dist):
 
     idx < 0 (no feasible candidate on that rank) never wins unless every rank has none."""
     import torch
-    Eg = E.clone()
-    dist.all_reduce(Eg, op=dist.ReduceOp.MIN)
-    cand = torch.where((E == Eg) & (idx >= 0), idx, torch.full_like(idx, IDX_NONE))
-    dist.all_reduce(cand, op=dist.ReduceOp.MIN)
-    cand = torch.where(cand == IDX_NONE, torch.full_like(cand, -1), cand)
-    return Eg, cand
+    with _nvtx("jdob.allreduce_argmin"):
+        Eg = E.clone()
+        dist.all_reduce(Eg, op=dist.ReduceOp.MIN)
+        cand = torch.where((E == Eg) & (idx >= 0), idx, torch.full_like(idx, IDX_NONE))
+        dist.all_reduce(cand, op=dist.ReduceOp.MIN)
+        cand = torch.where(cand == IDX_NONE, torch.full_like(cand, -1), cand)
+        return Eg, cand
