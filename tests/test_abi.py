@@ -66,6 +66,19 @@ def test_argument_errors_without_gpu(L):
     assert b"NULL" in L.jdob_last_error()
     assert L.jdob_solve_batch(None, 0, None, 0, None, None, 0, None) == B.EINVAL
     assert L.jdob_bruteforce(ms, 1, C.byref(b), 0, 0, 1, None, None, None, None, None, 0, None) == B.EINVAL
+    # the entry points added in round 2 reject bad arguments on the host, before any CUDA call
+    sb = B.JSharedBatch()
+    assert L.jdob_solve_shared_host(ms, 1, C.byref(sb), 0, C.byref(r), None, None, None) == B.EINVAL
+    assert L.jdob_solve_shared_host(ms, 1, None, 0, C.byref(r), None, None, None) == B.EINVAL
+    assert L.jdob_stats(None, None, None, 0, None) == B.EINVAL
+    assert L.jdob_stats_part(C.byref(b), C.byref(r), 10, 3, 0, None, 0, None) == B.EINVAL   # NULL stats
+    gp = B.JGenParams()
+    n_users = C.c_int64()
+    assert L.jdob_generate_c5_instances(C.byref(gp), C.byref(b), None, None, 0, None) == B.EINVAL
+    b5 = B.JBatch(5, 1)
+    assert L.jdob_generate_c5_instances(C.byref(gp), C.byref(b5), C.byref(n_users), None, 0, None) == B.EINVAL
+    assert L.jdob_generate_workspace_bytes(-1) == 0
+    assert L.jdob_workspace_bytes(None, 0, 2) > 0          # jdob_stats needs no model part
 
 
 def test_no_cpu_fallback():
