@@ -391,6 +391,30 @@ def test_bf_random_full_and_ranges(J):
                 assert int(I.item()) == Io
 
 
+@pytest.mark.parametrize("N_lo,N_hi", [(1, 3), (9, 15), (16, 17)])
+def test_bf_m8_constant_layout(J, N_lo, N_hi):
+    """M = 8: N <= 15 takes the constant-layout kernel (rows padded to 16), N = 16, 17 the generic M = 8
+    kernel; random models, t_free > 0 on some, oracle-checked on sub-ranges (the spaces reach 18^8 * k)
+    and in full where small, both index spaces."""
+    b = g.random_batch(seed=160 + N_lo, n_inst=6, M_lo=8, M_hi=8, N_lo=N_lo, N_hi=N_hi, k_max=6, tfree_frac=0.5)
+    rng = np.random.default_rng(N_lo)
+    for i in range(b.n_inst):
+        bi = b.subset(i, i + 1)
+        db = J.DeviceBatch(bi)
+        for space in (0, 1):
+            size = O.bf_space_size(bi, space)
+            ranges = [(0, min(size, 400_000))]
+            for _ in range(2):
+                lo = int(rng.integers(0, max(1, size - 300_000)))
+                ranges.append((lo, min(size, lo + int(rng.integers(1, 300_000)))))
+            for lo, hi in ranges:
+                E, I, S = J.bruteforce(db, space, lo, hi)
+                Eo, Io, So = O.bf(bi, space, lo, hi, threads=8)
+                assert int(S.item()) == So
+                assert_bits_equal(E.cpu().numpy(), np.array([Eo]), f"E {i} {space} {lo} {hi}")
+                assert int(I.item()) == Io
+
+
 def test_bf_tight_deadlines(J):
     """Deadlines just above the local minimum (beta in [0, 0.6]) and t_free > 0: most candidates are
     infeasible and the optimum sits near the feasibility boundary, where the exact vector bounds
