@@ -46,7 +46,7 @@ static size_t model_table_bytes(const jdob_model &m) {
 }
 
 static size_t stats_partial_bytes() {
-    return al((size_t)kStatsBlocks * 64 * kStatsF * sizeof(double));  // one group of 64 buckets (stats.cu)
+    return al((size_t)kStatsBlocks * 64 * kStatsF * sizeof(double));  // one group (<= 64 buckets, stats.cu)
 }
 
 static int check_models(const jdob_model *models, int32_t n_models) {

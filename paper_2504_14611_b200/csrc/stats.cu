@@ -25,10 +25,13 @@ __device__ __forceinline__ double combine(int f, double a, double b) {
     return a + b;
 }
 
-// Field slots kept per lane in floating point: sum r, sum r^2, max r, min r, sum E/M, sum E_lc/M.
-constexpr int kLaneF = 6;
-__device__ __forceinline__ int lane_slot(int f) {  // field -> per-lane slot, -1 = integer counter
-    return (f == 1) ? 0 : (f == 2) ? 1 : (f == 3) ? 2 : (f == 4) ? 3 : (f == 5) ? 4 : (f == 6) ? 5 : -1;
+// Field slots kept per lane in floating point (the sums, whose bits depend on the order): sum r,
+// sum r^2, sum E/M, sum E_lc/M.  max r and min r are exact in any order: integer atomics on the bits of
+// the non-negative r (E <= E_LC), NaN (a zero-energy instance's 0/0) never taking part, as in the
+// comparison form.
+constexpr int kLaneF = 4;
+__device__ __forceinline__ int lane_slot(int f) {  // field -> per-lane slot, -1 = not a lane slot
+    return (f == 1) ? 0 : (f == 2) ? 1 : (f == 5) ? 2 : (f == 6) ? 3 : -1;
 }
 
 // One warp per block.  Lane l of warp w owns the instances i0 + l, i0 + l + 32, ... of the warp's fixed
@@ -37,7 +40,10 @@ __device__ __forceinline__ int lane_slot(int f) {  // field -> per-lane slot, -1
 // are then folded in lane order, so the result is identical run to run.
 // One pass accumulates the buckets [b_lo, b_lo + n_buckets) of n_all (at most kBucketGroup, the shared
 // memory of one warp); more buckets take one pass per group over the same instances.
-constexpr int kBucketGroup = 64;
+#ifndef JDOB_STATS_GROUP
+#define JDOB_STATS_GROUP 16
+#endif
+constexpr int kBucketGroup = JDOB_STATS_GROUP;
 
 __global__ void __launch_bounds__(32) k_stats_partial(DevBatch b, DevResult r, double *partials, int n_buckets,
                                                       long long n_total, long long begin, long long w0, int b_lo,
@@ -45,11 +51,14 @@ __global__ void __launch_bounds__(32) k_stats_partial(DevBatch b, DevResult r, d
     // leaf w of the global tree = instances [n_total w / W, n_total (w + 1) / W); this block is w0 + blockIdx.x
     extern __shared__ double sh[];
     double *fs = sh;                                                        // [n_buckets][kLaneF][32]
-    int *cnt = (int *)(sh + (size_t)n_buckets * kLaneF * 32);               // [n_buckets][kStatsF]
+    unsigned long long *mxb = (unsigned long long *)(sh + (size_t)n_buckets * kLaneF * 32);  // [n_buckets]
+    unsigned long long *mnb = mxb + n_buckets;                              // [n_buckets]
+    int *cnt = (int *)(mnb + n_buckets);                                    // [n_buckets][kStatsF]
     const int lane = threadIdx.x;
-    for (int x = lane; x < n_buckets * kLaneF * 32; x += 32) {
-        const int slot = (x / 32) % kLaneF;
-        fs[x] = (slot == 2) ? -dinf() : (slot == 3) ? dinf() : 0.0;
+    for (int x = lane; x < n_buckets * kLaneF * 32; x += 32) fs[x] = 0.0;
+    for (int x = lane; x < n_buckets; x += 32) {
+        mxb[x] = 0ull;                    // +0; cnt field 3 says whether any r was seen
+        mnb[x] = 0x7ff0000000000000ull;   // +inf
     }
     for (int x = lane; x < n_buckets * kStatsF; x += 32) cnt[x] = 0;
     __syncwarp();
@@ -94,10 +103,14 @@ __global__ void __launch_bounds__(32) k_stats_partial(DevBatch b, DevResult r, d
             double *a = fs + (size_t)bk * kLaneF * 32 + lane;
             a[0 * 32] = a[0 * 32] + rr;
             a[1 * 32] = a[1 * 32] + rr * rr;
-            a[2 * 32] = (rr > a[2 * 32]) ? rr : a[2 * 32];
-            a[3 * 32] = (rr < a[3 * 32]) ? rr : a[3 * 32];
-            a[4 * 32] = a[4 * 32] + E / (double)M;
-            a[5 * 32] = a[5 * 32] + El / (double)M;
+            a[2 * 32] = a[2 * 32] + E / (double)M;
+            a[3 * 32] = a[3 * 32] + El / (double)M;
+            if (rr == rr) {  // not NaN
+                const unsigned long long rb = (unsigned long long)__double_as_longlong(rr);
+                atomicMax(mxb + bk, rb);
+                atomicMin(mnb + bk, rb);
+                c[3] = 1;  // some r seen (a benign same-value race)
+            }
             atomicAdd(c + 0, 1);
             if (Fq[q] > 0.0) atomicAdd(c + 7, 1);  // the plan offloads (f_e* = 0 only when all-local, R18)
             const int nt = nq[q];
@@ -110,7 +123,11 @@ __global__ void __launch_bounds__(32) k_stats_partial(DevBatch b, DevResult r, d
         const int f = x % kStatsF, bk = x / kStatsF;
         const int slot = lane_slot(f);
         double v;
-        if (slot < 0) {
+        if (f == 3) {
+            v = cnt[bk * kStatsF + 3] ? __longlong_as_double((long long)mxb[bk]) : field_init(f);
+        } else if (f == 4) {
+            v = __longlong_as_double((long long)mnb[bk]);
+        } else if (slot < 0) {
             v = (f == 0 || f == 7 || f == 8 || (f >= 9 && f < 9 + 64)) ? (double)cnt[x] : field_init(f);
         } else {
             const double *q = fs + ((size_t)bk * kLaneF + slot) * 32;
@@ -155,10 +172,12 @@ bool launch_stats(const DevBatch &b, const DevResult &r, double *partials, doubl
     if (b.n_inst != end - begin) return false;
     const long long nl = W / parts, w0 = nl * part;  // leaf w0 starts at n_total w0 / W = begin
     cudaFuncSetAttribute(k_stats_partial, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)((size_t)kBucketGroup * (kLaneF * 32 * sizeof(double) + kStatsF * sizeof(int))));
+                         (int)((size_t)kBucketGroup * (kLaneF * 32 * sizeof(double) + 2 * sizeof(long long) +
+                                                       kStatsF * sizeof(int))));
     for (int b_lo = 0; b_lo < n_buckets; b_lo += kBucketGroup) {  // partials reused group after group
         const int nb = (n_buckets - b_lo < kBucketGroup) ? n_buckets - b_lo : kBucketGroup;
-        const size_t smem = (size_t)nb * kLaneF * 32 * sizeof(double) + (size_t)nb * kStatsF * sizeof(int);
+        const size_t smem = (size_t)nb * kLaneF * 32 * sizeof(double) + 2 * (size_t)nb * sizeof(long long) +
+                            (size_t)nb * kStatsF * sizeof(int);
         k_stats_partial<<<(unsigned)nl, 32, smem, s>>>(b, r, partials, nb, n_total, begin, w0, b_lo, n_buckets);
         const int warps = nb * kStatsF;
         k_stats_final<<<(warps * 32 + 255) / 256, 256, 0, s>>>(partials, (int)nl, nb, stats + (size_t)b_lo * kStatsF);
