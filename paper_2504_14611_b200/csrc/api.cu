@@ -181,6 +181,17 @@ int jdob_release_pool(void) {
     return JDOB_OK;
 }
 
+namespace jdob {
+int grid_divisor() {
+    static const int d = [] {
+        const char *e = getenv("JDOB_GRID_DIV");
+        const int v = e ? atoi(e) : 1;
+        return v > 1 ? v : 1;
+    }();
+    return d;
+}
+}  // namespace jdob
+
 static int num_sms() {
     int dev = 0, n = 0;
     cudaGetDevice(&dev);

@@ -739,7 +739,8 @@ static int bf_grid() {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
         if (n <= 0) n = 148;
-        const long long want = (long long)n * JDOB_BF_GRID;
+        long long want = (long long)n * JDOB_BF_GRID / grid_divisor();
+        if (want < 1) want = 1;
         return (int)(want < kBfBlocks ? want : kBfBlocks);
     }();
     return g;

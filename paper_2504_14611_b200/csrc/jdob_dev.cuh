@@ -133,6 +133,10 @@ __device__ __forceinline__ bool d8_violated(double zvN, double f, double lim) {
     return zvN / f > lim;
 }
 
+// Test hook (results independent of the grid size): the environment variable
+// JDOB_GRID_DIV = d > 1 divides the persistent grids of K1 and K2 by d.  Host-side, read once.
+int grid_divisor();
+
 // Edge grid (R7): f_e(j) = f_e,max - j*rho, one multiply then one subtract.
 __device__ __forceinline__ double grid_fe(double fe_max, double rho, long long j) {
     return __dsub_rn(fe_max, __dmul_rn((double)j, rho));

@@ -753,7 +753,8 @@ static void launch_solve_t(const DevModel *models, const DevBatch &b, const DevR
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve<COUNTS, PRUNE, UNI, VERIFY>, kSolveWarps * 32, 0);
     if (per_sm < 1) per_sm = 1;
     const long long want = (b.n_inst + kSolveWarps - 1) / kSolveWarps;
-    long long grid = (long long)num_sms * per_sm;
+    long long grid = (long long)num_sms * per_sm / grid_divisor();
+    if (grid < 1) grid = 1;
     if (want < grid) grid = want;
     k_solve<COUNTS, PRUNE, UNI, VERIFY><<<(unsigned)grid, kSolveWarps * 32, 0, s>>>(models, b, r, mode);
 }
