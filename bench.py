@@ -441,7 +441,7 @@ def run_mine(args):
     res = J.solve_batch(db, f_user=False, verify=fused)
     # this rank's root of the statistics tree over the whole job's batch (jdob_stats_part); the
     # pairwise fold over ranks (dist.fold_stats) has the bits of one GPU over the whole batch
-    part = (n_total, world, rank)
+    part = (n_total, world, rank) if world & (world - 1) == 0 else None  # jdob_stats_part: power-of-two parts
     res["stats"] = J.stats(db, res, n_buckets=n_buckets, part=part)
     # the product path's decisions for the whole batch, on the host: the cpu_baseline leg compares
     # its oracle sample with them (the only place the bench run meets the oracle)
