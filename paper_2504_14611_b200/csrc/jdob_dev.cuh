@@ -183,10 +183,12 @@ struct InstRegs {  // lane-resident user parameters (lane = user)
 // statuses are then decided in the oracle's precedence order.
 constexpr unsigned kVBad = 1u, kVInfeas = 2u, kVRequire = 4u, kNotHomog = 8u, kNotUni = 16u, kNotSameT = 32u;
 
+// tmode (K1's kernel split by deadlines): 1 = return kStDefer when the users' deadlines differ, 2 = when
+// they are all equal; tested right after the loads, before the other checks (the next kernel decides).
 __device__ __forceinline__ int warp_validate_pre(const DevModel *models, const DevBatch &b, long long i, int lane,
                                                  long long off, long long M64, int mid, InstRegs &x, int &M,
                                                  long long &k, const DevModel *&mdp, GridKCache *kc = nullptr,
-                                                 unsigned *flags = nullptr) {
+                                                 unsigned *flags = nullptr, int tmode = 0) {
     M = (M64 >= 1 && M64 <= kMaxM) ? (int)M64 : 0;
     k = 0;
     x.z = x.k = x.f0 = x.f1 = x.R = x.p = 0.0;
@@ -216,6 +218,11 @@ __device__ __forceinline__ int warp_validate_pre(const DevModel *models, const D
     if (*mdp->valid == 0) return JDOB_ST_BADMODEL;
     if (M64 < 1 || M64 > kMaxMLarge || M64 > mdp->B1 - 1) return JDOB_ST_BADPARAM;
     if (M64 > kMaxM) return kStDefer;  // more users than lanes: the block-per-instance path
+    if (tmode) {
+        const double T0 = __shfl_sync(0xffffffffu, x.T, 0);
+        const bool differ = __any_sync(0xffffffffu, lane < M && !(x.T == T0));
+        if (differ == (tmode == 1)) return kStDefer;
+    }
     bool ok = true;
     unsigned bits = 0u;
     if (lane < M) {

@@ -67,6 +67,8 @@ struct SolveSmem {
     int inv_n;
     GridKCache kc;                       // k of the last (f_e,min, f_e,max, rho)
     double rinv[kMaxM];                  // RD(1 / R_m): lower-bound upload term
+    double rg[kMaxM];                    // per sorted position p: RD(1 / (L_p - t_free)) (batch-coupled bound)
+    double lbem[64];                     // per n~: the lower bound's member term (uniform users)
     double lb[64];                       // per n~: lower bound of every configuration's energy
     // uniform users (UNI kernel, N <= kUniCache): the per-n~ values that depend only on the model and
     // the users' shared (R, zeta, f_max, kappa, f_min, p_u) -- O/R, zeta v, gamma and the lower-bound
@@ -219,7 +221,11 @@ __device__ __forceinline__ void write_local(const DevResult &r, long long i, lon
 // UNI: the instance class this kernel solves.  true = uniform users (Table I; the other instances
 // are marked kStDefer), false = the rest (only instances marked kStDefer by the first kernel).
 // Two specialised kernels keep each one's code, and so its instruction-cache footprint, small.
-template <bool COUNTS, bool PRUNE, bool UNI, bool VERIFY>
+// TIGHT (uniform kernels only): false = the kernel of equal deadlines (Table I's identical-deadline
+// setting; instances whose deadlines differ are marked kStDefer), true = the kernel of differing deadlines,
+// which adds the batch-coupled n~ bound (it prunes 43-66 % of the set-ups there, little with equal
+// deadlines, and its code costs the other kernel 6 % when compiled in).
+template <bool COUNTS, bool PRUNE, bool UNI, bool VERIFY, bool TIGHT>
 __device__ __forceinline__ void solve_instance(long long i, long long off, long long M64, int mid,
                                                const DevModel *models, const DevBatch &b, const DevResult &r,
                                                int mode, SolveSmem &s, int lane) {
@@ -229,8 +235,12 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     const DevModel *mdp;
     InstRegs x;
     unsigned vflags = 0u;
-    const int st = warp_validate_pre(models, b, i, lane, off, M64, mid, x, M, k, mdp, &s.kc, &vflags);
-    if (st == kStDefer) return;  // M > 32: solved by k_solve_large (solve_large.cu)
+    const int st = warp_validate_pre(models, b, i, lane, off, M64, mid, x, M, k, mdp, &s.kc, &vflags,
+                                     UNI ? (TIGHT ? 2 : 1) : 0);
+    if (st == kStDefer) {  // the other uniform kernel, or M > 32: k_solve_large (solve_large.cu)
+        if (UNI && lane == 0) r.status[i] = kStDefer;
+        return;
+    }
     const double t_free = x.t_free, fe_max = x.fe_max, rho = x.rho;
     if (st == JDOB_ST_BADPARAM || st == JDOB_ST_BADMODEL) {
         write_bad(r, i, off, M, mdp ? mdp->N : 0, t_free, st, lane);
@@ -292,7 +302,8 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
         return;
     }
     const bool homog = UNI ? true : homog_, uni = UNI ? true : uni_;
-    if (homog && !(vflags & kNotSameT)) {
+    // (the uniform kernels know the deadline class: equal in the first, differing in the second)
+    if (homog && (UNI ? !TIGHT : !(vflags & kNotSameT))) {
         // equal gamma and equal deadlines (Table I identical-deadline setting): the key (T asc,
         // index asc) is the index order and every suffix minimum is T
         if (lane < M) {
@@ -335,6 +346,7 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     }
 #endif
     const bool use_lb = PRUNE && mode != JDOB_MODE_BINARY;
+    const bool tight = TIGHT;  // the batch-coupled n~ bound (kernel of differing deadlines)
     if (use_lb) {
         // Lower bound of E over every configuration at n~: a member's term
         // ((kappa u) f*) f* + (O/R) p >= ((kappa u) f_min) f_min + RN(RD(O RD(1/R)) p) (f* >= f_min, RN
@@ -344,6 +356,9 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
             const double rv = uc ? 0.0 : recip_rd(R0), kv = k0, fv = f00, pv = p0;  // user 0's values
             for (int nt = lane; nt < N; nt += 32) {
                 const double em = uc ? s.uEM[nt] : (((kv * md.u[nt]) * fv) * fv) + __dmul_rd(md.O[nt], rv) * pv;
+#ifndef JDOB_NO_TIGHT_LB
+                if (TIGHT) s.lbem[nt] = em;
+#endif
                 double S = 0.0;
                 for (int m = 0; m < M; m++) {
                     const double el = s.et[m].x;
@@ -368,6 +383,9 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                 s.lb[nt] = S;
             }
         }
+#ifndef JDOB_NO_TIGHT_LB
+        if (UNI && tight && lane < M) s.rg[lane] = recip_rd(s.Lg[lane].x - t_free);  // L_p >= t_free (Require)
+#endif
         __syncwarp();
     }
     double bE;
@@ -434,6 +452,30 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                 const int nx = __ffsll((long long)cand) - 1;
                 pruned |= nx > nt + 1;
                 nt = nx;
+#ifndef JDOB_NO_TIGHT_LB
+                if (UNI && tight) {
+                    // batch-coupled bound of the candidate n~: a configuration with set start p
+                    // has the members {m : r_m >= p} (terms >= the member term em of lb) and B = M - p, and
+                    // its f_e passes the guard, f_e >= RN(phi(B) / RN(L_p - t_free)) >= g_p =
+                    // RD(phi(B) RD(1 / (L_p - t_free))); so E >= RN(S_p + RD(RD(psi(B) g_p) g_p)), S_p the
+                    // user-order RN sum of those terms.  The minimum over p bounds every configuration at
+                    // n~; the n~ is skipped when it is not below the best so far, or above E_LC (LC wins)
+                    const double em = s.lbem[nt];
+                    double lbp = dinf();
+                    if (lane < M) {
+                        double S = 0.0;
+                        for (int m = 0; m < M; m++) S = S + ((s.rank[m] >= lane) ? em : s.et[m].x);
+                        const double rg = s.rg[lane];  // +inf only when L_p = t_free: no f_e passes the guard
+                        const double g = __dmul_rd(md.phi[nt * B1 + (M - lane)], rg);
+                        if (rg != dinf()) lbp = S + __dmul_rd(__dmul_rd(md.psi[nt * B1 + (M - lane)], g), g);
+                    }
+                    const double lt = warp_min_nonneg(lbp);
+                    if (!(lt < bEw) || lt > E_lc) {
+                        pruned = true;
+                        continue;
+                    }
+                }
+#endif
 #endif
             }
             if (COUNTS) c_setup += 1;
@@ -689,7 +731,7 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
 
 // VERIFY: the instantiation with row a11 in the epilogue (r.viol != NULL); the product kernel without
 // it carries none of that code (K1's speed is sensitive to its code size)
-template <bool COUNTS, bool PRUNE, bool UNI, bool VERIFY>
+template <bool COUNTS, bool PRUNE, bool UNI, bool VERIFY, bool TIGHT>
 __global__ void __launch_bounds__(kSolveWarps * 32, UNI ? JDOB_SOLVE_MINB_U : JDOB_SOLVE_MINB)
     k_solve(const DevModel *models, DevBatch b, DevResult r, int mode) {
     __shared__ SolveSmem smem[kSolveWarps];
@@ -704,7 +746,7 @@ __global__ void __launch_bounds__(kSolveWarps * 32, UNI ? JDOB_SOLVE_MINB_U : JD
     __syncwarp();
     const long long gw = (long long)blockIdx.x * kSolveWarps + (threadIdx.x >> 5);
     const long long nw = (long long)gridDim.x * kSolveWarps;
-    if (UNI) {
+    if (UNI && !TIGHT) {
         // (user_off, user count, model id) of the warp's next instance are loaded while it solves the
         // current one, so each instance's user loads issue at once (one HBM latency less per instance)
         auto head = [&](long long i, long long &o, long long &m, int &id) {
@@ -725,45 +767,60 @@ __global__ void __launch_bounds__(kSolveWarps * 32, UNI ? JDOB_SOLVE_MINB_U : JD
 #else
             head(i, o, m, id);
 #endif
-            solve_instance<COUNTS, PRUNE, UNI, VERIFY>(i, co, cm, cid, models, b, r, mode, s, lane);
+            solve_instance<COUNTS, PRUNE, UNI, VERIFY, TIGHT>(i, co, cm, cid, models, b, r, mode, s, lane);
 #ifdef JDOB_NO_PF
             head(i + nw, o, m, id);
 #endif
         }
     } else {
-        // only the instances the uniform-users kernel left (kStDefer): 32 statuses per coalesced read
-        for (long long base = gw * 32; base < b.n_inst; base += nw * 32) {
-            const long long ii = base + lane;
-            unsigned def = __ballot_sync(0xffffffffu, ii < b.n_inst && r.status[ii] == kStDefer);
+        // only the instances the kernels before left (kStDefer), 32 statuses per load; lane l of round t
+        // looks at instance gw + (32 t + l) nw, so the deferred instances are spread over the warps as in a
+        // grid-stride loop (consecutive groups of 32 per warp left most warps idle when few groups exist)
+        for (long long base = gw; base < b.n_inst; base += 32 * nw) {
+            const long long ii = base + lane * nw;
+            const bool in = ii < b.n_inst;
+            unsigned def = __ballot_sync(0xffffffffu, in && r.status[ii] == kStDefer);
+            // the heads (user_off, user count, model id) of the group's instances, one coalesced load each,
+            // handed to the instance's solve by shuffles (no dependent load per instance)
+            long long ho = 0, hm = 0;
+            int hid = 0;
+            if (def && in) {
+                ho = b.user_off[ii];
+                hm = (b.user_end ? b.user_end[ii] : b.user_off[ii + 1]) - ho;
+                hid = b.model_id[ii];
+            }
             while (def) {
                 const int q = __ffs(def) - 1;
                 def &= def - 1u;
-                const long long ii2 = base + q, o = b.user_off[ii2];
-                const long long m = (b.user_end ? b.user_end[ii2] : b.user_off[ii2 + 1]) - o;
-                solve_instance<COUNTS, PRUNE, UNI, VERIFY>(ii2, o, m, b.model_id[ii2], models, b, r, mode, s, lane);
+                const long long o = __shfl_sync(0xffffffffu, ho, q), m = __shfl_sync(0xffffffffu, hm, q);
+                const int id = __shfl_sync(0xffffffffu, hid, q);
+                solve_instance<COUNTS, PRUNE, UNI, VERIFY, TIGHT>(base + q * nw, o, m, id, models, b, r, mode, s,
+                                                                  lane);
             }
         }
     }
 }
 
-template <bool COUNTS, bool PRUNE, bool UNI, bool VERIFY>
+template <bool COUNTS, bool PRUNE, bool UNI, bool VERIFY, bool TIGHT>
 static void launch_solve_t(const DevModel *models, const DevBatch &b, const DevResult &r, int mode, cudaStream_t s,
                            int num_sms) {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve<COUNTS, PRUNE, UNI, VERIFY>, kSolveWarps * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve<COUNTS, PRUNE, UNI, VERIFY, TIGHT>,
+                                                  kSolveWarps * 32, 0);
     if (per_sm < 1) per_sm = 1;
     const long long want = (b.n_inst + kSolveWarps - 1) / kSolveWarps;
     long long grid = (long long)num_sms * per_sm / grid_divisor();
     if (grid < 1) grid = 1;
     if (want < grid) grid = want;
-    k_solve<COUNTS, PRUNE, UNI, VERIFY><<<(unsigned)grid, kSolveWarps * 32, 0, s>>>(models, b, r, mode);
+    k_solve<COUNTS, PRUNE, UNI, VERIFY, TIGHT><<<(unsigned)grid, kSolveWarps * 32, 0, s>>>(models, b, r, mode);
 }
 
 template <bool COUNTS, bool PRUNE, bool VERIFY = false>
 static void launch_pair(const DevModel *models, const DevBatch &b, const DevResult &r, int mode, cudaStream_t s,
                         int num_sms) {
-    launch_solve_t<COUNTS, PRUNE, true, VERIFY>(models, b, r, mode, s, num_sms);   // uniform users; marks the rest
-    launch_solve_t<COUNTS, PRUNE, false, VERIFY>(models, b, r, mode, s, num_sms);  // the rest
+    launch_solve_t<COUNTS, PRUNE, true, VERIFY, false>(models, b, r, mode, s, num_sms);  // uniform, equal deadlines
+    launch_solve_t<COUNTS, PRUNE, true, VERIFY, true>(models, b, r, mode, s, num_sms);   // uniform, differing ones
+    launch_solve_t<COUNTS, PRUNE, false, VERIFY, false>(models, b, r, mode, s, num_sms); // the rest
 }
 
 void launch_solve(const DevModel *models, const DevBatch &b, const DevResult &r, int mode, cudaStream_t s,
