@@ -67,7 +67,6 @@ struct SolveSmem {
     int inv_n;
     GridKCache kc;                       // k of the last (f_e,min, f_e,max, rho)
     double rinv[kMaxM];                  // RD(1 / R_m): lower-bound upload term
-    double rg[kMaxM];                    // per sorted position p: RD(1 / (L_p - t_free)) (batch-coupled bound)
     double lbem[64];                     // per n~: the lower bound's member term (uniform users)
     double lb[64];                       // per n~: lower bound of every configuration's energy
     // uniform users (UNI kernel, N <= kUniCache): the per-n~ values that depend only on the model and
@@ -346,7 +345,6 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     }
 #endif
     const bool use_lb = PRUNE && mode != JDOB_MODE_BINARY;
-    const bool tight = TIGHT;  // the batch-coupled n~ bound (kernel of differing deadlines)
     if (use_lb) {
         // Lower bound of E over every configuration at n~: a member's term
         // ((kappa u) f*) f* + (O/R) p >= ((kappa u) f_min) f_min + RN(RD(O RD(1/R)) p) (f* >= f_min, RN
@@ -383,9 +381,6 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                 s.lb[nt] = S;
             }
         }
-#ifndef JDOB_NO_TIGHT_LB
-        if (UNI && tight && lane < M) s.rg[lane] = recip_rd(s.Lg[lane].x - t_free);  // L_p >= t_free (Require)
-#endif
         __syncwarp();
     }
     double bE;
@@ -453,21 +448,29 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                 pruned |= nx > nt + 1;
                 nt = nx;
 #ifndef JDOB_NO_TIGHT_LB
-                if (UNI && tight) {
+                // (not in the equal-deadline kernel: there it removes 28 % of C2's set-ups, mostly of the
+                // instances LC wins, but its code costs that kernel 2 % more than the set-ups it saves)
+                if (UNI && TIGHT) {
                     // batch-coupled bound of the candidate n~: a configuration with set start p
-                    // has the members {m : r_m >= p} (terms >= the member term em of lb) and B = M - p, and
-                    // its f_e passes the guard, f_e >= RN(phi(B) / RN(L_p - t_free)) >= g_p =
-                    // RD(phi(B) RD(1 / (L_p - t_free))); so E >= RN(S_p + RD(RD(psi(B) g_p) g_p)), S_p the
-                    // user-order RN sum of those terms.  The minimum over p bounds every configuration at
-                    // n~; the n~ is skipped when it is not below the best so far, or above E_LC (LC wins)
+                    // has the members {m : r_m >= p} (terms >= the member term em of lb) and B = M - p; its f_e
+                    // passes the guard, f_e >= RN(phi(B) / RN(L_p - t_free)), and the membership threshold of p,
+                    // f_e >= th_p = RN(phi(B) / RN(L_p - gamma)) (uniform users: one gamma), so f_e >= g_p =
+                    // RD(phi(B) max(RD(1 / (L_p - t_free)), RD(1 / (L_p - gamma)))) (the second only when
+                    // L_p - gamma > 0).  Hence E >= RN(S_p + RD(RD(psi(B) g_p) g_p)), S_p the user-order RN
+                    // sum of the terms.  The minimum over p bounds every configuration at n~; the n~ is
+                    // skipped when it is not below the best so far, or above E_LC (LC wins)
                     const double em = s.lbem[nt];
+                    const double gam = uc ? s.uG[nt] : dinf();  // gamma of n~ (cached for N <= 32)
                     double lbp = dinf();
                     if (lane < M) {
                         double S = 0.0;
                         for (int m = 0; m < M; m++) S = S + ((s.rank[m] >= lane) ? em : s.et[m].x);
-                        const double rg = s.rg[lane];  // +inf only when L_p = t_free: no f_e passes the guard
-                        const double g = __dmul_rd(md.phi[nt * B1 + (M - lane)], rg);
-                        if (rg != dinf()) lbp = S + __dmul_rd(__dmul_rd(md.psi[nt * B1 + (M - lane)], g), g);
+                        const double L = s.Lg[lane].x;
+                        const double r1 = recip_rd(L - t_free);  // L_p >= t_free (Require); +inf iff L_p = t_free:
+                        const double dg = L - gam;               // then no f_e passes the guard
+                        const double r2 = (dg > 0.0) ? recip_rd(dg) : 0.0;
+                        const double g = __dmul_rd(md.phi[nt * B1 + (M - lane)], (r2 > r1) ? r2 : r1);
+                        if (r1 != dinf()) lbp = S + __dmul_rd(__dmul_rd(md.psi[nt * B1 + (M - lane)], g), g);
                     }
                     const double lt = warp_min_nonneg(lbp);
                     if (!(lt < bEw) || lt > E_lc) {

@@ -91,6 +91,30 @@ def test_random_uniform_users(J, seed, M_hi, N_hi, k_max):
     assert_solve_parity(gpu, orc, counts=True)
 
 
+def test_uniform_differing_deadlines_tight_bound(J):
+    """The differing-deadline kernel's batch-coupled n~ bound: uniform users with tight
+    and loose deadlines (LC wins often, so most n~ are skipped by the bound against E_LC), a user whose
+    deadline equals t_free (L_p = t_free: no f_e passes the guard for that set start) and small t_free
+    gaps; the pruned product path, its executed-work run and the literal counters agree bit for bit,
+    and all match the oracle."""
+    b = uniformise(g.random_batch(seed=171, n_inst=2000, M_lo=2, M_hi=16, N_lo=2, N_hi=12, k_max=64), 171)
+    rng = np.random.default_rng(171)
+    for i in range(b.n_inst):
+        o0, o1 = int(b.user_off[i]), int(b.user_off[i + 1])
+        lat = b.T[o0:o1].min()
+        r = rng.uniform()
+        if r < 0.3:    # tight: beta in [0, 0.6]
+            b.T[o0:o1] = lat * (1.0 + rng.uniform(0.0, 0.6, o1 - o0))
+        if r > 0.8:    # one user's deadline equals t_free (> 0)
+            b.t_free[i] = 0.25 * b.T[o0:o1].min()
+            b.T[o0 + int(rng.integers(0, o1 - o0))] = b.t_free[i]
+    b.T[b.user_off[0]:b.user_off[1]] = np.linspace(1.0, 2.0, b.M(0)) * b.T[b.user_off[0]]  # differing
+    _, gpu = run(J, b)
+    orc = O.solve_batch(b, counts=True)
+    assert_solve_parity(gpu, orc, counts=True)
+    assert (gpu["n_tilde"] == np.array([b.models[m].N for m in b.model_id])).mean() > 0.05  # LC wins often
+
+
 @pytest.mark.parametrize("uniform", [False, True])
 def test_grid_length_cache(J, uniform):
     """K1 caches k per warp keyed by (f_e,min, f_e,max, rho): instances that share f_e,max and rho but
