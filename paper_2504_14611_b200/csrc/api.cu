@@ -243,6 +243,9 @@ uint64_t jdob_bf_space_size(int32_t space, int32_t N, int32_t M, int64_t k) {
     return s;
 }
 
+static int solve_prepared(const jdob_model *models, int32_t n_models, const DevModel *dm, const jdob_batch *b,
+                          int32_t mode, const jdob_result *out, void *ws, cudaStream_t s);
+
 int jdob_solve_batch(const jdob_model *models, int32_t n_models, const jdob_batch *b, int32_t mode,
                      const jdob_result *out, void *ws, size_t ws_bytes, void *stream) {
     NvtxRange nvtx_("jdob_solve_batch");
@@ -264,6 +267,13 @@ int jdob_solve_batch(const jdob_model *models, int32_t n_models, const jdob_batc
     cudaStream_t s = (cudaStream_t)stream;
     DevModel *dm = nullptr;
     if ((rc = prepare_models(models, n_models, (char *)ws, &dm, s))) return rc;
+    return solve_prepared(models, n_models, dm, b, mode, out, ws, s);
+}
+
+// jdob_solve_batch after the model tables are prepared (K0) in ws: K1 (+ K1L), optional K4
+static int solve_prepared(const jdob_model *models, int32_t n_models, const DevModel *dm, const jdob_batch *b,
+                          int32_t mode, const jdob_result *out, void *ws, cudaStream_t s) {
+    int rc = JDOB_OK;
     DevBatch db = to_dev(b);
     DevResult dr;
     dr.E = out->E;
@@ -550,6 +560,37 @@ __global__ void k_expand_shared(long long n, const long long *user_off, const do
     }
 }
 
+// The host API's copy-in, compute and copy-out streams and its events, created once per device (the
+// host API's calls on one device are serialised through them; each call joins them into the caller's
+// stream before it returns).
+struct HostStreams {
+    static constexpr int kMaxChunks = 70;
+    cudaStream_t h2d, compute, d2h;
+    cudaEvent_t start, hdone, kdone, ddone, in[kMaxChunks], solved[kMaxChunks];
+};
+static HostStreams g_hs[64];
+static bool g_hs_made[64];
+
+static HostStreams &host_streams() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    HostStreams &h = g_hs[dev];
+    if (!g_hs_made[dev]) {
+        cudaStreamCreateWithFlags(&h.h2d, cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&h.compute, cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&h.d2h, cudaStreamNonBlocking);
+        cudaEvent_t *ev[4] = {&h.start, &h.hdone, &h.kdone, &h.ddone};
+        for (auto e : ev) cudaEventCreateWithFlags(e, cudaEventDisableTiming);
+        for (int c = 0; c < HostStreams::kMaxChunks; c++) {
+            cudaEventCreateWithFlags(&h.in[c], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&h.solved[c], cudaEventDisableTiming);
+        }
+        g_hs_made[dev] = true;
+    }
+    return h;
+}
+
 // jdob_solve_batch_host and jdob_solve_shared_host: exactly one of b (users as arrays) and sb (users
 // sharing their device parameters within an instance) is given
 static int solve_host_impl(const jdob_model *models, int32_t n_models, const jdob_batch *b_full,
@@ -597,11 +638,7 @@ static int solve_host_impl(const jdob_model *models, int32_t n_models, const jdo
     const long long n = b->n_inst;
     if (n > 0 && b->user_off[0] < 0) return fail(JDOB_EINVAL, "user_off[0] = %lld < 0", (long long)b->user_off[0]);
     const long long nu = n > 0 ? (long long)b->user_off[n] : 0;
-#ifndef JDOB_HOST_NS
-#define JDOB_HOST_NS 4
-#endif
-    constexpr int NS = JDOB_HOST_NS;  // copy/compute pipeline depth
-    // device layout: model tables | batch | outputs | NS workspaces
+    // device layout: model tables | batch | outputs | workspace
     size_t bytes = 0;
     for (int i = 0; i < n_models; i++) {
         const size_t n1 = (size_t)models[i].N + 1, b1 = (size_t)models[i].B_max + 1;
@@ -614,7 +651,7 @@ static int solve_host_impl(const jdob_model *models, int32_t n_models, const jdo
                         (out->counts ? al(n * 3 * 8) : 0) +
                         (out->stats ? al((size_t)out->n_buckets * JDOB_STATS_FIELDS * 8) : 0);
     const size_t wsb = jdob_workspace_bytes(models, n_models, 0);
-    bytes += in_inst + in_user + outb + NS * al(wsb);
+    bytes += in_inst + in_user + outb + al(wsb);
     char *base = nullptr;
     if ((pool ? cudaMallocFromPoolAsync((void **)&base, bytes, pool, s) : cudaMallocAsync((void **)&base, bytes, s)) !=
         cudaSuccess)
@@ -683,19 +720,27 @@ static int solve_host_impl(const jdob_model *models, int32_t n_models, const jdo
     dr.partition = out->partition ? (int32_t *)take(nu * 4) : nullptr;
     dr.work = nullptr;  // device-API diagnostic only
     dr.violations = nullptr;
-    void *ws[NS];
-    for (int k = 0; k < NS; k++) ws[k] = take(wsb);
+    void *ws = take(wsb);
 
-    // pipeline: chunk c copies in, solves and copies out on stream c % NS, so the copies of one
-    // chunk overlap the solve of the other (copy engines and SMs run concurrently)
-    cudaStream_t st[NS];
-    cudaEvent_t ev0, evs[NS];
-    cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming);
-    cudaEventRecord(ev0, s);
-    for (int k = 0; k < NS; k++) {
-        cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking);
-        cudaEventCreateWithFlags(&evs[k], cudaEventDisableTiming);
-        cudaStreamWaitEvent(st[k], ev0, 0);
+    // pipeline on three streams of the library (HostStreams): the copy-ins of every chunk back to back on
+    // one stream, each chunk's solve on a second stream once its copy-ins are done, its copy-outs on a
+    // third once its solve is done -- the H2D engine never waits for a solve or a copy-out, and the solve
+    // of chunk c overlaps the copy-ins of the chunks after it and the copy-outs of those before it
+    HostStreams &hs = host_streams();
+    cudaStream_t sh = hs.h2d, sk = hs.compute, sd = hs.d2h;
+    cudaEventRecord(hs.start, s);
+    cudaStreamWaitEvent(sh, hs.start, 0);
+    cudaStreamWaitEvent(sk, hs.start, 0);
+    cudaStreamWaitEvent(sd, hs.start, 0);
+    // the model tables were copied on s (above): K0 runs once on the compute stream, every chunk's solve
+    // uses its tables
+    DevModel *dmod = nullptr;
+    if ((rc = prepare_models(dm, n_models, (char *)ws, &dmod, sk))) {
+        cudaEventRecord(hs.kdone, sk);
+        cudaStreamWaitEvent(s, hs.kdone, 0);
+        cudaFreeAsync(base, s);
+        if (dm != dmods) delete[] dm;
+        return rc;
     }
 #ifndef JDOB_HOST_CHUNK
 #define JDOB_HOST_CHUNK 131072
@@ -704,21 +749,20 @@ static int solve_host_impl(const jdob_model *models, int32_t n_models, const jdo
     // that the solve and copy-out left after the last copy-in are short
     long long per = JDOB_HOST_CHUNK;
     if (n > 48 * per) per = (n + 47) / 48;
-    long long bounds[72];
+    long long bounds[HostStreams::kMaxChunks + 2];
     int nchunks = 0;
     bounds[0] = 0;
-    for (long long pos = 0; pos < n && nchunks < 70;) {
+    for (long long pos = 0; pos < n && nchunks < HostStreams::kMaxChunks;) {
         const long long rem = n - pos;
         long long sz = per;
 #ifndef JDOB_HOST_NO_TAIL
         if (rem <= 2 * per) sz = (rem / 2 > 16384) ? rem / 2 : 16384;
 #endif
-        if (sz > rem || nchunks == 69) sz = rem;
+        if (sz > rem || nchunks == HostStreams::kMaxChunks - 1) sz = rem;
         pos += sz;
         bounds[++nchunks] = pos;
     }
     for (int c = 0; c < nchunks && rc == JDOB_OK; c++) {
-        cudaStream_t ss = st[c % NS];
         const long long i0 = bounds[c], i1 = bounds[c + 1];
         if (i1 <= i0) continue;
         // the host offsets size this chunk's copies: a decreasing pair would wrap a byte count, so
@@ -731,9 +775,9 @@ static int solve_host_impl(const jdob_model *models, int32_t n_models, const jdo
             break;
         }
         const long long u0 = b->user_off[i0], u1 = b->user_off[i1];
-        // the chunk's copy-ins: one cudaMemcpyAsync per array on the chunk's stream
+        // the chunk's copy-ins: one cudaMemcpyAsync per array on the copy-in stream
         auto h2 = [&](const void *dst, const void *src, size_t nb) {
-            if (nb) cudaMemcpyAsync((void *)dst, src, nb, cudaMemcpyHostToDevice, ss);
+            if (nb) cudaMemcpyAsync((void *)dst, src, nb, cudaMemcpyHostToDevice, sh);
             h2d += (long long)nb;
         };
         h2(db.model_id + i0, b->model_id + i0, (i1 - i0) * 4);
@@ -747,8 +791,10 @@ static int solve_host_impl(const jdob_model *models, int32_t n_models, const jdo
         }
         for (int t = 0; t < 4; t++) h2(*inf[t] + i0, ih[t] + i0, (i1 - i0) * 8);
         if (b->bucket) h2(db.bucket + i0, b->bucket + i0, (i1 - i0) * 4);
+        cudaEventRecord(hs.in[c], sh);
+        cudaStreamWaitEvent(sk, hs.in[c], 0);
         if (shared)  // the users' arrays of this chunk from the instances' shared values
-            k_expand_shared<<<(unsigned)(((i1 - i0) * 32 + 255) / 256), 256, 0, ss>>>(
+            k_expand_shared<<<(unsigned)(((i1 - i0) * 32 + 255) / 256), 256, 0, sk>>>(
                 i1 - i0, (const long long *)db.user_off + i0, sh_dev[0] + i0, sh_dev[1] + i0, sh_dev[2] + i0,
                 sh_dev[3] + i0, sh_dev[4] + i0, sh_dev[5] + i0, (double *)db.zeta, (double *)db.kappa,
                 (double *)db.f_min, (double *)db.f_max, (double *)db.R, (double *)db.p_u);
@@ -772,10 +818,12 @@ static int solve_host_impl(const jdob_model *models, int32_t n_models, const jdo
         cr.mask = dr.mask + i0;
         cr.counts = dr.counts ? dr.counts + 3 * i0 : nullptr;
         cr.stats = nullptr;
-        rc = jdob_solve_batch(dm, n_models, &cb, mode, &cr, ws[c % NS], wsb, (void *)ss);
+        rc = solve_prepared(dm, n_models, dmod, &cb, mode, &cr, ws, sk);
         if (rc != JDOB_OK) break;
+        cudaEventRecord(hs.solved[c], sk);
+        cudaStreamWaitEvent(sd, hs.solved[c], 0);
         auto d2 = [&](void *dst, const void *src, size_t nb) {
-            if (nb) cudaMemcpyAsync(dst, src, nb, cudaMemcpyDeviceToHost, ss);
+            if (nb) cudaMemcpyAsync(dst, src, nb, cudaMemcpyDeviceToHost, sd);
             d2h += (long long)nb;
         };
         d2(out->E + i0, cr.E, (i1 - i0) * 8);
@@ -790,10 +838,13 @@ static int solve_host_impl(const jdob_model *models, int32_t n_models, const jdo
         if (out->partition) d2(out->partition + u0, dr.partition + u0, (u1 - u0) * 4);
         if (out->counts) d2(out->counts + 3 * i0, cr.counts, (i1 - i0) * 3 * 8);
     }
-    for (int k = 0; k < NS; k++) {
-        cudaEventRecord(evs[k], st[k]);
-        cudaStreamWaitEvent(s, evs[k], 0);
-    }
+    // join: s waits for the three streams (the copy-in stream's work precedes every solve it fed)
+    cudaEventRecord(hs.hdone, sh);
+    cudaEventRecord(hs.kdone, sk);
+    cudaEventRecord(hs.ddone, sd);
+    cudaStreamWaitEvent(s, hs.hdone, 0);
+    cudaStreamWaitEvent(s, hs.kdone, 0);
+    cudaStreamWaitEvent(s, hs.ddone, 0);
     if (rc == JDOB_OK && out->stats && n > 0) {
         DevResult r2;
         r2.E = dr.E;
@@ -807,7 +858,7 @@ static int solve_host_impl(const jdob_model *models, int32_t n_models, const jdo
         r2.f_user = dr.f_user;
         r2.counts = (long long *)dr.counts;
         r2.partition = dr.partition;
-        double *partials = (double *)((char *)ws[0] + models_bytes(models, n_models));
+        double *partials = (double *)((char *)ws + models_bytes(models, n_models));
         launch_stats(to_dev(&db), r2, partials, dr.stats, out->n_buckets, n, 1, 0, s);
         cudaMemcpyAsync(out->stats, dr.stats, (size_t)out->n_buckets * JDOB_STATS_FIELDS * 8,
                         cudaMemcpyDeviceToHost, s);
@@ -816,11 +867,6 @@ static int solve_host_impl(const jdob_model *models, int32_t n_models, const jdo
     if (dm != dmods) delete[] dm;
     cudaFreeAsync(base, s);
     cudaError_t e = cudaStreamSynchronize(s);
-    for (int k = 0; k < NS; k++) {
-        cudaStreamDestroy(st[k]);
-        cudaEventDestroy(evs[k]);
-    }
-    cudaEventDestroy(ev0);
     if (rc != JDOB_OK) return rc;
     if (e != cudaSuccess) return fail(JDOB_ECUDA, "solve_batch_host: %s", cudaGetErrorString(e));
     if (h2d_bytes) *h2d_bytes = h2d;
