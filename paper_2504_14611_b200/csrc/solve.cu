@@ -68,6 +68,7 @@ struct SolveSmem {
     GridKCache kc;                       // k of the last (f_e,min, f_e,max, rho)
     double rinv[kMaxM];                  // RD(1 / R_m): lower-bound upload term
     double lbem[64];                     // per n~: the lower bound's member term (uniform users)
+    double pre[kMaxM + 1];               // equal-deadline kernel: P[p] = user-order sum of the first p e_loc
     double lb[64];                       // per n~: lower bound of every configuration's energy
     // uniform users (UNI kernel, N <= kUniCache): the per-n~ values that depend only on the model and
     // the users' shared (R, zeta, f_max, kappa, f_min, p_u) -- O/R, zeta v, gamma and the lower-bound
@@ -227,7 +228,8 @@ __device__ __forceinline__ void write_local(const DevResult &r, long long i, lon
 template <bool COUNTS, bool PRUNE, bool UNI, bool VERIFY, bool TIGHT>
 __device__ __forceinline__ void solve_instance(long long i, long long off, long long M64, int mid,
                                                const DevModel *models, const DevBatch &b, const DevResult &r,
-                                               int mode, SolveSmem &s, int lane) {
+                                               int mode, SolveSmem &s, int lane, long long nx_off = 0,
+                                               long long nx_M = 0) {
     __syncwarp();
     long long k;
     int M;
@@ -236,6 +238,25 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     unsigned vflags = 0u;
     const int st = warp_validate_pre(models, b, i, lane, off, M64, mid, x, M, k, mdp, &s.kc, &vflags,
                                      UNI ? (TIGHT ? 2 : 1) : 0);
+#ifndef JDOB_L1PF
+#define JDOB_L1PF 1
+#endif
+#if JDOB_L1PF
+    // the next instance's users (nx_off, nx_M: the head the kernel loop loaded ahead) are pulled toward the
+    // SM while this one is solved, so its validation loads hit the cache
+    if (lane < nx_M && nx_M <= kMaxM) {
+        const long long u = nx_off + lane;
+        const double *pp[7] = {b.zeta + u, b.kappa + u, b.f_min + u, b.f_max + u, b.R + u, b.p_u + u, b.T + u};
+#pragma unroll
+        for (int q = 0; q < 7; q++) {
+#if JDOB_L1PF == 2
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(pp[q]));
+#else
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(pp[q]));
+#endif
+        }
+    }
+#endif
     if (st == kStDefer) {  // the other uniform kernel, or M > 32: k_solve_large (solve_large.cu)
         if (UNI && lane == 0) r.status[i] = kStDefer;
         return;
@@ -267,7 +288,12 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     s.T[lane] = x.T;  // +inf beyond M
     __syncwarp();
     double E_lc = 0.0;
-    for (int t = 0; t < M; t++) E_lc = E_lc + s.et[t].x;  // user-index order
+    for (int t = 0; t < M; t++) {
+        E_lc = E_lc + s.et[t].x;  // user-index order
+#ifndef JDOB_NO_PREFIX
+        if (UNI && !TIGHT && lane == 0) s.pre[t + 1] = E_lc;  // P[t + 1]: the sum of the first t + 1 terms
+#endif
+    }
     if (st != JDOB_ST_OK || mode == JDOB_MODE_LC) {
         write_local(r, i, off, M, N, E_lc, t_free, floc, st, lane, true);
         if (VERIFY) {
@@ -549,11 +575,26 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                         fB = clampf(a0.y / budB, t0.x, t0.y);
                     const double emA = ((c0.x * fA) * fA) + c0.y;  // D21 offloader term
                     const double emB = ((c0.x * fB) * fB) + c0.y;
+#ifndef JDOB_NO_PREFIX
+                    if (!TIGHT) {
+                        // equal deadlines: the ranks are the user indices, so the members are the users
+                        // m >= p (thresholds non-increasing from i^) and the user-order sum is the prefix
+                        // P[p] of the e_loc terms (formed with E_LC) followed by M - p member terms
+                        EA = s.pre[pA];
+                        EB = s.pre[pB];
+                        for (int m = (pA < pB) ? pA : pB; m < M; m++) {
+                            if (m >= pA) EA = EA + emA;
+                            if (m >= pB) EB = EB + emB;
+                        }
+                    } else
+#endif
+                    {
 #pragma unroll 4
-                    for (int m = 0; m < M; m++) {
-                        const double2 et = s.et[m];  // eloc, thu
-                        EA = EA + ((!(feA < et.y)) ? emA : et.x);
-                        EB = EB + ((!(feB < et.y)) ? emB : et.x);
+                        for (int m = 0; m < M; m++) {
+                            const double2 et = s.et[m];  // eloc, thu
+                            EA = EA + ((!(feA < et.y)) ? emA : et.x);
+                            EB = EB + ((!(feB < et.y)) ? emB : et.x);
+                        }
                     }
                 } else {
                     const long long fbA = __double_as_longlong(feA), fbB = __double_as_longlong(feB);
@@ -745,6 +786,7 @@ __global__ void __launch_bounds__(kSolveWarps * 32, UNI ? JDOB_SOLVE_MINB_U : JD
         s.inv_n = 0;
         s.kc = GridKCache{0.0, 0.0, 0.0, 0};  // rho > 0 in every valid instance: no false hit
         s.ukey[0] = -1;                       // no model id -1: no false hit
+        s.pre[0] = 0.0;
     }
     __syncwarp();
     const long long gw = (long long)blockIdx.x * kSolveWarps + (threadIdx.x >> 5);
@@ -770,7 +812,8 @@ __global__ void __launch_bounds__(kSolveWarps * 32, UNI ? JDOB_SOLVE_MINB_U : JD
 #else
             head(i, o, m, id);
 #endif
-            solve_instance<COUNTS, PRUNE, UNI, VERIFY, TIGHT>(i, co, cm, cid, models, b, r, mode, s, lane);
+            solve_instance<COUNTS, PRUNE, UNI, VERIFY, TIGHT>(i, co, cm, cid, models, b, r, mode, s, lane,
+                                                              i + nw < b.n_inst ? o : 0, i + nw < b.n_inst ? m : 0);
 #ifdef JDOB_NO_PF
             head(i + nw, o, m, id);
 #endif
