@@ -616,7 +616,7 @@ def run_mine(args):
                                 "jdob_solve_batch (K0+K1) + jdob_stats (K4) + jdob_eval of every plan (K3)")
                                + (" + NCCL stats allreduce" if dist else ""),
                        "parallelism": f"dp{world}"},
-            "roofline": {"bound": "alu", "kernel": "k_solve (K1)", "unit": "G FP64-pipe instr/s",
+            "roofline": {"bound": "alu", "kernel": "k_solve<0,1,1,0,0> (K1, equal-deadline uniform-users kernel)", "unit": "G FP64-pipe instr/s",
                          # the measured executed rate when the committed ncu record of this launch exists
                          "achieved": (ncu_exec or executed)["achieved"], "peak": peak,
                          "frac": (ncu_exec or executed)["frac"],
@@ -641,7 +641,7 @@ def run_mine(args):
                                       "this launch (profiles/) over the live time"},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": (5 if fused else 6) * K,
+            "gpu_launches": (6 if fused else 7) * K,  # K0, K1 x3 (equal / differing deadlines, general), K4 x2, K3
             "clocks": clk,
             "bruteforce": bf,
             "plan_violations": viol,

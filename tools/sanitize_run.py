@@ -46,5 +46,10 @@ g5 = J.DeviceBatch.generate_c5(models, params, 3000)
 J.solve_batch(g5, stats=True, n_buckets=480)
 hb = J.HostBuffers(c, stats=True, n_buckets=3)
 J.solve_batch_host(hb)
+c2 = G.config_batch("c2", n_inst=300)                # equal-deadline uniform kernel, K3 windows
+d2 = J.DeviceBatch(c2)
+r2 = J.solve_batch(d2, stats=True, n_buckets=7)
+J.eval_plans(d2, plans=r2, f_user=False)
+J.solve_batch_host(J.HostBuffers(c2, stats=True, n_buckets=7, shared=True))
 torch.cuda.synchronize()
 print("sanitize run ok")
