@@ -616,7 +616,8 @@ def run_mine(args):
                                 "jdob_solve_batch (K0+K1) + jdob_stats (K4) + jdob_eval of every plan (K3)")
                                + (" + NCCL stats allreduce" if dist else ""),
                        "parallelism": f"dp{world}"},
-            "roofline": {"bound": "alu", "kernel": "k_solve<0,1,1,0,0> (K1, equal-deadline uniform-users kernel)", "unit": "G FP64-pipe instr/s",
+            "roofline": {"bound": "alu", "kernel": ("k_solve<0,1,1,0,0> (K1, equal-deadline uniform-users kernel)" if default_c2 else
+                                    "k_solve (K1: equal-deadline, differing-deadline and general kernels)"), "unit": "G FP64-pipe instr/s",
                          # the measured executed rate when the committed ncu record of this launch exists
                          "achieved": (ncu_exec or executed)["achieved"], "peak": peak,
                          "frac": (ncu_exec or executed)["frac"],

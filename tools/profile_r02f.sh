@@ -1,8 +1,8 @@
 #!/bin/bash
 # Round-2 final profiling pass (one B200 under gpurun), after the K1 kernel split and the staged K3:
 # launch list of the bench step, ncu --set full (+ FP64 instruction counters) of K1 (equal-deadline
-# kernel on C2, differing-deadline kernel on C3 and C5), K2 (full C4), K3, K4, compute-sanitizer over
-# tools/sanitize_run.py.  Outputs in $OUT (default gpurun_out/r02f).  The bench lines are a second pass
+# kernel on C2, differing-deadline kernel on C3 and C5), K2 (full C4), K3, K4, (no compute-sanitizer:
+# closed on the pool).  Outputs in $OUT (default gpurun_out/r02f).  The bench lines are a second pass
 # (tools/bench_r02f.sh) once profiles/ncu_traffic.json holds this capture's counters.
 set -x
 OUT=${OUT:-gpurun_out/r02f}
@@ -28,9 +28,6 @@ timeout 600 ncu --set full $X --clock-control none --import-source on -k regex:k
     python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --no-bf > $OUT/prof_eval.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_stats_partial -c 1 -o $OUT/prof_stats -f \
     python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --no-bf > $OUT/prof_stats.log 2>&1
-if [ -z "$NOSAN" ]; then
-for tool in memcheck racecheck synccheck initcheck; do
-    timeout 900 compute-sanitizer --tool $tool python tools/sanitize_run.py > $OUT/sanitize_$tool.txt 2>&1
-done
-fi
+# (compute-sanitizer is closed on the GPU pool since this pass was written: profiles/r02_compute_sanitizer.txt
+# is the earlier r02s capture)
 ls -la $OUT
