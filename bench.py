@@ -633,8 +633,9 @@ def run_mine(args):
                          "literal_member_evals_per_launch": n_member,
                          "n_tilde_setups_frac": setup_frac,
                          "launch_ms": solve_ms,
-                         "peak_note": PEAK_NOTE + "; launch_ms = CUDA events around jdob_solve_batch (K0 + K1; "
-                                      "K0 is one block per model, < 0.3 % of the launch list); literal = SURVEY "
+                         "peak_note": PEAK_NOTE + "; launch_ms = CUDA events around jdob_solve_batch (K0 + the three "
+                                      "K1 kernels; on C2 the equal-deadline kernel is 99 % of it, K0 and the "
+                                      "other two kernels' status scans about 1 %); literal = SURVEY "
                                       "§8(d)'s Alg. 1/2 work (every n~ swept, oracle-checked counters) with a "
                                       "division weighted w_div FP64-pipe instructions, > 1 is the pruning's "
                                       "signature; executed = the work the pruned sweep ran (its counters, same "
