@@ -229,7 +229,7 @@ template <bool COUNTS, bool PRUNE, bool UNI, bool VERIFY, bool TIGHT>
 __device__ __forceinline__ void solve_instance(long long i, long long off, long long M64, int mid,
                                                const DevModel *models, const DevBatch &b, const DevResult &r,
                                                int mode, SolveSmem &s, int lane, long long nx_off = 0,
-                                               long long nx_M = 0) {
+                                               long long nx_end = 0) {
     __syncwarp();
     long long k;
     int M;
@@ -242,8 +242,9 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
 #define JDOB_L1PF 1
 #endif
 #if JDOB_L1PF
-    // the next instance's users (nx_off, nx_M: the head the kernel loop loaded ahead) are pulled toward the
-    // SM while this one is solved, so its validation loads hit the cache
+    // the next instance's users (nx_off, nx_end: the head the kernel loop loaded ahead) are pulled toward
+    // the SM while this one is solved, so its validation loads hit the cache
+    const long long nx_M = nx_end - nx_off;
     if (lane < nx_M && nx_M <= kMaxM) {
         const long long u = nx_off + lane;
         const double *pp[7] = {b.zeta + u, b.kappa + u, b.f_min + u, b.f_max + u, b.R + u, b.p_u + u, b.T + u};
@@ -384,9 +385,14 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                 if (TIGHT) s.lbem[nt] = em;
 #endif
                 double S = 0.0;
-                for (int m = 0; m < M; m++) {
-                    const double el = s.et[m].x;
-                    S = S + ((em < el) ? em : el);
+                if (!TIGHT) {  // equal deadlines: every user's e_loc is the same bits (identical inputs)
+                    const double el = s.et[0].x, t = (em < el) ? em : el;
+                    for (int m = 0; m < M; m++) S = S + t;
+                } else {
+                    for (int m = 0; m < M; m++) {
+                        const double el = s.et[m].x;
+                        S = S + ((em < el) ? em : el);
+                    }
                 }
                 s.lb[nt] = S;
             }
@@ -794,29 +800,25 @@ __global__ void __launch_bounds__(kSolveWarps * 32, UNI ? JDOB_SOLVE_MINB_U : JD
     if (UNI && !TIGHT) {
         // (user_off, user count, model id) of the warp's next instance are loaded while it solves the
         // current one, so each instance's user loads issue at once (one HBM latency less per instance)
-        auto head = [&](long long i, long long &o, long long &m, int &id) {
+        // (the user count is formed when the instance starts, not next to the loads: the subtraction
+        // would wait for them there)
+        auto head = [&](long long i, long long &o, long long &e, int &id) {
             if (i < b.n_inst) {
                 o = b.user_off[i];
-                m = (b.user_end ? b.user_end[i] : b.user_off[i + 1]) - o;
+                e = b.user_end ? b.user_end[i] : b.user_off[i + 1];
                 id = b.model_id[i];
             }
         };
-        long long o = 0, m = 0;
+        long long o = 0, e = 0;
         int id = 0;
-        head(gw, o, m, id);
+        head(gw, o, e, id);
         for (long long i = gw; i < b.n_inst; i += nw) {
-            const long long co = o, cm = m;
+            const long long co = o, cm = e - o;
             const int cid = id;
-#ifndef JDOB_NO_PF
-            head(i + nw, o, m, id);
-#else
-            head(i, o, m, id);
-#endif
+            head(i + nw, o, e, id);
+            const bool nx = i + nw < b.n_inst;
             solve_instance<COUNTS, PRUNE, UNI, VERIFY, TIGHT>(i, co, cm, cid, models, b, r, mode, s, lane,
-                                                              i + nw < b.n_inst ? o : 0, i + nw < b.n_inst ? m : 0);
-#ifdef JDOB_NO_PF
-            head(i + nw, o, m, id);
-#endif
+                                                              nx ? o : 0, nx ? e : 0);
         }
     } else {
         // only the instances the kernels before left (kStDefer), 32 statuses per load; lane l of round t
