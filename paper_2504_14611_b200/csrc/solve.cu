@@ -122,8 +122,10 @@ __device__ __noinline__ void sort_users_T(int M, double T, SolveSmem &s, int lan
 }
 
 // Alg. 1 lines 4-6 for partition point nt.  Returns i^ (M if none).
+// need_et = false: the caller does not read the per-user thresholds et.y (the equal-deadline kernel sums
+// members from the prefix P[p]).
 __device__ __forceinline__ int setup_nt(const DevModel &md, int nt, int M, bool homog, bool uni, double t_free,
-                                        SolveSmem &s, int lane, bool uc = false) {
+                                        SolveSmem &s, int lane, bool uc = false, bool need_et = true) {
     const double v_nt = md.v[nt], u_nt = md.u[nt], O_nt = md.O[nt];
     double gam = 0.0;
     if (lane < M) {
@@ -135,7 +137,7 @@ __device__ __forceinline__ int setup_nt(const DevModel &md, int nt, int M, bool 
             s.orzv[lane] = make_double2(OR, zv);
             s.kuup[lane] = make_double2(s.kap[lane] * u_nt, OR * s.pu[lane]);  // Eq. (4)
         }
-        s.gam[lane] = gam;
+        if (!homog) s.gam[lane] = gam;  // (homogeneous: every user's gamma is this lane's)
     }
     if (!homog) sort_users(M, gam, s.T[lane], s, lane);  // homogeneous: order fixed per instance
     double th = 0.0;
@@ -151,11 +153,13 @@ __device__ __forceinline__ int setup_nt(const DevModel &md, int nt, int M, bool 
     const unsigned nn = __ballot_sync(0xffffffffu, lane < M && th >= 0.0);
     const int ihat = nn ? (__ffs(nn) - 1) : M;
     __syncwarp();
-    if (lane < M) {
-        const int rm = s.rank[lane];
-        s.et[lane].y = (rm >= ihat) ? s.th[rm] : dinf();
+    if (need_et) {
+        if (lane < M) {
+            const int rm = s.rank[lane];
+            s.et[lane].y = (rm >= ihat) ? s.th[rm] : dinf();
+        }
+        __syncwarp();
     }
-    __syncwarp();
     return ihat;
 }
 
@@ -267,6 +271,13 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
         write_bad(r, i, off, M, mdp ? mdp->N : 0, t_free, st, lane);
         return;
     }
+    // the uniform kernels leave non-uniform instances, whatever their status, to the general kernel
+    const bool homog_ = !(vflags & kNotHomog);
+    const bool uni_ = homog_ && !(vflags & kNotUni);
+    if (UNI && !uni_) {
+        if (lane == 0) r.status[i] = kStDefer;
+        return;
+    }
     const DevModel &md = *mdp;
     const int N = md.N;
     const double vN = md.v[N], uN = md.u[N];
@@ -289,8 +300,11 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     s.T[lane] = x.T;  // +inf beyond M
     __syncwarp();
     double E_lc = 0.0;
+    // equal-deadline kernel (uniform users, equal deadlines): every user's e_loc is the same bits
+    const bool same_el = UNI && !TIGHT;
+    const double el0 = __shfl_sync(0xffffffffu, eloc, 0);
     for (int t = 0; t < M; t++) {
-        E_lc = E_lc + s.et[t].x;  // user-index order
+        E_lc = E_lc + (same_el ? el0 : s.et[t].x);  // user-index order
 #ifndef JDOB_NO_PREFIX
         if (UNI && !TIGHT && lane == 0) s.pre[t + 1] = E_lc;  // P[t + 1]: the sum of the first t + 1 terms
 #endif
@@ -320,13 +334,7 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     // instance-level flags (warp-uniform)
     const double R0 = s.R[0], z0 = s.z[0], f10 = s.f1[0];  // user 0's values
     // (from the validation's single warp reduction)
-    const bool homog_ = !(vflags & kNotHomog);
     const double f00 = s.fmm[0].x, k0 = s.kap[0], p0 = s.pu[0];
-    const bool uni_ = homog_ && !(vflags & kNotUni);
-    if (UNI && !uni_) {  // left to the general kernel
-        if (lane == 0) r.status[i] = kStDefer;
-        return;
-    }
     const bool homog = UNI ? true : homog_, uni = UNI ? true : uni_;
     // (the uniform kernels know the deadline class: equal in the first, differing in the second)
     if (homog && (UNI ? !TIGHT : !(vflags & kNotSameT))) {
@@ -515,7 +523,7 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
             }
             if (COUNTS) c_setup += 1;
             last_nt = nt;
-            const int ihat = setup_nt(md, nt, M, homog, uni, t_free, s, lane, uc);
+            const int ihat = setup_nt(md, nt, M, homog, uni, t_free, s, lane, uc, !(UNI && !TIGHT));
             // two grid points per lane (j0 + lane and j0 + 32 + lane): the two energy chains are
             // independent, which doubles the instruction-level parallelism of the sweep and lets both
             // share each user's shared-memory loads
