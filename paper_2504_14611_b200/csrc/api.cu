@@ -62,6 +62,8 @@ static int check_models(const jdob_model *models, int32_t n_models) {
     return JDOB_OK;
 }
 
+constexpr size_t kFlagBytes = 2 * sizeof(int);  // K1's deferral flags, after the statistics partials
+
 static size_t models_bytes(const jdob_model *models, int32_t n_models) {
     size_t s = al((size_t)n_models * sizeof(DevModel));
     for (int i = 0; i < n_models; i++) s += model_table_bytes(models[i]);
@@ -219,7 +221,7 @@ size_t jdob_workspace_bytes(const jdob_model *models, int32_t n_models, int32_t 
             models[i].B_max > JDOB_MAX_M_LARGE)
             return 0;
     size_t s = models_bytes(models, n_models);
-    if (which == 0) return s + stats_partial_bytes();
+    if (which == 0) return s + stats_partial_bytes() + al(kFlagBytes);  // + K1's deferral flags
     if (which == 1) return s + al(bf_workspace_bytes());
     return 0;
 }
@@ -290,6 +292,8 @@ static int solve_prepared(const jdob_model *models, int32_t n_models, const DevM
     dr.work = (long long *)out->work;
     dr.viol = out->violations;
     dr.slack = out->slack;
+    dr.flags = (int *)((char *)ws + models_bytes(models, n_models) + stats_partial_bytes());
+    cudaMemsetAsync(dr.flags, 0, kFlagBytes, s);
     launch_solve(dm, db, dr, mode, s, num_sms());
     // instances with 32 < M <= B_max (block per instance); M > B_max is BADPARAM, so the launch is
     // needed only when some model admits batches wider than a warp

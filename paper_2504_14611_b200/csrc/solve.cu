@@ -68,6 +68,7 @@ struct SolveSmem {
     GridKCache kc;                       // k of the last (f_e,min, f_e,max, rho)
     double rinv[kMaxM];                  // RD(1 / R_m): lower-bound upload term
     double lbem[64];                     // per n~: the lower bound's member term (uniform users)
+    int defer;                           // this warp deferred an instance (uniform kernels)
     double pre[kMaxM + 1];               // equal-deadline kernel: P[p] = user-order sum of the first p e_loc
     double lb[64];                       // per n~: lower bound of every configuration's energy
     // uniform users (UNI kernel, N <= kUniCache): the per-n~ values that depend only on the model and
@@ -263,7 +264,10 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     }
 #endif
     if (st == kStDefer) {  // the other uniform kernel, or M > 32: k_solve_large (solve_large.cu)
-        if (UNI && lane == 0) r.status[i] = kStDefer;
+        if (UNI && lane == 0) {
+            r.status[i] = kStDefer;
+            s.defer = 1;  // published once per warp when the kernel ends
+        }
         return;
     }
     const double t_free = x.t_free, fe_max = x.fe_max, rho = x.rho;
@@ -275,7 +279,10 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     const bool homog_ = !(vflags & kNotHomog);
     const bool uni_ = homog_ && !(vflags & kNotUni);
     if (UNI && !uni_) {
-        if (lane == 0) r.status[i] = kStDefer;
+        if (lane == 0) {
+            r.status[i] = kStDefer;
+            s.defer = 1;  // published once per warp when the kernel ends
+        }
         return;
     }
     const DevModel &md = *mdp;
@@ -393,9 +400,13 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                 if (TIGHT) s.lbem[nt] = em;
 #endif
                 double S = 0.0;
-                if (!TIGHT) {  // equal deadlines: every user's e_loc is the same bits (identical inputs)
+                if (!TIGHT) {
+                    // equal deadlines: every user's e_loc is the same bits, so every term is t; the RN sum of
+                    // M copies of t >= M t (1 - u)^(M-1) >= M t (1 - (M-1) u) (u = 2^-53, each RN step
+                    // >= (1 - u) times its exact sum), bounded below by two RD products (a valid, slightly
+                    // weaker bound: pruning stays exact)
                     const double el = s.et[0].x, t = (em < el) ? em : el;
-                    for (int m = 0; m < M; m++) S = S + t;
+                    S = __dmul_rd(__dmul_rd((double)M, t), 1.0 - (double)(M - 1) * 0x1p-53);
                 } else {
                     for (int m = 0; m < M; m++) {
                         const double el = s.et[m].x;
@@ -800,6 +811,7 @@ __global__ void __launch_bounds__(kSolveWarps * 32, UNI ? JDOB_SOLVE_MINB_U : JD
         s.inv_n = 0;
         s.kc = GridKCache{0.0, 0.0, 0.0, 0};  // rho > 0 in every valid instance: no false hit
         s.ukey[0] = -1;                       // no model id -1: no false hit
+        s.defer = 0;
         s.pre[0] = 0.0;
     }
     __syncwarp();
@@ -824,11 +836,15 @@ __global__ void __launch_bounds__(kSolveWarps * 32, UNI ? JDOB_SOLVE_MINB_U : JD
             const long long co = o, cm = e - o;
             const int cid = id;
             head(i + nw, o, e, id);
-            const bool nx = i + nw < b.n_inst;
-            solve_instance<COUNTS, PRUNE, UNI, VERIFY, TIGHT>(i, co, cm, cid, models, b, r, mode, s, lane,
-                                                              nx ? o : 0, nx ? e : 0);
+            // (o, e: the next instance's head; for a warp's last instance the current one's, whose users
+            // the prefetch then touches again -- valid addresses, no select waiting on the loads)
+            solve_instance<COUNTS, PRUNE, UNI, VERIFY, TIGHT>(i, co, cm, cid, models, b, r, mode, s, lane, o, e);
         }
+        __syncwarp();
+        if (lane == 0 && s.defer && r.flags) r.flags[0] = 1;  // one store per warp, not per deferral
     } else {
+        // nothing deferred by the kernel before: no instance to visit
+        if (r.flags && r.flags[UNI ? 0 : 1] == 0) return;
         // only the instances the kernels before left (kStDefer), 32 statuses per load; lane l of round t
         // looks at instance gw + (32 t + l) nw, so the deferred instances are spread over the warps as in a
         // grid-stride loop (consecutive groups of 32 per warp left most warps idle when few groups exist)
@@ -854,6 +870,8 @@ __global__ void __launch_bounds__(kSolveWarps * 32, UNI ? JDOB_SOLVE_MINB_U : JD
                                                                   lane);
             }
         }
+        __syncwarp();
+        if (UNI && lane == 0 && s.defer && r.flags) r.flags[1] = 1;  // the differing-deadline kernel's deferrals
     }
 }
 
