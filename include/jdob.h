@@ -232,8 +232,10 @@ JDOB_API int jdob_stats_part(const jdob_batch *b, const jdob_result *res, int64_
  * Errors: as jdob_solve_batch, plus JDOB_EINVAL when the host user_off is not a
  * non-decreasing sequence starting at >= 0 (checked per chunk before its copies).
  * If `h2d_bytes`/`d2h_bytes` are non-NULL they receive the bytes copied.  The batch is processed in
- * chunks on two streams (copy-in, solve, copy-out overlap); a chunk's copy-ins are one
- * cudaMemcpyAsync per array.
+ * chunks on three streams of the library (every chunk's copy-ins on one, each chunk's solve on a
+ * second after its copy-ins, its copy-outs on a third after its solve), joined into `stream`
+ * before the call returns; a chunk's copy-ins are one cudaMemcpyAsync per array.  The library's
+ * streams are per device: host calls on one device from several threads are serialised by a lock.
  */
 JDOB_API int jdob_solve_batch_host(const jdob_model *models, int32_t n_models, const jdob_batch *b, int32_t mode,
                           const jdob_result *out, void *stream, int64_t *h2d_bytes, int64_t *d2h_bytes);

@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "jdob_dev.cuh"
@@ -575,6 +576,8 @@ struct HostStreams {
 static HostStreams g_hs[64];
 static bool g_hs_made[64];
 
+static std::mutex g_hs_mutex[64];  // one host call per device at a time (the streams and events are shared)
+
 static HostStreams &host_streams() {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -730,6 +733,9 @@ static int solve_host_impl(const jdob_model *models, int32_t n_models, const jdo
     // one stream, each chunk's solve on a second stream once its copy-ins are done, its copy-outs on a
     // third once its solve is done -- the H2D engine never waits for a solve or a copy-out, and the solve
     // of chunk c overlaps the copy-ins of the chunks after it and the copy-outs of those before it
+    int hdev = 0;
+    cudaGetDevice(&hdev);
+    std::lock_guard<std::mutex> hs_lock(g_hs_mutex[(hdev >= 0 && hdev < 64) ? hdev : 0]);
     HostStreams &hs = host_streams();
     cudaStream_t sh = hs.h2d, sk = hs.compute, sd = hs.d2h;
     cudaEventRecord(hs.start, s);
