@@ -42,7 +42,10 @@
 
 namespace jdob {
 
-constexpr int kInvCache = 192;    // 1/f_e(j) cached for j < kInvCache
+#ifndef JDOB_INV_CACHE
+#define JDOB_INV_CACHE 192
+#endif
+constexpr int kInvCache = JDOB_INV_CACHE;  // 1/f_e(j) cached for j < kInvCache
 
 // Order of the pruned n~ sweep (DESIGN.md §4 "n~ pruning"): 0 ascending n~ (the literal order),
 // 1 ascending with the bound also capped at E_LC, 2 best first (smallest lower bound first).
