@@ -193,6 +193,23 @@ JDOB_API int jdob_solve_batch(const jdob_model *models, int32_t n_models, const 
                      const jdob_result *out, void *ws, size_t ws_bytes, void *stream);
 
 /*
+ * The paper's comparison set minus IP-SSA (NEXT-2) in ONE pass: J-DOB (JDOB_MODE_FULL) into
+ * out[0], J-DOB without edge DVFS (JDOB_MODE_NO_EDGE_DVFS: f_e fixed at f_e,max, the j = 0
+ * configurations) into out[1], and binary J-DOB (JDOB_MODE_BINARY: n~ in {0, N}, the n~ = 0
+ * configurations) into out[2], from one validation, one LC evaluation and one pruned sweep per
+ * instance (an n~ is visited while either pruned mode may still improve there; each mode keeps its own
+ * strict (E, n~, j) minimum and all-local key, R8).  LC is every result's E_lc.  Every output is
+ * bit-identical to jdob_solve_batch with that mode.
+ *   models, b, ws, ws_bytes, stream : as jdob_solve_batch.
+ *   out      : HOST array of 3 structs of DEVICE output arrays, each as jdob_solve_batch's `out`
+ *              (f_user, partition and stats optional per mode); counts, work and violations must be
+ *              NULL (JDOB_EINVAL otherwise).
+ * Errors: as jdob_solve_batch.
+ */
+JDOB_API int jdob_solve_batch_modes(const jdob_model *models, int32_t n_models, const jdob_batch *b,
+                                    const jdob_result *out, void *ws, size_t ws_bytes, void *stream);
+
+/*
  * Energy-saving statistics (row a12; R16) of solved instances, as a call of
  * its own: the same bucketed fields, the same fixed reduction tree and the same bits as the
  * `stats` output of jdob_solve_batch (described there).

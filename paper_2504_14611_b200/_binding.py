@@ -94,6 +94,8 @@ def lib():
             L = C.CDLL(LIB_PATH)
             _sig(L, "jdob_workspace_bytes", [_P(JModel), C.c_int32, C.c_int32], C.c_size_t)
             _sig(L, "jdob_solve_batch", [_P(JModel), C.c_int32, _P(JBatch), C.c_int32, _P(JResult), C.c_void_p, C.c_size_t, C.c_void_p])
+            _sig(L, "jdob_solve_batch_modes", [_P(JModel), C.c_int32, _P(JBatch), _P(JResult), C.c_void_p, C.c_size_t,
+                                               C.c_void_p])
             _sig(L, "jdob_solve_batch_host", [_P(JModel), C.c_int32, _P(JBatch), C.c_int32, _P(JResult), C.c_void_p, _P(C.c_int64), _P(C.c_int64)])
             _sig(L, "jdob_bruteforce", [_P(JModel), C.c_int32, _P(JBatch), C.c_int32, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p])
             _sig(L, "jdob_stats", [_P(JBatch), _P(JResult), C.c_void_p, C.c_size_t, C.c_void_p])
@@ -118,7 +120,7 @@ EXPORTED = ("jdob_workspace_bytes", "jdob_solve_batch", "jdob_solve_batch_host",
             "jdob_bf_space_size", "jdob_eval", "jdob_grouped_workspace_bytes", "jdob_solve_grouped",
             "jdob_last_error", "jdob_version", "jdob_release_pool", "jdob_stats", "jdob_stats_part",
             "jdob_generate_workspace_bytes", "jdob_generate_c5_instances", "jdob_generate_c5_users",
-            "jdob_solve_shared_host")
+            "jdob_solve_shared_host", "jdob_solve_batch_modes")
 
 
 def _check(rc):
@@ -284,6 +286,42 @@ def solve_batch(db: DeviceBatch, mode: int = MODE_FULL, f_user: bool = True, cou
     _check(lib().jdob_solve_batch(db.jmodels, db.n_models, C.byref(db.jbatch), int(mode), C.byref(r),
                                   ws.data_ptr(), ws.numel(), _stream_handle(stream)))
     return out
+
+
+def solve_batch_modes(db: DeviceBatch, f_user: bool = True, stats: bool = False, n_buckets: Optional[int] = None,
+                      partition: bool = False, stream=None) -> dict:
+    """jdob_solve_batch_modes: J-DOB, J-DOB without edge DVFS and binary J-DOB (NEXT-2) in one pass;
+    returns {MODE_FULL: res, MODE_NO_EDGE_DVFS: res, MODE_BINARY: res}, each as solve_batch's dict."""
+    torch = _torch()
+    dev = db.device
+    n, nu = db.n_inst, db.n_users
+    outs, rs = {}, []
+    for mode in (MODE_FULL, MODE_NO_EDGE_DVFS, MODE_BINARY):
+        o = dict(E=torch.empty(n, dtype=torch.float64, device=dev),
+                 E_lc=torch.empty(n, dtype=torch.float64, device=dev),
+                 t_free_next=torch.empty(n, dtype=torch.float64, device=dev),
+                 f_e=torch.empty(n, dtype=torch.float64, device=dev),
+                 n_tilde=torch.empty(n, dtype=torch.int32, device=dev),
+                 j=torch.empty(n, dtype=torch.int32, device=dev),
+                 status=torch.empty(n, dtype=torch.int32, device=dev),
+                 mask=torch.empty(n, dtype=torch.int32, device=dev))
+        if f_user:
+            o["f_user"] = torch.empty(nu, dtype=torch.float64, device=dev)
+        if stats:
+            nb = n_buckets if n_buckets is not None else db.n_buckets
+            o["stats"] = torch.empty((nb, STATS_FIELDS), dtype=torch.float64, device=dev)
+        if partition:
+            o["partition"] = torch.empty(nu, dtype=torch.int32, device=dev)
+        outs[mode] = o
+        rs.append(JResult(*[_ptr(o.get(f)) for f in ("E", "E_lc", "t_free_next", "f_e", "n_tilde", "j", "status",
+                                                     "mask", "f_user")], None, _ptr(o.get("stats")),
+                          int(o["stats"].shape[0]) if o.get("stats") is not None else 0, _ptr(o.get("partition")),
+                          None, None, 0.0))
+    arr = (JResult * 3)(*rs)
+    ws = db.workspace(0)
+    _check(lib().jdob_solve_batch_modes(db.jmodels, db.n_models, C.byref(db.jbatch), arr, ws.data_ptr(), ws.numel(),
+                                        _stream_handle(stream)))
+    return outs
 
 
 def stats(db: DeviceBatch, res: dict, n_buckets: Optional[int] = None, stream=None, out=None,

@@ -310,6 +310,69 @@ static int solve_prepared(const jdob_model *models, int32_t n_models, const DevM
     return JDOB_OK;
 }
 
+static DevResult dev_result(const jdob_result *out) {
+    DevResult dr;
+    dr.E = out->E;
+    dr.E_lc = out->E_lc;
+    dr.t_free_next = out->t_free_next;
+    dr.f_e = out->f_e;
+    dr.n_tilde = out->n_tilde;
+    dr.j = out->j;
+    dr.status = out->status;
+    dr.mask = out->mask;
+    dr.f_user = out->f_user;
+    dr.counts = nullptr;
+    dr.partition = out->partition;
+    dr.work = nullptr;
+    dr.viol = nullptr;
+    dr.slack = out->slack;
+    return dr;
+}
+
+int jdob_solve_batch_modes(const jdob_model *models, int32_t n_models, const jdob_batch *b, const jdob_result *out,
+                           void *ws, size_t ws_bytes, void *stream) {
+    NvtxRange nvtx_("jdob_solve_batch_modes");
+    g_err.clear();
+    int rc = check_models(models, n_models);
+    if (rc) return rc;
+    if ((rc = check_batch(b, n_models))) return rc;
+    if (!out) return fail(JDOB_EINVAL, "out is NULL");
+    for (int m = 0; m < 3; m++) {
+        const jdob_result *o = &out[m];
+        if (b->n_inst > 0 && (!o->E || !o->E_lc || !o->t_free_next || !o->f_e || !o->n_tilde || !o->j || !o->status ||
+                              !o->mask))
+            return fail(JDOB_EINVAL, "result %d has a NULL required array", m);
+        if (o->counts || o->work || o->violations)
+            return fail(JDOB_EINVAL, "result %d: counts/work/violations are not produced by the one-pass call", m);
+        if (o->stats && (o->n_buckets < 1 || o->n_buckets > JDOB_MAX_BUCKETS))
+            return fail(JDOB_EINVAL, "result %d: n_buckets = %d outside [1, %d]", m, o->n_buckets, JDOB_MAX_BUCKETS);
+    }
+    const size_t need = jdob_workspace_bytes(models, n_models, 0);
+    if (!ws || ws_bytes < need) return fail(JDOB_EINVAL, "workspace %zu bytes < %zu", ws_bytes, need);
+    cudaStream_t s = (cudaStream_t)stream;
+    DevModel *dm = nullptr;
+    if ((rc = prepare_models(models, n_models, (char *)ws, &dm, s))) return rc;
+    const DevBatch db = to_dev(b);
+    const DevResult r0 = dev_result(&out[0]), r1 = dev_result(&out[1]), r2 = dev_result(&out[2]);
+    launch_solve_multi(dm, db, r0, r1, r2, s, num_sms());
+    bool wide = false;  // instances with 32 < M <= B_max: the block-per-instance kernel, once per mode
+    for (int i = 0; i < n_models; i++) wide |= models[i].B_max > JDOB_MAX_M;
+    if (wide) {
+        launch_solve_large(dm, db, r0, JDOB_MODE_FULL, s, num_sms());
+        launch_solve_large(dm, db, r1, JDOB_MODE_NO_EDGE_DVFS, s, num_sms());
+        launch_solve_large(dm, db, r2, JDOB_MODE_BINARY, s, num_sms());
+    }
+    if ((rc = cuda_check("solve_modes"))) return rc;
+    const DevResult *rs[3] = {&r0, &r1, &r2};
+    for (int m = 0; m < 3; m++) {
+        if (!out[m].stats) continue;
+        double *partials = (double *)((char *)ws + models_bytes(models, n_models));
+        launch_stats(db, *rs[m], partials, out[m].stats, out[m].n_buckets, b->n_inst, 1, 0, s);
+        if ((rc = cuda_check("stats"))) return rc;
+    }
+    return JDOB_OK;
+}
+
 int jdob_stats(const jdob_batch *b, const jdob_result *res, void *ws, size_t ws_bytes, void *stream) {
     return jdob_stats_part(b, res, b ? b->n_inst : 0, 1, 0, ws, ws_bytes, stream);
 }

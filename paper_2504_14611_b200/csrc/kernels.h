@@ -50,6 +50,8 @@ int launch_grouped(const DevModel *models, const DevBatch &b, int mode, const Og
                    cudaStream_t s, int num_sms, bool wide);  // wide: some model has B_max > 32
 void launch_solve(const DevModel *models, const DevBatch &b, const DevResult &r, int mode, cudaStream_t s,
                   int num_sms);
+void launch_solve_multi(const DevModel *models, const DevBatch &b, const DevResult &r0, const DevResult &r1,
+                        const DevResult &r2, cudaStream_t s, int num_sms);
 void launch_solve_large(const DevModel *models, const DevBatch &b, const DevResult &r, int mode, cudaStream_t s,
                         int num_sms);
 // Statistics of the local batch b = part `part` of `parts` (a power of two <= kStatsBlocks) of a batch

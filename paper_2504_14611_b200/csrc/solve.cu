@@ -233,11 +233,14 @@ __device__ __forceinline__ void write_local(const DevResult &r, long long i, lon
 // setting; instances whose deadlines differ are marked kStDefer), true = the kernel of differing deadlines,
 // which adds the batch-coupled n~ bound (it prunes 43-66 % of the set-ups there, little with equal
 // deadlines, and its code costs the other kernel 6 % when compiled in).
-template <bool COUNTS, bool PRUNE, bool UNI, bool VERIFY, bool TIGHT>
+// MULTI (NEXT-2, general kernel only): one pass answers JDOB_MODE_FULL into r and, from the same sweep,
+// JDOB_MODE_NO_EDGE_DVFS (the candidates at j = 0) and JDOB_MODE_BINARY (the candidates at n~ = 0) into
+// rx[0] and rx[1]; every mode's (E, n~, j) tie rule and all-local key are kept as in its own pass.
+template <bool COUNTS, bool PRUNE, bool UNI, bool VERIFY, bool TIGHT, bool MULTI = false>
 __device__ __forceinline__ void solve_instance(long long i, long long off, long long M64, int mid,
                                                const DevModel *models, const DevBatch &b, const DevResult &r,
                                                int mode, SolveSmem &s, int lane, long long nx_off = 0,
-                                               long long nx_end = 0) {
+                                               long long nx_end = 0, const DevResult *rx = nullptr) {
     __syncwarp();
     long long k;
     int M;
@@ -276,6 +279,10 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     const double t_free = x.t_free, fe_max = x.fe_max, rho = x.rho;
     if (st == JDOB_ST_BADPARAM || st == JDOB_ST_BADMODEL) {
         write_bad(r, i, off, M, mdp ? mdp->N : 0, t_free, st, lane);
+        if (MULTI) {
+            write_bad(rx[0], i, off, M, mdp ? mdp->N : 0, t_free, st, lane);
+            write_bad(rx[1], i, off, M, mdp ? mdp->N : 0, t_free, st, lane);
+        }
         return;
     }
     // the uniform kernels leave non-uniform instances, whatever their status, to the general kernel
@@ -320,6 +327,10 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
 #endif
     }
     if (st != JDOB_ST_OK || mode == JDOB_MODE_LC) {
+        if (MULTI) {
+            write_local(rx[0], i, off, M, N, E_lc, t_free, floc, st, lane, true);
+            write_local(rx[1], i, off, M, N, E_lc, t_free, floc, st, lane, true);
+        }
         write_local(r, i, off, M, N, E_lc, t_free, floc, st, lane, true);
         if (VERIFY) {
             const unsigned vb = verify_local(x, vN, floc, M, vflags, r.slack, lane);
@@ -439,6 +450,10 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     }
     double bE;
     int bN, bP, bJ, aN, aJ;
+    // MULTI: the no-edge-DVFS mode's best (candidates at j = 0: lane 0's first point) and all-local key,
+    // and the binary mode's (candidates at n~ = 0)
+    double gE = dinf(), hE = dinf();
+    int gN = 0x7fffffff, gP = 0, gaN = N, gaJ = 0, hJ = 0, hP = 0, haN = N, haJ = 0;
     long long c_setup = 0, c_visit = 0, c_eval = 0, c_member = 0;
     int last_nt = -1;  // the n~ whose set-up is in shared memory
     for (int pass = 0;; pass++) {
@@ -447,12 +462,20 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
         const bool prune = use_lb && pass == 0;
         bool pruned = false;
         double bEw = dinf();  // warp-uniform best energy so far
+        double bEwG = dinf();  // MULTI: the no-edge-DVFS mode's
         bE = dinf();
         bN = 0x7fffffff;
         bP = 0;
         bJ = 0;
         aN = N;  // first all-local evaluation key (R8); n~ = N at j = 0 by default (R4)
         aJ = 0;
+        if (MULTI) {
+            gE = hE = dinf();
+            gN = 0x7fffffff;
+            gP = hJ = hP = 0;
+            gaN = haN = N;
+            gaJ = haJ = 0;
+        }
 
 #if JDOB_PRUNE_ORDER == 2
         unsigned long long done = 0ull;  // n~ swept in this pass (best-first order)
@@ -489,9 +512,11 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                 if (N > 32) cand |= (unsigned long long)__ballot_sync(0xffffffffu, lane + 32 < N && s.lb[lane + 32] < bEw &&
                                                                                 s.lb[lane + 32] <= E_lc) << 32;
 #else
-                unsigned long long cand = __ballot_sync(0xffffffffu, lane < N && s.lb[lane] < bEw);
+                // (MULTI: an n~ is visited when either pruned mode may still improve there)
+                const double bEs = MULTI ? ((bEwG > bEw) ? bEwG : bEw) : bEw;
+                unsigned long long cand = __ballot_sync(0xffffffffu, lane < N && s.lb[lane] < bEs);
                 if (N > 32) cand |= (unsigned long long)__ballot_sync(0xffffffffu, lane + 32 < N &&
-                                                                                s.lb[lane + 32] < bEw) << 32;
+                                                                                s.lb[lane + 32] < bEs) << 32;
 #endif
                 cand &= ~0ull << (nt + 1);
                 if (cand == 0ull) {
@@ -567,6 +592,16 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                     aN = nt;
                     aJ = (int)jb;
                 }
+                if (MULTI && emp) {
+                    if (jb == 0 && nt < gaN) {  // no edge DVFS: the set at j = 0 is empty
+                        gaN = nt;
+                        gaJ = 0;
+                    }
+                    if (nt == 0 && haN == N) {  // binary: the first all-local evaluation at n~ = 0
+                        haN = 0;
+                        haJ = (int)jb;
+                    }
+                }
                 if (COUNTS && emp && lane == 0) {  // the all-local evaluation at jb (guard passes: 0 / inf = 0)
                     c_visit += 1;
                     c_eval += 1;
@@ -604,7 +639,7 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                     const double emA = ((c0.x * fA) * fA) + c0.y;  // D21 offloader term
                     const double emB = ((c0.x * fB) * fB) + c0.y;
 #ifndef JDOB_NO_PREFIX
-                    if (!TIGHT) {
+                    if (UNI && !TIGHT) {  // (the equal-deadline kernel: members are the users m >= p)
                         // equal deadlines: the ranks are the user indices, so the members are the users
                         // m >= p (thresholds non-increasing from i^) and the user-order sum is the prefix
                         // P[p] of the e_loc terms (formed with E_LC) followed by M - p member terms
@@ -666,11 +701,31 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                     bJ = (int)jB;
                     bP = pB;
                 }
+                if (MULTI) {
+                    if (j0 == 0 && lane == 0 && passA && (EA < gE || (EA == gE && nt < gN))) {  // j = 0
+                        gE = EA;
+                        gN = nt;
+                        gP = pA;
+                    }
+                    if (nt == 0) {  // binary: n~ = 0 only; a lane's j ascend
+                        if (passA && EA < hE) {
+                            hE = EA;
+                            hJ = (int)jA;
+                            hP = pA;
+                        }
+                        if (passB && EB < hE) {
+                            hE = EB;
+                            hJ = (int)jB;
+                            hP = pB;
+                        }
+                    }
+                }
                 if (emp) break;
             }
             if (prune) {  // warp minimum of the lane bests (energies are >= 0)
                 const double w = warp_min_nonneg(bE);
                 bEw = (w < bEw) ? w : bEw;
+                if (MULTI) bEwG = __shfl_sync(0xffffffffu, gE, 0);
             }
             __syncwarp();
         }
@@ -694,7 +749,19 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                 bP = 0;
             }
         }
-        if (!(pruned && bE == E_lc)) break;
+        if (MULTI) {
+            // binary: the same argmin at n~ = 0; no edge DVFS: lane 0 holds its best
+            const double Hmin = warp_min_nonneg(hE);
+            const unsigned key = (hE == Hmin && hE < dinf()) ? (((unsigned)hJ << 5) | (unsigned)hP) : 0xffffffffu;
+            const unsigned mk = __reduce_min_sync(0xffffffffu, key);
+            hE = Hmin;
+            hJ = (mk != 0xffffffffu) ? (int)((mk >> 5) & 0xffffu) : 0;
+            hP = (mk != 0xffffffffu) ? (int)(mk & 31u) : 0;
+            gE = __shfl_sync(0xffffffffu, gE, 0);
+            gN = __shfl_sync(0xffffffffu, gN, 0);
+            gP = __shfl_sync(0xffffffffu, gP, 0);
+        }
+        if (!(pruned && (bE == E_lc || (MULTI && gE == E_lc)))) break;
     }
     if (COUNTS) {
 #pragma unroll
@@ -715,82 +782,94 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
             r.work[4 * i + 3] = c_member;
         }
     }
-    const bool offload_wins = (bE < E_lc) || (bE == E_lc && (bN < aN || (bN == aN && bJ < aJ)));
-    if (!offload_wins) {
-        write_local(r, i, off, M, N, E_lc, t_free, floc, st, lane, false);
-        if (VERIFY) {
-            const unsigned vb = verify_local(x, vN, floc, M, vflags, r.slack, lane);
-            if (lane == 0) r.viol[i] = vb;
-        }
-        return;
-    }
-    // winner: recompute D20 and D22 lane = user (same arithmetic as the sweep)
-#ifdef JDOB_WIN_SETUP
-    const bool win_direct = false;
-#else
-    // homogeneous users: ranks and sorted deadlines are per instance, only (O/R, zv) depend on n~,
-    // so the winner's are formed directly (same expressions as setup_nt) instead of a new set-up
-    const bool win_direct = homog;
-#endif
-    if (!win_direct && bN != last_nt) setup_nt(md, bN, M, homog, uni, t_free, s, lane, uc);
-    const int Bo = M - bP;
-    const double lo_ = s.Lg[bP].x;
-    const double fe = grid_fe(fe_max, rho, bJ);
-    const double inv = (bJ < kInvCache) ? s.inv[bJ] : 1.0 / fe;  // the sweep's cached 1/f_e(j), same bits
-    const double te = md.phi[bN * B1 + Bo] * inv;
-    const bool member = (lane < M) && (s.rank[lane] >= bP);
-    double f = floc, arr = t_free;
-    unsigned vbits = 0u;  // the plan re-verified with jdob_eval's formulas (row a11)
-    if (VERIFY) {
-        if (lane == 0) {
-            if (!(fe >= x.fe_min && fe <= fe_max)) vbits |= 32u;
-            if (t_free + te > lo_ + r.slack * fabs(lo_)) vbits |= 1u;  // D6: the ASAP start of batch n~ + 1
-        }
-        if (!member && lane < M && d8_violated(x.z * vN, floc, x.T + r.slack * fabs(x.T))) vbits |= 4u;  // D8
-    }
-    if (member) {
-        const double2 a = (win_direct && uc) ? make_double2(s.uOR[bN], s.uZV[bN])
-                          : win_direct ? make_double2(md.O[bN] / s.R[lane], s.z[lane] * md.v[bN])
-                                     : s.orzv[uni ? 0 : lane];  // (O/R, zv)
-        const double2 t = s.fmm[lane];                          // (f_min, f_max)
-        const double budget = (lo_ - a.x) - te;
-        const bool low = (a.y == 0.0) || (__fma_rn(t.x, budget, -a.y) > 0.0);
-        f = low ? t.x : clampf(a.y / budget, t.x, t.y);
-        arr = div_z(a.y, f) + a.x;
-        if (VERIFY) {
-            // jdob_eval's D20 branches (bit 3 and the f of an infeasible budget) and its D7 finish test
-            double fev = f;
-            if (a.y == 0.0) {
-                if (budget < 0.0) vbits |= 8u;
-            } else if (!(__fma_rn(t.x, budget, -a.y) > 0.0) && !(budget > 0.0)) {
-                vbits |= 8u;
-                fev = t.y;
+    // the answer of one mode (the winner re-evaluated lane = user, or the all-local plan)
+    auto emit = [&](const DevResult &rr, const double bE, const int bN, const int bJ, const int bP, const int aN,
+                    const int aJ) {
+        const bool offload_wins = (bE < E_lc) || (bE == E_lc && (bN < aN || (bN == aN && bJ < aJ)));
+        if (!offload_wins) {
+            write_local(rr, i, off, M, N, E_lc, t_free, floc, st, lane, false);
+            if (VERIFY) {
+                const unsigned vb = verify_local(x, vN, floc, M, vflags, rr.slack, lane);
+                if (lane == 0) rr.viol[i] = vb;
             }
-            double fin = arr;  // eval's arrival div_z(zv, f) + O/R: arr unless eval took f_max
-            if (fev != f) fin = div_z(a.y, fev) + a.x;
-            fin = fin + te;
-            if (fin > lo_ + r.slack * fabs(lo_)) vbits |= 2u;
+            return;
         }
-        if (arr < t_free) arr = t_free;
+        // winner: recompute D20 and D22 lane = user (same arithmetic as the sweep)
+#ifdef JDOB_WIN_SETUP
+        const bool win_direct = false;
+#else
+        // homogeneous users: ranks and sorted deadlines are per instance, only (O/R, zv) depend on n~,
+        // so the winner's are formed directly (same expressions as setup_nt) instead of a new set-up
+        const bool win_direct = homog;
+#endif
+        if (!win_direct && bN != last_nt) {
+            setup_nt(md, bN, M, homog, uni, t_free, s, lane, uc);
+            last_nt = bN;
+        }
+        const int Bo = M - bP;
+        const double lo_ = s.Lg[bP].x;
+        const double fe = grid_fe(fe_max, rho, bJ);
+        const double inv = (bJ < kInvCache) ? s.inv[bJ] : 1.0 / fe;  // the sweep's cached 1/f_e(j), same bits
+        const double te = md.phi[bN * B1 + Bo] * inv;
+        const bool member = (lane < M) && (s.rank[lane] >= bP);
+        double f = floc, arr = t_free;
+        unsigned vbits = 0u;  // the plan re-verified with jdob_eval's formulas (row a11)
+        if (VERIFY) {
+            if (lane == 0) {
+                if (!(fe >= x.fe_min && fe <= fe_max)) vbits |= 32u;
+                if (t_free + te > lo_ + rr.slack * fabs(lo_)) vbits |= 1u;  // D6: the ASAP start of batch n~ + 1
+            }
+            if (!member && lane < M && d8_violated(x.z * vN, floc, x.T + rr.slack * fabs(x.T))) vbits |= 4u;  // D8
+        }
+        if (member) {
+            const double2 a = (win_direct && uc) ? make_double2(s.uOR[bN], s.uZV[bN])
+                              : win_direct ? make_double2(md.O[bN] / s.R[lane], s.z[lane] * md.v[bN])
+                                         : s.orzv[uni ? 0 : lane];  // (O/R, zv)
+            const double2 t = s.fmm[lane];                          // (f_min, f_max)
+            const double budget = (lo_ - a.x) - te;
+            const bool low = (a.y == 0.0) || (__fma_rn(t.x, budget, -a.y) > 0.0);
+            f = low ? t.x : clampf(a.y / budget, t.x, t.y);
+            arr = div_z(a.y, f) + a.x;
+            if (VERIFY) {
+                // jdob_eval's D20 branches (bit 3 and the f of an infeasible budget) and its D7 finish test
+                double fev = f;
+                if (a.y == 0.0) {
+                    if (budget < 0.0) vbits |= 8u;
+                } else if (!(__fma_rn(t.x, budget, -a.y) > 0.0) && !(budget > 0.0)) {
+                    vbits |= 8u;
+                    fev = t.y;
+                }
+                double fin = arr;  // eval's arrival div_z(zv, f) + O/R: arr unless eval took f_max
+                if (fev != f) fin = div_z(a.y, fev) + a.x;
+                fin = fin + te;
+                if (fin > lo_ + rr.slack * fabs(lo_)) vbits |= 2u;
+            }
+            if (arr < t_free) arr = t_free;
+        }
+        arr = warp_max_nonneg(arr);  // arrivals >= t_free >= 0
+        const unsigned mask = __ballot_sync(0xffffffffu, member);
+        if (VERIFY) {
+            vbits = __reduce_or_sync(0xffffffffu, vbits);
+            if (lane == 0) rr.viol[i] = vbits;
+        }
+        if (lane == 0) {
+            rr.E[i] = bE;
+            rr.E_lc[i] = E_lc;
+            rr.t_free_next[i] = arr + te;  // D22
+            rr.f_e[i] = fe;
+            rr.n_tilde[i] = bN;
+            rr.j[i] = (int)bJ;
+            rr.status[i] = st;
+            rr.mask[i] = mask;
+        }
+        if (rr.f_user && lane < M) rr.f_user[off + lane] = f;
+        if (rr.partition && lane < M) rr.partition[off + lane] = member ? bN : N;
+    };
+    if (MULTI) {
+        emit(rx[0], gE, gN, 0, gP, gaN, gaJ);                                  // no edge DVFS
+        emit(rx[1], hE, (hE < dinf()) ? 0 : 0x7fffffff, hJ, hP, haN, haJ);      // binary
     }
-    arr = warp_max_nonneg(arr);  // arrivals >= t_free >= 0
-    const unsigned mask = __ballot_sync(0xffffffffu, member);
-    if (VERIFY) {
-        vbits = __reduce_or_sync(0xffffffffu, vbits);
-        if (lane == 0) r.viol[i] = vbits;
-    }
-    if (lane == 0) {
-        r.E[i] = bE;
-        r.E_lc[i] = E_lc;
-        r.t_free_next[i] = arr + te;  // D22
-        r.f_e[i] = fe;
-        r.n_tilde[i] = bN;
-        r.j[i] = (int)bJ;
-        r.status[i] = st;
-        r.mask[i] = mask;
-    }
-    if (r.f_user && lane < M) r.f_user[off + lane] = f;
-    if (r.partition && lane < M) r.partition[off + lane] = member ? bN : N;
+    emit(r, bE, bN, bJ, bP, aN, aJ);
 }
 
 #ifndef JDOB_SOLVE_MINB
@@ -898,6 +977,47 @@ static void launch_pair(const DevModel *models, const DevBatch &b, const DevResu
     launch_solve_t<COUNTS, PRUNE, true, VERIFY, false>(models, b, r, mode, s, num_sms);  // uniform, equal deadlines
     launch_solve_t<COUNTS, PRUNE, true, VERIFY, true>(models, b, r, mode, s, num_sms);   // uniform, differing ones
     launch_solve_t<COUNTS, PRUNE, false, VERIFY, false>(models, b, r, mode, s, num_sms); // the rest
+}
+
+// NEXT-2 in one pass: JDOB_MODE_FULL into r0, JDOB_MODE_NO_EDGE_DVFS into r1, JDOB_MODE_BINARY into r2
+// (the general kernel over every instance, grid-stride with the heads loaded ahead; M > 32 is left to
+// k_solve_large, one launch per mode)
+__global__ void __launch_bounds__(kSolveWarps * 32, JDOB_SOLVE_MINB)
+    k_solve_multi(const DevModel *models, DevBatch b, DevResult r0, DevResult r1, DevResult r2) {
+    __shared__ SolveSmem smem[kSolveWarps];
+    const int lane = threadIdx.x & 31;
+    SolveSmem &s = smem[threadIdx.x >> 5];
+    if (lane == 0) {
+        s.inv_key = make_double2(0.0, 0.0);
+        s.inv_n = 0;
+        s.kc = GridKCache{0.0, 0.0, 0.0, 0};
+        s.ukey[0] = -1;
+        s.pre[0] = 0.0;
+        s.defer = 0;
+    }
+    __syncwarp();
+    const DevResult rx[2] = {r1, r2};
+    const long long gw = (long long)blockIdx.x * kSolveWarps + (threadIdx.x >> 5);
+    const long long nw = (long long)gridDim.x * kSolveWarps;
+    for (long long i = gw; i < b.n_inst; i += nw) {
+        const long long o = b.user_off[i];
+        const long long m = (b.user_end ? b.user_end[i] : b.user_off[i + 1]) - o;
+        solve_instance<false, true, false, false, false, true>(i, o, m, b.model_id[i], models, b, r0, JDOB_MODE_FULL,
+                                                               s, lane, 0, 0, rx);
+    }
+}
+
+void launch_solve_multi(const DevModel *models, const DevBatch &b, const DevResult &r0, const DevResult &r1,
+                        const DevResult &r2, cudaStream_t s, int num_sms) {
+    if (b.n_inst <= 0) return;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve_multi, kSolveWarps * 32, 0);
+    if (per_sm < 1) per_sm = 1;
+    const long long want = (b.n_inst + kSolveWarps - 1) / kSolveWarps;
+    long long grid = (long long)num_sms * per_sm / grid_divisor();
+    if (grid < 1) grid = 1;
+    if (want < grid) grid = want;
+    k_solve_multi<<<(unsigned)grid, kSolveWarps * 32, 0, s>>>(models, b, r0, r1, r2);
 }
 
 void launch_solve(const DevModel *models, const DevBatch &b, const DevResult &r, int mode, cudaStream_t s,

@@ -25,7 +25,7 @@ def declared_symbols():
 
 def test_header_symbols_exported(L):
     syms = declared_symbols()
-    assert len(syms) == 17, syms
+    assert len(syms) == 18, syms
     assert set(syms) == set(__import__("paper_2504_14611_b200").EXPORTED), syms
     for s in syms:
         assert hasattr(L, s), s
@@ -67,6 +67,9 @@ def test_argument_errors_without_gpu(L):
     assert L.jdob_solve_batch(None, 0, None, 0, None, None, 0, None) == B.EINVAL
     assert L.jdob_bruteforce(ms, 1, C.byref(b), 0, 0, 1, None, None, None, None, None, 0, None) == B.EINVAL
     # the entry points added in round 2 reject bad arguments on the host, before any CUDA call
+    r3 = (B.JResult * 3)()
+    assert L.jdob_solve_batch_modes(ms, 1, C.byref(b), r3, None, 0, None) == B.EINVAL
+    assert L.jdob_solve_batch_modes(None, 0, None, None, None, 0, None) == B.EINVAL
     sb = B.JSharedBatch()
     assert L.jdob_solve_shared_host(ms, 1, C.byref(sb), 0, C.byref(r), None, None, None) == B.EINVAL
     assert L.jdob_solve_shared_host(ms, 1, None, 0, C.byref(r), None, None, None) == B.EINVAL
