@@ -75,11 +75,13 @@ def fig4(J, out_dir):
     rows = []
     for beta, T, Ms, b in fig4_batches():
         db = J.DeviceBatch(b)
+        # J-DOB and its two variants from one pass (jdob_solve_batch_modes); LC is every result's E_lc
+        multi = J.solve_batch_modes(db, f_user=False)
+        torch.cuda.synchronize()
         res = {}
         for name, mode in METHODS:
-            r = J.solve_batch(db, mode=mode, f_user=False)
-            torch.cuda.synchronize()
-            res[name] = r["E"].cpu().numpy() / np.array(Ms)
+            r = multi[J.MODE_FULL] if mode == J.MODE_LC else multi[mode]
+            res[name] = (r["E_lc"] if mode == J.MODE_LC else r["E"]).cpu().numpy() / np.array(Ms)
         for q, M in enumerate(Ms):
             row = dict(beta=beta, T_ms=T * 1e3, M=M)
             for name, _ in METHODS:

@@ -26,11 +26,16 @@ def J():
 def test_fig4_instances_vs_oracle(J):
     for beta, T, Ms, b in F.fig4_batches():
         db = J.DeviceBatch(b)
+        multi = {m: to_np(r) for m, r in J.solve_batch_modes(db, f_user=False).items()}  # the sweep's call
         for name, mode in F.METHODS:
             gpu = to_np(J.solve_batch(db, mode=mode, f_user=False))
             orc = O.solve_batch(b, mode=mode)
             for f in ("E", "E_lc", "t_free_next", "f_e", "n_tilde", "j", "status"):
                 assert_bits_equal(gpu[f], orc[f], f"fig4 beta={beta} {name} {f}")
+                if mode != J.MODE_LC:
+                    assert_bits_equal(multi[mode][f], orc[f], f"fig4 one-pass beta={beta} {name} {f}")
+            if mode == J.MODE_LC:
+                assert_bits_equal(multi[J.MODE_FULL]["E_lc"], orc["E"], f"fig4 one-pass LC beta={beta}")
 
 
 def test_fig5_grouped_instances_vs_oracle(J):

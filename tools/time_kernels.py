@@ -86,6 +86,29 @@ def t_eval(cfg, n):
     return {"cfg": cfg + "_eval", "n": n, "ms": ms, "inst_per_s": n / ms * 1e3}
 
 
+def t_modes(cfg, n):
+    """jdob_solve_batch_modes (J-DOB + its two variants in one pass) against the three separate calls."""
+    b = G.config_batch(cfg, n_inst=n)
+    db = J.DeviceBatch(b)
+    J.solve_batch_modes(db, f_user=False)
+    torch.cuda.synchronize()
+    out = {}
+    for name, fn in (("one_pass", lambda: J.solve_batch_modes(db, f_user=False)),
+                     ("three_calls", lambda: [J.solve_batch(db, mode=m, f_user=False) for m in (0, 2, 3)])):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(5):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            fn()
+            e.record()
+            torch.cuda.synchronize()
+            ts.append(s.elapsed_time(e))
+        out[name] = float(np.median(ts))
+    return {"cfg": cfg + "_modes", "n": n, "ms_one_pass": out["one_pass"], "ms_three_calls": out["three_calls"]}
+
+
 def t_bf(frac):
     b = G.config_batch("c4")
     db = J.DeviceBatch(b)
@@ -123,7 +146,8 @@ if __name__ == "__main__":
     todo = {"c2": lambda: t_solve("c2", 1 << 20), "c3": lambda: t_solve("c3", 100_000),
             "c5": lambda: t_solve("c5", 1_000_000), "bf": lambda: t_bf(0.25),
             "og": lambda: t_grouped("c3", 100_000), "eval": lambda: t_eval("c2", 1 << 20),
-            "stats": lambda: t_stats("c2", 1 << 20), "e2e": lambda: t_e2e("c2", 1 << 20), "e2es": lambda: t_e2e("c2", 1 << 20, True), "c2lc": lambda: t_solve("c2", 1 << 20, J.MODE_LC),
+            "stats": lambda: t_stats("c2", 1 << 20), "modes2": lambda: t_modes("c2", 1 << 20),
+            "modes3": lambda: t_modes("c3", 100_000), "e2e": lambda: t_e2e("c2", 1 << 20), "e2es": lambda: t_e2e("c2", 1 << 20, True), "c2lc": lambda: t_solve("c2", 1 << 20, J.MODE_LC),
             "c2noedge": lambda: t_solve("c2", 1 << 20, J.MODE_NO_EDGE_DVFS), "stats5": lambda: t_stats("c5", 1_000_000)}
     for r in (todo[w]() for w in which):
         r["lib"] = os.path.basename(lib)
