@@ -481,6 +481,7 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
         unsigned long long done = 0ull;  // n~ swept in this pass (best-first order)
 #endif
         for (int nt = -1;;) {
+            int kkn = kk;  // this n~'s grid length (MULTI: 1 when only the no-edge-DVFS mode needs the n~)
             if (!prune) {
                 if (++nt >= N || (mode == JDOB_MODE_BINARY && nt != 0)) break;
             } else {
@@ -526,6 +527,12 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                 const int nx = __ffsll((long long)cand) - 1;
                 pruned |= nx > nt + 1;
                 nt = nx;
+                if (MULTI && !(s.lb[nt] < bEw) && kk > 1) {
+                    // the full mode skips this n~ (its configurations cannot win there); the no-edge-DVFS
+                    // mode needs its j = 0 only.  A partial sweep counts as pruning for the R8 re-sweep.
+                    kkn = 1;
+                    pruned = true;
+                }
 #ifndef JDOB_NO_TIGHT_LB
                 // (not in the equal-deadline kernel: there it removes 28 % of C2's set-ups, mostly of the
                 // instances LC wins, but its code costs that kernel 2 % more than the set-ups it saves)
@@ -566,9 +573,9 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
             // two grid points per lane (j0 + lane and j0 + 32 + lane): the two energy chains are
             // independent, which doubles the instruction-level parallelism of the sweep and lets both
             // share each user's shared-memory loads
-            for (int j0 = 0; j0 < kk; j0 += 64) {
+            for (int j0 = 0; j0 < kkn; j0 += 64) {
                 const int jA = j0 + lane, jB = jA + 32;
-                const bool vA = jA < kk, vB = jB < kk;
+                const bool vA = jA < kkn, vB = jB < kkn;
                 const double feA = grid_fe(fe_max, rho, jA), feB = grid_fe(fe_max, rho, jB);
                 // p(j): first sorted position >= i^ with !(f_e < th_i)  (M if the set is empty)
                 int loA = ihat, hiA = M, loB = ihat, hiB = M;
@@ -586,7 +593,7 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                 // Alg. 2's break: the first j with an empty set ends this n~'s sweep
                 const unsigned empA = __ballot_sync(0xffffffffu, vA && pA == M);
                 const unsigned empB = __ballot_sync(0xffffffffu, vB && pB == M);
-                const int jb = empA ? j0 + (__ffs(empA) - 1) : (empB ? j0 + 32 + (__ffs(empB) - 1) : kk);
+                const int jb = empA ? j0 + (__ffs(empA) - 1) : (empB ? j0 + 32 + (__ffs(empB) - 1) : kkn);
                 const bool emp = (empA | empB) != 0u;
                 if (emp && nt < aN) {  // the first all-local evaluation in the literal (n~, j) order
                     aN = nt;
