@@ -231,6 +231,25 @@ def test_configs_full_size_sampled(J, cfg, n):
         assert rel_close(st_g[:, f], st_o[:, f], 1e-9), f
 
 
+def test_c2_full_batch_vs_oracle(J):
+    """The bench workload C2 at its full size (2^20 instances: the equal-deadline kernel) against the
+    oracle on every instance (the bench's cpu_baseline leg does the same at run time)."""
+    b = g.config_batch("c2", n_inst=1 << 20)
+    gpu = to_np(J.solve_batch(J.DeviceBatch(b)))
+    assert_solve_parity(gpu, O.solve_batch(b, threads=16))
+
+
+def test_c3_full_batch_vs_oracle(J):
+    """BASELINE config C3 at its full size (10^5 instances, M 4..20, differing deadlines: the
+    differing-deadline kernel with the batch-coupled bound) against the oracle on every instance."""
+    b = g.config_batch("c3", n_inst=100_000)
+    db = J.DeviceBatch(b)
+    gpu = to_np(J.solve_batch(db, partition=True))
+    orc = O.solve_batch(b, threads=16)
+    assert_solve_parity(gpu, orc)
+    assert_bits_equal(gpu["partition"], O.partition_from_plan(b, orc), "partition vs the oracle plan")
+
+
 def test_stats_small_exact(J):
     b = g.random_batch(seed=120, n_inst=3000, M_hi=32, N_hi=6, k_max=40)
     _, gpu = run(J, b, stats=True, n_buckets=32)
