@@ -828,6 +828,10 @@ static int solve_host_impl(const jdob_model *models, int32_t n_models, const jdo
     for (long long pos = 0; pos < n && nchunks < HostStreams::kMaxChunks;) {
         const long long rem = n - pos;
         long long sz = per;
+#ifdef JDOB_HOST_RAMP
+        // geometric ramp-up: the first solve starts after a small copy-in
+        if (nchunks < 8 && (JDOB_HOST_RAMP << nchunks) < per) sz = (long long)JDOB_HOST_RAMP << nchunks;
+#endif
 #ifndef JDOB_HOST_NO_TAIL
         if (rem <= 2 * per) sz = (rem / 2 > 16384) ? rem / 2 : 16384;
 #endif
