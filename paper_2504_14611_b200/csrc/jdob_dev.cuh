@@ -186,7 +186,8 @@ struct InstRegs {  // lane-resident user parameters (lane = user)
 constexpr unsigned kVBad = 1u, kVInfeas = 2u, kVRequire = 4u, kNotHomog = 8u, kNotUni = 16u, kNotSameT = 32u;
 
 // tmode (K1's kernel split by deadlines): 1 = return kStDefer when the users' deadlines differ, 2 = when
-// they are all equal; tested right after the loads, before the other checks (the next kernel decides).
+// they are all equal, 3 = always; tested right after the loads, before the other checks (the next
+// kernel decides).
 __device__ __forceinline__ int warp_validate_pre(const DevModel *models, const DevBatch &b, long long i, int lane,
                                                  long long off, long long M64, int mid, InstRegs &x, int &M,
                                                  long long &k, const DevModel *&mdp, GridKCache *kc = nullptr,
@@ -220,6 +221,7 @@ __device__ __forceinline__ int warp_validate_pre(const DevModel *models, const D
     if (*mdp->valid == 0) return JDOB_ST_BADMODEL;
     if (M64 < 1 || M64 > kMaxMLarge || M64 > mdp->B1 - 1) return JDOB_ST_BADPARAM;
     if (M64 > kMaxM) return kStDefer;  // more users than lanes: the block-per-instance path
+    if (tmode == 3) return kStDefer;  // (every instance to the next kernel)
     if (tmode) {
         const double T0 = __shfl_sync(0xffffffffu, x.T, 0);
         const bool differ = __any_sync(0xffffffffu, lane < M && !(x.T == T0));

@@ -247,8 +247,11 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
     const DevModel *mdp;
     InstRegs x;
     unsigned vflags = 0u;
+    // (without edge DVFS the differing-deadline kernel takes every uniform instance: its batch-coupled
+    // bound, exact at the one grid point f_e,max, skips the set-ups of the n~ that cannot beat LC)
+    const bool noedge = mode == JDOB_MODE_NO_EDGE_DVFS;
     const int st = warp_validate_pre(models, b, i, lane, off, M64, mid, x, M, k, mdp, &s.kc, &vflags,
-                                     UNI ? (TIGHT ? 2 : 1) : 0);
+                                     UNI ? (TIGHT ? (noedge ? 0 : 2) : (noedge ? 3 : 1)) : 0);
 #ifndef JDOB_L1PF
 #define JDOB_L1PF 1
 #endif
@@ -556,7 +559,11 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                         const double dg = L - gam;               // then no f_e passes the guard
                         const double r2 = (dg > 0.0) ? recip_rd(dg) : 0.0;
                         const double g = __dmul_rd(md.phi[nt * B1 + (M - lane)], (r2 > r1) ? r2 : r1);
-                        if (r1 != dinf()) lbp = S + __dmul_rd(__dmul_rd(md.psi[nt * B1 + (M - lane)], g), g);
+                        // g > f_e,max: no grid point reaches set start p.  With one grid point (no edge
+                        // DVFS) f_e = f_e,max exactly, and the edge term is the sweep's own expression
+                        const double psi = md.psi[nt * B1 + (M - lane)];
+                        if (r1 != dinf() && !(g > fe_max))
+                            lbp = S + ((kk == 1) ? (psi * fe_max) * fe_max : __dmul_rd(__dmul_rd(psi, g), g));
                     }
                     const double lt = warp_min_nonneg(lbp);
                     if (!(lt < bEw) || lt > E_lc) {
