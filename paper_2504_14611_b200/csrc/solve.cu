@@ -69,10 +69,12 @@ struct SolveSmem {
     double2 inv_key;                     // (f_e,max, rho) of the cached 1/f_e(j), j < inv_n
     int inv_n;
     GridKCache kc;                       // k of the last (f_e,min, f_e,max, rho)
-    double rinv[kMaxM];                  // RD(1 / R_m): lower-bound upload term
+    double rinv[kMaxM];                  // general kernel: RD(1 / R_m), lower-bound upload term; differing-
+                                         // deadline kernel: RD sum of e_loc over sorted positions >= p (p < M)
     double lbem[64];                     // per n~: the lower bound's member term (uniform users)
     int defer;                           // this warp deferred an instance (uniform kernels)
-    double pre[kMaxM + 1];               // equal-deadline kernel: P[p] = user-order sum of the first p e_loc
+    double pre[kMaxM + 1];               // equal-deadline kernel: P[p] = user-order sum of the first p e_loc;
+                                         // differing-deadline kernel: RD sum of e_loc over sorted positions < p
     double lb[64];                       // per n~: lower bound of every configuration's energy
     // uniform users (UNI kernel, N <= kUniCache): the per-n~ values that depend only on the model and
     // the users' shared (R, zeta, f_max, kappa, f_min, p_u) -- O/R, zeta v, gamma and the lower-bound
@@ -411,6 +413,25 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
         // RN sum of the minima is <= the sum of the terms, and the edge term (psi f_e) f_e >= 0.
         if (UNI) {  // every user has user 0's kappa, f_min, p_u and R: one bound term per n~
             const double rv = uc ? 0.0 : recip_rd(R0), kv = k0, fv = f00, pv = p0;  // user 0's values
+            const double cM = 1.0 - (double)(M - 1) * 0x1p-53;  // (1 - (M-1) u), exact
+            if (TIGHT) {
+                // differing deadlines: e_loc along the sorted positions (deadline ascending) is non-increasing
+                // (uniform users: f_loc = clamp(RN(zeta v_N / T)) is non-increasing in T, e_loc non-decreasing
+                // in f_loc, RN monotone); its RD prefix / suffix sums (each <= the exact sum) serve both bounds
+                if (lane < M) s.gam[lane] = s.et[s.order[lane]].x;  // (gamma is not stored for equal-gamma users)
+                __syncwarp();
+                if (lane < M) {
+                    double pr = 0.0, sf = 0.0;
+                    for (int t = 0; t < M; t++) {
+                        const double v = s.gam[t];
+                        if (t < lane) pr = __dadd_rd(pr, v);
+                        else sf = __dadd_rd(sf, v);
+                    }
+                    s.pre[lane] = pr;
+                    s.rinv[lane] = sf;
+                }
+                __syncwarp();
+            }
             for (int nt = lane; nt < N; nt += 32) {
                 const double em = uc ? s.uEM[nt] : (((kv * md.u[nt]) * fv) * fv) + __dmul_rd(md.O[nt], rv) * pv;
 #ifndef JDOB_NO_TIGHT_LB
@@ -425,10 +446,16 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                     const double el = s.et[0].x, t = (em < el) ? em : el;
                     S = __dmul_rd(__dmul_rd((double)M, t), 1.0 - (double)(M - 1) * 0x1p-53);
                 } else {
-                    for (int m = 0; m < M; m++) {
-                        const double el = s.et[m].x;
-                        S = S + ((em < el) ? em : el);
+                    // every term >= min(em, e_loc_m), whose exact sum is c em + (the e_loc of the sorted
+                    // positions >= c), c = #{q : e_loc(q) >= em} (a prefix: e_loc non-increasing); the RN sum of
+                    // non-negative terms in any order is >= (1 - (M-1) u) times the exact sum
+                    int lo = 0, hi = M;
+                    while (lo < hi) {
+                        const int mm = (lo + hi) >> 1;
+                        if (s.gam[mm] >= em) lo = mm + 1;
+                        else hi = mm;
                     }
+                    S = __dmul_rd(__dadd_rd(__dmul_rd((double)lo, em), (lo < M) ? s.rinv[lo] : 0.0), cM);
                 }
                 s.lb[nt] = S;
             }
@@ -552,8 +579,10 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                     const double gam = uc ? s.uG[nt] : dinf();  // gamma of n~ (cached for N <= 32)
                     double lbp = dinf();
                     if (lane < M) {
-                        double S = 0.0;
-                        for (int m = 0; m < M; m++) S = S + ((s.rank[m] >= lane) ? em : s.et[m].x);
+                        // the members' terms >= em, the others' are e_loc: the exact sum is >= the RD sum of
+                        // e_loc over the sorted positions < p plus (M - p) em; the RN sum >= (1 - (M-1) u) times it
+                        const double S = __dmul_rd(__dadd_rd(s.pre[lane], __dmul_rd((double)(M - lane), em)),
+                                                   1.0 - (double)(M - 1) * 0x1p-53);
                         const double L = s.Lg[lane].x;
                         const double r1 = recip_rd(L - t_free);  // L_p >= t_free (Require); +inf iff L_p = t_free:
                         const double dg = L - gam;               // then no f_e passes the guard

@@ -88,3 +88,34 @@ def test_recip_rd_algorithm_equals_rd():
         q = 1.0 / x
         alg = math.nextafter(q, -math.inf) if Fraction(q) * Fraction(x) - 1 > 0 else q
         assert alg == rd_recip(x), x
+
+
+def rd_add(a: float, b: float) -> float:
+    return rd(Fraction(a) + Fraction(b))
+
+
+@pytest.mark.parametrize("seed", [8, 9])
+def test_rn_sum_any_order_vs_rd_sum_bound(seed):
+    """The differing-deadline kernel's bounds: for non-negative terms t_m, the RN sum in any order is
+    >= RD(RD-sum of the terms (any order) x (1 - (M - 1) 2^-53)); also with some terms replaced by a
+    smaller common value em (RD(k em) + RD-sum of the rest)."""
+    rng = random.Random(seed)
+    pool = samples(rng, 300)
+    for _ in range(400):
+        M = rng.choice([1, 2, 5, 10, 17, 32])
+        ts = [rng.choice(pool) for _ in range(M)]
+        s = 0.0
+        for t in ts:
+            s = s + t
+        c = 1.0 - (M - 1) * 2.0 ** -53
+        r = 0.0
+        for t in sorted(ts):                  # a different order for the RD sum
+            r = rd_add(r, t)
+        assert rd_mul(r, c) <= s, (ts,)
+        k = rng.randrange(0, M + 1)          # the first k terms bounded below by em = min of them
+        em = min(ts[:k]) if k else 0.0
+        r2 = 0.0
+        for t in ts[k:]:
+            r2 = rd_add(r2, t)
+        lb = rd_mul(rd_add(rd_mul(float(k), em), r2), c)
+        assert lb <= s, (ts, k)
