@@ -11,9 +11,10 @@
  * Conventions for every entry point
  *  - Plain C types only.  Pointers documented "device" must point to device memory
  *    valid on the current device; "host" pointers to host memory.
- *  - The caller owns every buffer.  The library allocates nothing that outlives a
- *    call (jdob_solve_batch_host allocates and frees its own stream-ordered
- *    device buffers inside the call).
+ *  - The caller owns every buffer.  The library allocates no buffer that outlives a
+ *    call (the host calls allocate and free their own stream-ordered device buffers
+ *    inside the call, from a private pool that jdob_release_pool() trims); the host
+ *    calls' three streams and their events are created once per device and kept.
  *  - Return value: JDOB_OK, or a call-level error (JDOB_EINVAL bad shape/pointer/
  *    limit detectable on the host, JDOB_ECUDA a CUDA launch/runtime failure).  The
  *    message of the last error of the calling thread is jdob_last_error().
