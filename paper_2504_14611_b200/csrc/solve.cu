@@ -29,12 +29,21 @@
 // f_min, kappa and p_u agree ("uniform users": all of Table I's experiments, where
 // only deadlines differ), every member of a configuration has the same budget, f*
 // and offloader energy, which are then formed once per (n~, j) instead of per user.
-// Uniform-user instances are solved by their own kernel (UNI = true), whose smaller
-// code keeps instruction-cache stalls down; the general kernel takes the rest.
+// Uniform-user instances are solved by their own kernels (UNI = true), compiled once for
+// equal deadlines (TIGHT = false: every user identical; members are the users m >= p,
+// summed from a prefix of the e_loc terms) and once for differing deadlines (TIGHT =
+// true: with the batch-coupled bound below); each defers the other class, and the
+// general kernel takes the rest.  Small per-class code keeps K1 fast (it is sensitive
+// to its code size and register allocation); deferral flags let a kernel with nothing
+// deferred to it return at once.  k_solve_multi answers J-DOB, no edge DVFS and binary
+// J-DOB from one sweep (NEXT-2).
 //
 // Branch and bound over n~ (DESIGN.md §4 "n~ pruning"): a lower bound of every
 // configuration's energy is formed per n~ (lane = n~); n~ are visited in ascending
-// order and one whose bound is not below the best energy so far is skipped.  An
+// order and one whose bound is not below the best energy so far is skipped.  The
+// differing-deadline kernel also bounds each candidate n~ per set start p (members at
+// f_min, the edge energy at the lowest f_e that passes the guard and the membership
+// threshold of p) and skips it when that is not below the best or above E_LC.  An
 // exact tie of the best offloading energy with E_LC after pruning re-sweeps the
 // instance literally (the all-local key of a skipped n~ could matter, R8).
 #include "jdob_dev.cuh"
