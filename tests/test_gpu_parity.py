@@ -485,6 +485,34 @@ def test_bf_tight_deadlines(J):
                 assert int(I.item()) == Io
 
 
+def test_bf_random_scales_full_space(J):
+    """K2's exact vector bounds and margins over many random instances: M 2..8, N 1..4, heterogeneous
+    users, deadlines at every scale (beta in [0, 0.3] .. [5, 30]) and t_free > 0, each whole general space
+    against the literal oracle."""
+    rng = np.random.default_rng(77)
+    b = g.random_batch(seed=177, n_inst=150, M_lo=2, M_hi=8, N_lo=1, N_hi=4, k_max=20, tfree_frac=0.4)
+    scales = ((0.0, 0.3), (0.0, 1.0), (1.0, 5.0), (5.0, 30.0))
+    n_off = 0
+    for i in range(b.n_inst):
+        o0, o1 = int(b.user_off[i]), int(b.user_off[i + 1])
+        lat = g.min_local_latency(b.models[b.model_id[i]], b.zeta[o0:o1], b.f_max[o0:o1])
+        lo, hi = scales[i % len(scales)]
+        b.T[o0:o1] = (1.0 + rng.uniform(lo, hi, o1 - o0)) * lat
+        b.t_free[i] = rng.uniform(0.0, 0.5) * b.T[o0:o1].min() if rng.uniform() < 0.4 else 0.0
+    for i in range(b.n_inst):
+        bi = b.subset(i, i + 1)
+        size = O.bf_space_size(bi, 0)
+        if size > 3_000_000:
+            continue
+        E, I, S = J.bruteforce(J.DeviceBatch(bi), 0, 0, size)
+        Eo, Io, So = O.bf(bi, 0, 0, size)
+        assert int(S.item()) == So
+        assert_bits_equal(E.cpu().numpy(), np.array([Eo]), f"E {i}")
+        assert int(I.item()) == Io
+        n_off += int(Io >= 0)
+    assert n_off >= 50
+
+
 def test_bf_zero_energy_ties(J):
     """kappa = p_u = c = 0: every feasible candidate has E = 0, so the answer is the lowest feasible
     index -- the vector bound (LB = 0 >= best = 0) must never drop a lower-index tie."""
