@@ -91,6 +91,24 @@ def test_random_uniform_users(J, seed, M_hi, N_hi, k_max):
     assert_solve_parity(gpu, orc, counts=True)
 
 
+@pytest.mark.parametrize("M_lo,M_hi", [(17, 32), (32, 32)])
+def test_uniform_differing_deadlines_wide(J, M_lo, M_hi):
+    """The differing-deadline kernel's RD prefix/suffix sums and bounds up to M = 32 (no lane M there),
+    deadlines at every scale: pruned, executed-work and literal runs agree and match the oracle."""
+    b = uniformise(g.random_batch(seed=172 + M_lo, n_inst=600, M_lo=M_lo, M_hi=M_hi, N_lo=2, N_hi=14,
+                                  k_max=64), 172)
+    rng = np.random.default_rng(M_lo)
+    for i in range(b.n_inst):
+        o0, o1 = int(b.user_off[i]), int(b.user_off[i + 1])
+        lat = b.T[o0:o1].min()
+        if i % 3 == 0:
+            b.T[o0:o1] = lat * (1.0 + rng.uniform(0.0, 0.5, o1 - o0))
+        elif i % 3 == 1:
+            b.T[o0:o1] = lat * (1.0 + rng.uniform(5.0, 30.0, o1 - o0))
+    _, gpu = run(J, b)
+    assert_solve_parity(gpu, O.solve_batch(b, counts=True, threads=8), counts=True)
+
+
 def test_uniform_differing_deadlines_tight_bound(J):
     """The differing-deadline kernel's batch-coupled n~ bound: uniform users with tight
     and loose deadlines (LC wins often, so most n~ are skipped by the bound against E_LC), a user whose
