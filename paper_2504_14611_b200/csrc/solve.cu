@@ -571,6 +571,31 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                     // mode needs its j = 0 only.  A partial sweep counts as pruning for the R8 re-sweep.
                     kkn = 1;
                     pruned = true;
+                    if (homog) {
+                        // the j = 0 configurations' bound (f_e = f_e,max exactly): set start p needs f_e,max >=
+                        // th_p and >= the guard quotient (the set-up's own expressions), members' terms >=
+                        // their lower-bound terms, the edge term is the sweep's; skip the n~ when no such
+                        // configuration can beat the no-edge-DVFS best so far or LC (homogeneous users:
+                        // the ranks and suffix-min deadlines are the instance's)
+                        const double O_nt = md.O[nt], v_nt = md.v[nt], u_nt = md.u[nt];
+                        const double ORg = O_nt / s.R[0];
+                        const double gamg = ORg + div_z(s.z[0] * v_nt, s.f1[0]);
+                        double lbp = dinf();
+                        if (lane < M) {
+                            double S = 0.0;
+                            for (int m = 0; m < M; m++) {
+                                const double fm = s.fmm[m].x;
+                                const double emm = (((s.kap[m] * u_nt) * fm) * fm) + __dmul_rd(O_nt, s.rinv[m]) * s.pu[m];
+                                S = S + ((s.rank[m] >= lane) ? emm : s.et[m].x);
+                            }
+                            const double phi = md.phi[nt * B1 + (M - lane)], psi = md.psi[nt * B1 + (M - lane)];
+                            const double L = s.Lg[lane].x;
+                            const double thp = phi / (L - gamg), gp = phi / (L - t_free);
+                            if (!(fe_max < thp) && fe_max >= gp) lbp = S + (psi * fe_max) * fe_max;
+                        }
+                        const double lg = warp_min_nonneg(lbp);
+                        if (!(lg < bEwG) || lg > E_lc) continue;
+                    }
                 }
 #ifndef JDOB_NO_TIGHT_LB
                 // (not in the equal-deadline kernel: there it removes 28 % of C2's set-ups, mostly of the
