@@ -353,7 +353,10 @@ int jdob_solve_batch_modes(const jdob_model *models, int32_t n_models, const jdo
     DevModel *dm = nullptr;
     if ((rc = prepare_models(models, n_models, (char *)ws, &dm, s))) return rc;
     const DevBatch db = to_dev(b);
-    const DevResult r0 = dev_result(&out[0]), r1 = dev_result(&out[1]), r2 = dev_result(&out[2]);
+    DevResult r0 = dev_result(&out[0]);
+    const DevResult r1 = dev_result(&out[1]), r2 = dev_result(&out[2]);
+    r0.flags = (int *)((char *)ws + models_bytes(models, n_models) + stats_partial_bytes());  // deferral flags
+    cudaMemsetAsync(r0.flags, 0, kFlagBytes, s);
     launch_solve_multi(dm, db, r0, r1, r2, s, num_sms());
     bool wide = false;  // instances with 32 < M <= B_max: the block-per-instance kernel, once per mode
     for (int i = 0; i < n_models; i++) wide |= models[i].B_max > JDOB_MAX_M;

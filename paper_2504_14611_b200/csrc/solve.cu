@@ -444,7 +444,7 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
             for (int nt = lane; nt < N; nt += 32) {
                 const double em = uc ? s.uEM[nt] : (((kv * md.u[nt]) * fv) * fv) + __dmul_rd(md.O[nt], rv) * pv;
 #ifndef JDOB_NO_TIGHT_LB
-                if (TIGHT) s.lbem[nt] = em;
+                if (TIGHT || MULTI) s.lbem[nt] = em;
 #endif
                 double S = 0.0;
                 if (!TIGHT) {
@@ -584,8 +584,10 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                         if (lane < M) {
                             double S = 0.0;
                             for (int m = 0; m < M; m++) {
-                                const double fm = s.fmm[m].x;
-                                const double emm = (((s.kap[m] * u_nt) * fm) * fm) + __dmul_rd(O_nt, s.rinv[m]) * s.pu[m];
+                                const double fm = s.fmm[m].x;  // (uniform kernels: the per-n~ bound's member term)
+                                const double emm = UNI ? s.lbem[nt]
+                                                       : (((s.kap[m] * u_nt) * fm) * fm) +
+                                                             __dmul_rd(O_nt, s.rinv[m]) * s.pu[m];
                                 S = S + ((s.rank[m] >= lane) ? emm : s.et[m].x);
                             }
                             const double phi = md.phi[nt * B1 + (M - lane)], psi = md.psi[nt * B1 + (M - lane)];
@@ -629,7 +631,7 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                             lbp = S + ((kk == 1) ? (psi * fe_max) * fe_max : __dmul_rd(__dmul_rd(psi, g), g));
                     }
                     const double lt = warp_min_nonneg(lbp);
-                    if (!(lt < bEw) || lt > E_lc) {
+                    if (!(lt < (MULTI ? ((bEwG > bEw) ? bEwG : bEw) : bEw)) || lt > E_lc) {
                         pruned = true;
                         continue;
                     }
@@ -1056,10 +1058,10 @@ static void launch_pair(const DevModel *models, const DevBatch &b, const DevResu
     launch_solve_t<COUNTS, PRUNE, false, VERIFY, false>(models, b, r, mode, s, num_sms); // the rest
 }
 
-// NEXT-2 in one pass: JDOB_MODE_FULL into r0, JDOB_MODE_NO_EDGE_DVFS into r1, JDOB_MODE_BINARY into r2
-// (the general kernel over every instance, grid-stride with the heads loaded ahead; M > 32 is left to
-// k_solve_large, one launch per mode)
-__global__ void __launch_bounds__(kSolveWarps * 32, JDOB_SOLVE_MINB)
+// NEXT-2 in one pass (k_solve's structure with MULTI solve_instance): JDOB_MODE_FULL into r0,
+// JDOB_MODE_NO_EDGE_DVFS into r1, JDOB_MODE_BINARY into r2
+template <bool UNI, bool TIGHT>
+__global__ void __launch_bounds__(kSolveWarps * 32, UNI ? JDOB_SOLVE_MINB_U : JDOB_SOLVE_MINB)
     k_solve_multi(const DevModel *models, DevBatch b, DevResult r0, DevResult r1, DevResult r2) {
     __shared__ SolveSmem smem[kSolveWarps];
     const int lane = threadIdx.x & 31;
@@ -1076,25 +1078,64 @@ __global__ void __launch_bounds__(kSolveWarps * 32, JDOB_SOLVE_MINB)
     const DevResult rx[2] = {r1, r2};
     const long long gw = (long long)blockIdx.x * kSolveWarps + (threadIdx.x >> 5);
     const long long nw = (long long)gridDim.x * kSolveWarps;
-    for (long long i = gw; i < b.n_inst; i += nw) {
-        const long long o = b.user_off[i];
-        const long long m = (b.user_end ? b.user_end[i] : b.user_off[i + 1]) - o;
-        solve_instance<false, true, false, false, false, true>(i, o, m, b.model_id[i], models, b, r0, JDOB_MODE_FULL,
-                                                               s, lane, 0, 0, rx);
+    if (UNI && !TIGHT) {  // every instance (the equal-deadline kernel defers the others)
+        for (long long i = gw; i < b.n_inst; i += nw) {
+            const long long o = b.user_off[i];
+            const long long m = (b.user_end ? b.user_end[i] : b.user_off[i + 1]) - o;
+            solve_instance<false, true, UNI, false, TIGHT, true>(i, o, m, b.model_id[i], models, b, r0,
+                                                                 JDOB_MODE_FULL, s, lane, 0, 0, rx);
+        }
+        __syncwarp();
+        if (lane == 0 && s.defer && r0.flags) r0.flags[0] = 1;
+    } else {  // the deferred ones, spread like a grid-stride loop (as k_solve)
+        if (r0.flags && r0.flags[UNI ? 0 : 1] == 0) return;
+        for (long long base = gw; base < b.n_inst; base += 32 * nw) {
+            const long long ii = base + lane * nw;
+            const bool in = ii < b.n_inst;
+            unsigned def = __ballot_sync(0xffffffffu, in && r0.status[ii] == kStDefer);
+            long long ho = 0, hm = 0;
+            int hid = 0;
+            if (def && in) {
+                ho = b.user_off[ii];
+                hm = (b.user_end ? b.user_end[ii] : b.user_off[ii + 1]) - ho;
+                hid = b.model_id[ii];
+            }
+            while (def) {
+                const int q = __ffs(def) - 1;
+                def &= def - 1u;
+                const long long o = __shfl_sync(0xffffffffu, ho, q), m = __shfl_sync(0xffffffffu, hm, q);
+                const int id = __shfl_sync(0xffffffffu, hid, q);
+                solve_instance<false, true, UNI, false, TIGHT, true>(base + q * nw, o, m, id, models, b, r0,
+                                                                     JDOB_MODE_FULL, s, lane, 0, 0, rx);
+            }
+        }
+        __syncwarp();
+        if (UNI && lane == 0 && s.defer && r0.flags) r0.flags[1] = 1;
     }
 }
 
-void launch_solve_multi(const DevModel *models, const DevBatch &b, const DevResult &r0, const DevResult &r1,
-                        const DevResult &r2, cudaStream_t s, int num_sms) {
-    if (b.n_inst <= 0) return;
+template <bool UNI, bool TIGHT>
+static void launch_multi_t(const DevModel *models, const DevBatch &b, const DevResult &r0, const DevResult &r1,
+                           const DevResult &r2, cudaStream_t s, int num_sms) {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve_multi, kSolveWarps * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve_multi<UNI, TIGHT>, kSolveWarps * 32, 0);
     if (per_sm < 1) per_sm = 1;
     const long long want = (b.n_inst + kSolveWarps - 1) / kSolveWarps;
     long long grid = (long long)num_sms * per_sm / grid_divisor();
     if (grid < 1) grid = 1;
     if (want < grid) grid = want;
-    k_solve_multi<<<(unsigned)grid, kSolveWarps * 32, 0, s>>>(models, b, r0, r1, r2);
+    k_solve_multi<UNI, TIGHT><<<(unsigned)grid, kSolveWarps * 32, 0, s>>>(models, b, r0, r1, r2);
+}
+
+// NEXT-2 in one pass through the same three-kernel chain as launch_solve (equal-deadline uniform,
+// differing-deadline uniform, general; r0.flags zeroed by the caller): J-DOB into r0, no edge DVFS into r1,
+// binary into r2; M > 32 is left to k_solve_large, one launch per mode
+void launch_solve_multi(const DevModel *models, const DevBatch &b, const DevResult &r0, const DevResult &r1,
+                        const DevResult &r2, cudaStream_t s, int num_sms) {
+    if (b.n_inst <= 0) return;
+    launch_multi_t<true, false>(models, b, r0, r1, r2, s, num_sms);
+    launch_multi_t<true, true>(models, b, r0, r1, r2, s, num_sms);
+    launch_multi_t<false, false>(models, b, r0, r1, r2, s, num_sms);
 }
 
 void launch_solve(const DevModel *models, const DevBatch &b, const DevResult &r, int mode, cudaStream_t s,
