@@ -583,12 +583,21 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                         double lbp = dinf();
                         if (lane < M) {
                             double S = 0.0;
-                            for (int m = 0; m < M; m++) {
-                                const double fm = s.fmm[m].x;  // (uniform kernels: the per-n~ bound's member term)
-                                const double emm = UNI ? s.lbem[nt]
-                                                       : (((s.kap[m] * u_nt) * fm) * fm) +
-                                                             __dmul_rd(O_nt, s.rinv[m]) * s.pu[m];
-                                S = S + ((s.rank[m] >= lane) ? emm : s.et[m].x);
+                            if (UNI) {
+                                // uniform users: the members' term bound em is common; the RD sum of the
+                                // non-members' e_loc (the sorted positions < p) plus (M - p) em, times
+                                // (1 - (M-1) u), bounds the RN sum (as the batch-coupled bound)
+                                const double em = s.lbem[nt];
+                                const double pel = TIGHT ? s.pre[lane] : __dmul_rd((double)lane, s.et[0].x);
+                                S = __dmul_rd(__dadd_rd(pel, __dmul_rd((double)(M - lane), em)),
+                                              1.0 - (double)(M - 1) * 0x1p-53);
+                            } else {
+                                for (int m = 0; m < M; m++) {
+                                    const double fm = s.fmm[m].x;
+                                    const double emm = (((s.kap[m] * u_nt) * fm) * fm) +
+                                                       __dmul_rd(O_nt, s.rinv[m]) * s.pu[m];
+                                    S = S + ((s.rank[m] >= lane) ? emm : s.et[m].x);
+                                }
                             }
                             const double phi = md.phi[nt * B1 + (M - lane)], psi = md.psi[nt * B1 + (M - lane)];
                             const double L = s.Lg[lane].x;
