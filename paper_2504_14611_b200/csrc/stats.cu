@@ -45,9 +45,9 @@ __device__ __forceinline__ int lane_slot(int f) {  // field -> per-lane slot, -1
 #endif
 constexpr int kBucketGroup = JDOB_STATS_GROUP;
 
-__global__ void __launch_bounds__(32) k_stats_partial(DevBatch b, DevResult r, double *partials, int n_buckets,
-                                                      long long n_total, long long begin, long long w0, int b_lo,
-                                                      int n_all) {
+__global__ void __launch_bounds__(32) k_stats_partial(DevBatch b, DevResult r, double *partials, double *stats,
+                                                      int n_buckets, long long n_total, long long begin, long long w0,
+                                                      int b_lo, int n_all) {
     // leaf w of the global tree = instances [n_total w / W, n_total (w + 1) / W); this block is w0 + blockIdx.x
     extern __shared__ double sh[];
     double *fs = sh;                                                        // [n_buckets][kLaneF][32]
@@ -118,24 +118,44 @@ __global__ void __launch_bounds__(32) k_stats_partial(DevBatch b, DevResult r, d
         }
     }
     __syncwarp();
-    double *dst = partials + (size_t)blockIdx.x * n_buckets * kStatsF;
+    // the exact fields go straight to the output: counts by integer-valued double atomics (exact in any
+    // order below 2^53), max r / min r by integer atomics on their bits (max stored as bits + 1, 0 = none,
+    // decoded by k_stats_max_decode); only the four floating-point sums go through the fixed tree
+    double *out = stats + (size_t)b_lo * kStatsF;
     for (int x = lane; x < n_buckets * kStatsF; x += 32) {
         const int f = x % kStatsF, bk = x / kStatsF;
-        const int slot = lane_slot(f);
-        double v;
         if (f == 3) {
-            v = cnt[bk * kStatsF + 3] ? __longlong_as_double((long long)mxb[bk]) : field_init(f);
+            if (cnt[bk * kStatsF + 3]) atomicMax((unsigned long long *)(out + x), mxb[bk] + 1ull);
         } else if (f == 4) {
-            v = __longlong_as_double((long long)mnb[bk]);
-        } else if (slot < 0) {
-            v = (f == 0 || f == 7 || f == 8 || (f >= 9 && f < 9 + 64)) ? (double)cnt[x] : field_init(f);
-        } else {
-            const double *q = fs + ((size_t)bk * kLaneF + slot) * 32;
-            v = field_init(f);
-            for (int l = 0; l < 32; l++) v = combine(f, v, q[l]);
+            if (mnb[bk] != 0x7ff0000000000000ull) atomicMin((unsigned long long *)(out + x), mnb[bk]);
+        } else if ((f == 0 || f == 7 || f == 8 || (f >= 9 && f < 9 + 64)) && cnt[x] != 0) {
+            atomicAdd(out + x, (double)cnt[x]);
         }
+    }
+    double *dst = partials + (size_t)blockIdx.x * n_buckets * kLaneF;
+    for (int x = lane; x < n_buckets * kLaneF; x += 32) {
+        const int slot = x % kLaneF, bk = x / kLaneF;
+        const int f = (slot == 0) ? 1 : (slot == 1) ? 2 : (slot == 2) ? 5 : 6;
+        const double *q = fs + ((size_t)bk * kLaneF + slot) * 32;
+        double v = field_init(f);
+        for (int l = 0; l < 32; l++) v = combine(f, v, q[l]);
         dst[x] = v;
     }
+}
+
+// The output's initial values (every field of every bucket): 0 for the sums and counts, the max slot's
+// "none" code 0, +inf for the min.
+__global__ void k_stats_init(double *stats, int n) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x < n) stats[x] = (x % kStatsF == 4) ? dinf() : 0.0;
+}
+
+// max r: the atomics' code (bits + 1, 0 = no r seen) back to the double (-inf when none, field_init)
+__global__ void k_stats_max_decode(double *stats, int n_buckets) {
+    const int bk = blockIdx.x * blockDim.x + threadIdx.x;
+    if (bk >= n_buckets) return;
+    const unsigned long long u = (unsigned long long)__double_as_longlong(stats[(size_t)bk * kStatsF + 3]);
+    stats[(size_t)bk * kStatsF + 3] = u ? __longlong_as_double((long long)(u - 1ull)) : -dinf();
 }
 
 // One warp per output element: the dyadic tree over the nl (a power of two) leaves.  Lane l folds
@@ -144,15 +164,16 @@ __global__ void __launch_bounds__(32) k_stats_partial(DevBatch b, DevResult r, d
 // bit for bit, so lane l and lane l ^ d hold the same subtree value at every level.
 __global__ void k_stats_final(const double *partials, int nl, int n_buckets, double *stats) {
     const int lane = threadIdx.x & 31;
-    const int x = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (x >= n_buckets * kStatsF) return;
-    const int f = x % kStatsF;
+    const int x = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // (bucket, floating-point slot)
+    if (x >= n_buckets * kLaneF) return;
+    const int slot = x % kLaneF, bk = x / kLaneF;
+    const int f = (slot == 0) ? 1 : (slot == 1) ? 2 : (slot == 2) ? 5 : 6;
     const int s = nl >= 32 ? nl / 32 : 1;
     double stack[11];
     double v = field_init(f);
     if (lane < nl) {
         for (int i = 0; i < s; i++) {
-            double y = partials[(size_t)(lane * s + i) * n_buckets * kStatsF + x];
+            double y = partials[(size_t)(lane * s + i) * n_buckets * kLaneF + x];
             int lev = 0;
             for (; (i >> lev) & 1; lev++) y = combine(f, stack[lev], y);
             stack[lev] = y;
@@ -161,7 +182,7 @@ __global__ void k_stats_final(const double *partials, int nl, int n_buckets, dou
     }
     const int lanes = nl >= 32 ? 32 : nl;
     for (int d = 1; d < lanes; d <<= 1) v = combine(f, v, __shfl_xor_sync(0xffffffffu, v, d));
-    if (lane == 0) stats[x] = v;
+    if (lane == 0) stats[(size_t)bk * kStatsF + f] = v;
 }
 
 bool launch_stats(const DevBatch &b, const DevResult &r, double *partials, double *stats, int n_buckets,
@@ -174,14 +195,18 @@ bool launch_stats(const DevBatch &b, const DevResult &r, double *partials, doubl
     cudaFuncSetAttribute(k_stats_partial, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)((size_t)kBucketGroup * (kLaneF * 32 * sizeof(double) + 2 * sizeof(long long) +
                                                        kStatsF * sizeof(int))));
+    const int n_out = n_buckets * kStatsF;
+    k_stats_init<<<(n_out + 255) / 256, 256, 0, s>>>(stats, n_out);
     for (int b_lo = 0; b_lo < n_buckets; b_lo += kBucketGroup) {  // partials reused group after group
         const int nb = (n_buckets - b_lo < kBucketGroup) ? n_buckets - b_lo : kBucketGroup;
         const size_t smem = (size_t)nb * kLaneF * 32 * sizeof(double) + 2 * (size_t)nb * sizeof(long long) +
                             (size_t)nb * kStatsF * sizeof(int);
-        k_stats_partial<<<(unsigned)nl, 32, smem, s>>>(b, r, partials, nb, n_total, begin, w0, b_lo, n_buckets);
-        const int warps = nb * kStatsF;
+        k_stats_partial<<<(unsigned)nl, 32, smem, s>>>(b, r, partials, stats, nb, n_total, begin, w0, b_lo,
+                                                       n_buckets);
+        const int warps = nb * kLaneF;
         k_stats_final<<<(warps * 32 + 255) / 256, 256, 0, s>>>(partials, (int)nl, nb, stats + (size_t)b_lo * kStatsF);
     }
+    k_stats_max_decode<<<(n_buckets + 255) / 256, 256, 0, s>>>(stats, n_buckets);
     return true;
 }
 
