@@ -646,7 +646,9 @@ def run_mine(args):
                                       "this launch (profiles/) over the live time"},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": (6 if fused else 7) * K,  # K0, K1 x3 (equal / differing deadlines, general), K4 x2, K3
+            # K0, K1 x3 (equal / differing deadlines, general), K4 (init, a partial + a final kernel per
+            # 16 buckets, the max decode), K3 unless fused
+            "gpu_launches": (1 + 3 + 2 + 2 * ((n_buckets + 15) // 16) + (0 if fused else 1)) * K,
             "clocks": clk,
             "bruteforce": bf,
             "plan_violations": viol,
