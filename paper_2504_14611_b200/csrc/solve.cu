@@ -238,13 +238,13 @@ __device__ __forceinline__ void write_local(const DevResult &r, long long i, lon
 // counters (r.counts), <true, true> = executed-work counters of the pruned sweep (r.work),
 // <false, true> = the product path.
 // UNI: the instance class this kernel solves.  true = uniform users (Table I; the other instances
-// are marked kStDefer), false = the rest (only instances marked kStDefer by the first kernel).
-// Two specialised kernels keep each one's code, and so its instruction-cache footprint, small.
+// are marked kStDefer), false = the rest (only instances marked kStDefer by the kernels before).
+// Specialised kernels keep each one's code, and so its instruction-cache footprint, small.
 // TIGHT (uniform kernels only): false = the kernel of equal deadlines (Table I's identical-deadline
 // setting; instances whose deadlines differ are marked kStDefer), true = the kernel of differing deadlines,
 // which adds the batch-coupled n~ bound (it prunes 43-66 % of the set-ups there, little with equal
-// deadlines, and its code costs the other kernel 6 % when compiled in).
-// MULTI (NEXT-2, general kernel only): one pass answers JDOB_MODE_FULL into r and, from the same sweep,
+// deadlines, and its code costs the other kernel 2-6 % when compiled in).
+// MULTI (NEXT-2, k_solve_multi): one pass answers JDOB_MODE_FULL into r and, from the same sweep,
 // JDOB_MODE_NO_EDGE_DVFS (the candidates at j = 0) and JDOB_MODE_BINARY (the candidates at n~ = 0) into
 // rx[0] and rx[1]; every mode's (E, n~, j) tie rule and all-local key are kept as in its own pass.
 template <bool COUNTS, bool PRUNE, bool UNI, bool VERIFY, bool TIGHT, bool MULTI = false>
