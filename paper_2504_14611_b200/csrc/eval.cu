@@ -255,6 +255,7 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval(const DevModel *models, D
             const long long w0 = lo & ~1ll;                                   // 16-byte aligned start
             const long long w1 = (hi - w0 <= kEvalWin) ? hi : w0 + kEvalWin;  // window end (exclusive)
             const long long nb = (w1 - w0) & ~1ll;                            // bulk part: 16-byte multiple
+            JDOB_CHECK(w0 >= 0 && w1 > w0 && w1 - w0 <= kEvalWin && (w0 & 1) == 0);
             if (bulk) {
                 if (tid == 0) {
                     const unsigned bytes = (unsigned)(nb * 8 * 7);
@@ -299,6 +300,7 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval(const DevModel *models, D
 #endif
             if (pending && off >= w0 && off + M64 <= w1) {
                 const long long e = off - w0;
+                JDOB_CHECK(e >= 0 && e + M64 <= kEvalStride && M64 >= 1 && M64 <= kMaxM);
                 const UserView v{ewin + e, ewin + kEvalStride + e, ewin + 2 * kEvalStride + e,
                                  ewin + 3 * kEvalStride + e, ewin + 4 * kEvalStride + e, ewin + 5 * kEvalStride + e,
                                  ewin + 6 * kEvalStride + e};

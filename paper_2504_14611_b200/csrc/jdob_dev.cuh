@@ -14,6 +14,20 @@
 
 namespace jdob {
 
+// Bounds checks of the shared-memory and workspace indexing, compiled in only for the checking build
+// (-DJDOB_BOUNDS: tools/bounds_check.sh runs the GPU suite on it; compute-sanitizer is closed on the
+// GPU pool).  A failed check traps the kernel, which fails the calling test.
+#ifdef JDOB_BOUNDS
+#define JDOB_CHECK(cond) \
+    do {                 \
+        if (!(cond)) __trap(); \
+    } while (0)
+#else
+#define JDOB_CHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
+
 constexpr int kMaxM = JDOB_MAX_M;
 constexpr int kMaxMLarge = JDOB_MAX_M_LARGE;
 constexpr int kStDefer = -1;  // internal status: M > 32, handled by k_solve_large

@@ -427,6 +427,7 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                 // differing deadlines: e_loc along the sorted positions (deadline ascending) is non-increasing
                 // (uniform users: f_loc = clamp(RN(zeta v_N / T)) is non-increasing in T, e_loc non-decreasing
                 // in f_loc, RN monotone); its RD prefix / suffix sums (each <= the exact sum) serve both bounds
+                JDOB_CHECK(M >= 1 && M <= kMaxM);
                 if (lane < M) s.gam[lane] = s.et[s.order[lane]].x;  // (gamma is not stored for equal-gamma users)
                 __syncwarp();
                 if (lane < M) {
@@ -464,6 +465,7 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                         if (s.gam[mm] >= em) lo = mm + 1;
                         else hi = mm;
                     }
+                    JDOB_CHECK(lo >= 0 && lo <= M && nt < 64);
                     S = __dmul_rd(__dadd_rd(__dmul_rd((double)lo, em), (lo < M) ? s.rinv[lo] : 0.0), cM);
                 }
                 s.lb[nt] = S;
@@ -731,6 +733,7 @@ __device__ __forceinline__ void solve_instance(long long i, long long off, long 
                         // equal deadlines: the ranks are the user indices, so the members are the users
                         // m >= p (thresholds non-increasing from i^) and the user-order sum is the prefix
                         // P[p] of the e_loc terms (formed with E_LC) followed by M - p member terms
+                        JDOB_CHECK(pA >= 0 && pA <= M && pB >= 0 && pB <= M);
                         EA = s.pre[pA];
                         EB = s.pre[pB];
                         for (int m = (pA < pB) ? pA : pB; m < M; m++) {

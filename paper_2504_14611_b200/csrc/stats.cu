@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(32) k_stats_partial(DevBatch b, DevResult r, d
         for (int q = 0; q < U; q++) {
             const int bk = bq[q];
             if (bk < 0 || bk >= n_buckets) continue;  // also: beyond the range
+            JDOB_CHECK(bk < kBucketGroup);
             int *c = cnt + bk * kStatsF;
             if (sq[q] != JDOB_ST_OK) {
                 atomicAdd(c + 8, 1);
