@@ -63,7 +63,7 @@ static int check_models(const jdob_model *models, int32_t n_models) {
     return JDOB_OK;
 }
 
-constexpr size_t kFlagBytes = 2 * sizeof(int);  // K1's deferral flags, after the statistics partials
+constexpr size_t kFlagBytes = 8 * sizeof(int);  // K1's deferral flags [2] and its three kernels' work counters
 
 static size_t models_bytes(const jdob_model *models, int32_t n_models) {
     size_t s = al((size_t)n_models * sizeof(DevModel));

@@ -66,8 +66,9 @@ struct DevResult {
     int *partition = nullptr;   // per user n~* or N, or NULL
     long long *work = nullptr;  // [4 n_inst] executed-work counters of the pruned sweep, or NULL
     unsigned *viol = nullptr;   // [n_inst] the plan re-verified in the epilogue (jdob_eval bits), or NULL
-    int *flags = nullptr;       // [2] zeroed before K1: set when the equal- / differing-deadline kernel
-                                // defers an instance (a later kernel with nothing to do returns at once)
+    int *flags = nullptr;       // [8] zeroed before K1: [0..1] set when the equal- / differing-deadline kernel
+                                // defers an instance (a later kernel with nothing to do returns at once);
+                                // [2..7] three 64-bit work counters (dynamic hand-out of instance chunks)
     double slack = 0.0;
 };
 

@@ -1004,6 +1004,42 @@ __global__ void __launch_bounds__(kSolveWarps * 32, UNI ? JDOB_SOLVE_MINB_U : JD
         };
         long long o = 0, e = 0;
         int id = 0;
+#ifndef JDOB_STRIDED
+        // dynamic hand-out of 32-instance chunks from a counter in the workspace (the warps that drew
+        // expensive instances take fewer chunks: no tail of a few late warps); the next chunk is drawn
+        // when the current one starts
+        // (a batch with fewer than 8 chunks per warp keeps the static grid-stride order: chunks of one
+        // instance, gw, gw + nw, ...; the chunks' granularity would otherwise leave a tail)
+        const bool dyn = r.flags && b.n_inst >= 8ll * 32 * nw;
+        unsigned long long *ctr = dyn ? (unsigned long long *)(r.flags + 2) : nullptr;
+        const int csz = dyn ? 32 : 1;
+        long long kst = 0;
+        auto grab = [&]() -> long long {
+            if (!ctr) return gw + nw * (kst++);
+            long long v = 0;
+            if (lane == 0) v = (long long)atomicAdd(ctr, 1ull);
+            return __shfl_sync(0xffffffffu, v, 0);
+        };
+        long long nchunk = grab();
+        long long i = nchunk * csz;
+        nchunk = grab();
+        int q = 0;
+        head(i, o, e, id);
+        while (i < b.n_inst) {
+            const long long co = o, cm = e - o;
+            const int cid = id;
+            const long long inext = (q < csz - 1) ? i + 1 : nchunk * csz;
+            head(inext, o, e, id);
+            solve_instance<COUNTS, PRUNE, UNI, VERIFY, TIGHT>(i, co, cm, cid, models, b, r, mode, s, lane, o, e);
+            if (q < csz - 1) {
+                q++;
+            } else {
+                q = 0;
+                nchunk = grab();
+            }
+            i = inext;
+        }
+#else
         head(gw, o, e, id);
         for (long long i = gw; i < b.n_inst; i += nw) {
             const long long co = o, cm = e - o;
@@ -1013,16 +1049,32 @@ __global__ void __launch_bounds__(kSolveWarps * 32, UNI ? JDOB_SOLVE_MINB_U : JD
             // the prefetch then touches again -- valid addresses, no select waiting on the loads)
             solve_instance<COUNTS, PRUNE, UNI, VERIFY, TIGHT>(i, co, cm, cid, models, b, r, mode, s, lane, o, e);
         }
+#endif
         __syncwarp();
         if (lane == 0 && s.defer && r.flags) r.flags[0] = 1;  // one store per warp, not per deferral
     } else {
         // nothing deferred by the kernel before: no instance to visit
         if (r.flags && r.flags[UNI ? 0 : 1] == 0) return;
-        // only the instances the kernels before left (kStDefer), 32 statuses per load; lane l of round t
-        // looks at instance gw + (32 t + l) nw, so the deferred instances are spread over the warps as in a
-        // grid-stride loop (consecutive groups of 32 per warp left most warps idle when few groups exist)
-        for (long long base = gw; base < b.n_inst; base += 32 * nw) {
-            const long long ii = base + lane * nw;
+        // only the instances the kernels before left (kStDefer), 32 statuses per load.  Groups of 32
+        // consecutive instances are handed out dynamically from a counter in the workspace (a warp that
+        // drew expensive instances takes fewer groups); without one, lane l of round t looks at instance
+        // gw + (32 t + l) nw, the deferred instances spread over the warps as in a grid-stride loop
+        // (dynamic groups only for a batch of at least 8 groups per warp, as in the kernel before)
+        unsigned long long *ctr = (r.flags && b.n_inst >= 8ll * 32 * nw) ? (unsigned long long *)(r.flags + (UNI ? 4 : 6))
+                                                                        : nullptr;
+        for (long long t = 0;; t++) {
+            long long base, step;
+            if (ctr) {
+                long long g = 0;
+                if (lane == 0) g = (long long)atomicAdd(ctr, 1ull);
+                base = __shfl_sync(0xffffffffu, g, 0) * 32;
+                step = 1;
+            } else {
+                base = gw + t * 32 * nw;
+                step = nw;
+            }
+            if (base >= b.n_inst) break;
+            const long long ii = base + lane * step;
             const bool in = ii < b.n_inst;
             unsigned def = __ballot_sync(0xffffffffu, in && r.status[ii] == kStDefer);
             // the heads (user_off, user count, model id) of the group's instances, one coalesced load each,
@@ -1039,7 +1091,7 @@ __global__ void __launch_bounds__(kSolveWarps * 32, UNI ? JDOB_SOLVE_MINB_U : JD
                 def &= def - 1u;
                 const long long o = __shfl_sync(0xffffffffu, ho, q), m = __shfl_sync(0xffffffffu, hm, q);
                 const int id = __shfl_sync(0xffffffffu, hid, q);
-                solve_instance<COUNTS, PRUNE, UNI, VERIFY, TIGHT>(base + q * nw, o, m, id, models, b, r, mode, s,
+                solve_instance<COUNTS, PRUNE, UNI, VERIFY, TIGHT>(base + q * step, o, m, id, models, b, r, mode, s,
                                                                   lane);
             }
         }
