@@ -1010,9 +1010,12 @@ __global__ void __launch_bounds__(kSolveWarps * 32, UNI ? JDOB_SOLVE_MINB_U : JD
         // when the current one starts
         // (a batch with fewer than 8 chunks per warp keeps the static grid-stride order: chunks of one
         // instance, gw, gw + nw, ...; the chunks' granularity would otherwise leave a tail)
-        const bool dyn = r.flags && b.n_inst >= 8ll * 32 * nw;
+#ifndef JDOB_CHUNK
+#define JDOB_CHUNK 8
+#endif
+        const bool dyn = r.flags && b.n_inst >= 8ll * JDOB_CHUNK * nw;
         unsigned long long *ctr = dyn ? (unsigned long long *)(r.flags + 2) : nullptr;
-        const int csz = dyn ? 32 : 1;
+        const int csz = dyn ? JDOB_CHUNK : 1;
         long long kst = 0;
         auto grab = [&]() -> long long {
             if (!ctr) return gw + nw * (kst++);
